@@ -1,0 +1,127 @@
+/*
+ * rstg.h -- C ABI of the B200-native rooted-spanning-tree engine.
+ *
+ * The drop-in boundary for the three RST strategies of arXiv 2603.11645.
+ * Plain pointers and sizes only; every entry point returns RSTG_OK (0) or
+ * an error code, with the message in rstg_last_error() (thread-local).
+ * Error messages reproduce the reference's exception texts where its tests
+ * pin them (SURVEY.md §8b "Error conventions").
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj/core):
+ *   rstg_graph_create*    Graph / build_csr          include/rst/graph.hpp:29-43,71
+ *   rstg_run              run_algorithm              include/rst/bench.hpp:36
+ *                         (bfs_rst bfs_rst.hpp:23, cc_euler_rst
+ *                          euler_rooting.hpp:69, pr_rst pr_rst.hpp:94-95)
+ *   rstg_cc_spanning_forest  cc_spanning_forest     include/rst/cc_forest.hpp:42
+ *   rstg_euler_root_forest   euler_root_forest      include/rst/euler_rooting.hpp:63-66
+ *   rstg_validate         validate_rooted_forest     include/rst/validate.hpp:46-47
+ *   rstg_k_*              hook_step / jump_to_convergence / list_rank
+ *                         (cc_forest.hpp:29-40, euler_rooting.hpp:52-53):
+ *                         kernel-level entry points for parity tests.
+ */
+#ifndef RSTG_H
+#define RSTG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSTG_OK 0
+#define RSTG_ERR_ARG 1   /* invalid argument (reference: std::invalid_argument) */
+#define RSTG_ERR_ALGO 2  /* algorithm failure (reference: std::runtime_error)   */
+#define RSTG_ERR_CUDA 3  /* CUDA runtime error / no device                      */
+
+/* AlgoKind order of bench.hpp:16 */
+#define RSTG_BFS 0
+#define RSTG_CC_EULER 1
+#define RSTG_PR_RST 2
+
+typedef struct rstg_graph rstg_graph;
+
+/* Mirrors StepReport (step_engine.hpp:21-25) plus device-side figures. */
+typedef struct {
+  int64_t steps;      /* device-wide barriers of the pipeline            */
+  int64_t work;       /* element updates                                 */
+  int64_t rounds;     /* hook / graft rounds (incl. the final empty one) */
+  int64_t launches;   /* kernels launched                                */
+  int64_t tree_edges; /* spanning-forest edges                           */
+  int64_t components; /* roots                                           */
+  int64_t levels;     /* BFS levels                                      */
+  double device_ms;   /* CUDA-event time of the device pipeline          */
+  double total_ms;    /* wall time of the call incl. host<->device copies */
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+} rstg_stats;
+
+const char* rstg_last_error(void);
+int rstg_device_count(int* count);
+
+/* Graph from the reference's host arrays (int64): offsets[n+1],
+ * neighbors[2m], edge_origin[2m], edges_uv[2m] (u,v interleaved, normalized:
+ * u < v, lexicographically sorted, unique). CSR arrays may be NULL: the CSR
+ * is then built on the device from edges_uv. */
+int rstg_graph_create(const int64_t* offsets, const int64_t* neighbors,
+                      const int64_t* edge_origin, const int64_t* edges_uv, int64_t n,
+                      int64_t m, int device, rstg_graph** out);
+/* Graph from device-resident int32 arrays (copied into the handle).
+ * d_offsets/d_nbrs/d_arc_edge may be NULL (CSR built on the device). */
+int rstg_graph_create_device(const int32_t* d_edges_uv, const uint32_t* d_offsets,
+                             const int32_t* d_nbrs, const uint32_t* d_arc_edge, int64_t n,
+                             int64_t m, int device, rstg_graph** out);
+/* Device generator: "path:N", "star:N", "grid:R:C", "road:R[:p]",
+ * "kron:SCALE[:EF]" (SURVEY.md Appendix B shapes; identical edge lists to
+ * the host generators). */
+int rstg_graph_generate(const char* spec, int device, rstg_graph** out);
+int rstg_graph_info(const rstg_graph* g, int64_t* n, int64_t* m);
+/* Copies the device edge list out as int64 pairs (2m). */
+int rstg_graph_edges(rstg_graph* g, int64_t* edges_uv);
+int rstg_graph_destroy(rstg_graph* g);
+/* Launch on a caller stream (cudaStream_t) instead of the handle's own. */
+int rstg_set_stream(rstg_graph* g, void* cuda_stream);
+/* Per-phase CUDA-event timing (read with rstg_phase_times). */
+int rstg_set_timing(rstg_graph* g, int enabled);
+/* JSON object {"phase": ms, ...} of the last run. */
+int rstg_phase_times(rstg_graph* g, char* buf, int64_t cap);
+
+/* run_algorithm (bench.cpp:38-54): parent_out[n] (P[r] = r); levels_out[n]
+ * for BFS (nullable); roots_out (capacity n, nullable) in the reference's
+ * order: BFS discovery order, cc-euler / pr-rst ascending. */
+int rstg_run(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, int64_t* parent_out,
+             int64_t* levels_out, int64_t* roots_out, int64_t* num_roots, rstg_stats* stats);
+/* Device-resident variant: int32 parent (and levels, nullable) on device. */
+int rstg_run_device(rstg_graph* g, int algo, int64_t root, int64_t jump_batch,
+                    int32_t* d_parent, int32_t* d_levels, rstg_stats* stats);
+
+/* cc_spanning_forest: labels[n] = converged reps, tree_edges ascending ids. */
+int rstg_cc_spanning_forest(rstg_graph* g, int64_t* labels_out, int64_t* tree_edges_out,
+                            int64_t* num_tree_edges, rstg_stats* stats);
+
+/* euler_root_forest(n, tree_edges, labels, designated_root) on `device`.
+ * tree_uv: T edges as (u,v) pairs; designated_root -1 = none. */
+int rstg_euler_root_forest(int64_t n, const int64_t* tree_uv, int64_t T, const int64_t* labels,
+                           int64_t nlabels, int64_t designated_root, int device,
+                           int64_t* parent_out, int64_t* roots_out, int64_t* num_roots);
+
+/* validate_rooted_forest on the device. *valid = 1/0; *code = 0 or
+ * 1 range, 2 non-edge, 3 cycle, 4 roots per component, 5 cross-component,
+ * 6 required root; *bad_vertex = first offender. */
+int rstg_validate(rstg_graph* g, const int64_t* parent, int64_t required_root, int* valid,
+                  int* code, int64_t* bad_vertex);
+
+/* ---- kernel-level entry points (device kernels, host buffers) ---- */
+/* hook_step (cc_forest.cpp:8-48): slot[n] uses INT64_MAX as empty.
+ * *applied = 1 if any hook was applied. */
+int rstg_k_hook_step(int64_t n, int64_t m, const int64_t* edges_uv, int mode, int64_t* rep,
+                     uint8_t* tree_flag, int64_t* slot, int* applied);
+/* jump_to_convergence fixed point (cc_forest.cpp:50-71). */
+int rstg_k_jump(int64_t n, int64_t* rep);
+/* list ranking of NONE(-1)-terminated lists (euler_rooting.cpp:104-153):
+ * rank = distance from the list head. */
+int rstg_k_list_rank(int64_t E, const int64_t* succ, int64_t* rank);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSTG_H */

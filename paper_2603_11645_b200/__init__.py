@@ -1,0 +1,259 @@
+"""B200-native rooted-spanning-tree engine (arXiv 2603.11645 strategies).
+
+Python binding over the C ABI in ``include/rstg.h`` (``librstg.so``, built
+in-tree by ``make``). The reference is C++; its drop-in host API is the C++
+``rst::`` mirror in ``host/`` (``librst_b200.so``). This module exists for
+the tests and ``bench.py``: the same entry points, numpy in/out.
+
+There is no CPU fallback: if the CUDA library cannot be loaded, or no GPU is
+visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librstg.so")
+
+BFS, CC_EULER, PR_RST = 0, 1, 2  # bench.hpp:16 AlgoKind
+ALGOS = {"bfs": BFS, "cc-euler": CC_EULER, "pr-rst": PR_RST}
+
+RSTG_OK, RSTG_ERR_ARG, RSTG_ERR_ALGO, RSTG_ERR_CUDA = 0, 1, 2, 3
+
+# Symbols include/rstg.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "rstg_last_error", "rstg_device_count", "rstg_graph_create", "rstg_graph_create_device",
+    "rstg_graph_generate", "rstg_graph_info", "rstg_graph_edges", "rstg_graph_destroy",
+    "rstg_set_stream", "rstg_set_timing", "rstg_phase_times", "rstg_run", "rstg_run_device",
+    "rstg_cc_spanning_forest", "rstg_euler_root_forest", "rstg_validate", "rstg_k_hook_step",
+    "rstg_k_jump", "rstg_k_list_rank",
+)
+
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+_vp = ctypes.c_void_p
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_int64), ("work", ctypes.c_int64), ("rounds", ctypes.c_int64),
+                ("launches", ctypes.c_int64), ("tree_edges", ctypes.c_int64),
+                ("components", ctypes.c_int64), ("levels", ctypes.c_int64),
+                ("device_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
+                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class RSTError(RuntimeError):
+    """Algorithm failure; message = the reference's std::runtime_error text."""
+
+
+class RSTArgError(ValueError):
+    """Invalid argument (reference: std::invalid_argument)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Loads librstg.so (raises if it is missing: no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run `make` (or __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        L.rstg_last_error.restype = ctypes.c_char_p
+        L.rstg_graph_create.argtypes = [_i64p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_int, ctypes.POINTER(_vp)]
+        L.rstg_graph_create_device.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64,
+                                               ctypes.c_int, ctypes.POINTER(_vp)]
+        L.rstg_graph_generate.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(_vp)]
+        L.rstg_graph_info.argtypes = [_vp, _i64p, _i64p]
+        L.rstg_graph_edges.argtypes = [_vp, _i64p]
+        L.rstg_graph_destroy.argtypes = [_vp]
+        L.rstg_set_stream.argtypes = [_vp, _vp]
+        L.rstg_set_timing.argtypes = [_vp, ctypes.c_int]
+        L.rstg_phase_times.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int64]
+        L.rstg_run.argtypes = [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _i64p, _i64p,
+                               _i64p, _i64p, ctypes.POINTER(Stats)]
+        L.rstg_run_device.argtypes = [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _vp, _vp,
+                                      ctypes.POINTER(Stats)]
+        L.rstg_cc_spanning_forest.argtypes = [_vp, _i64p, _i64p, _i64p, ctypes.POINTER(Stats)]
+        L.rstg_euler_root_forest.argtypes = [ctypes.c_int64, _i64p, ctypes.c_int64, _i64p,
+                                             ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _i64p,
+                                             _i64p, _i64p]
+        L.rstg_validate.argtypes = [_vp, _i64p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int),
+                                    ctypes.POINTER(ctypes.c_int), _i64p]
+        L.rstg_k_hook_step.argtypes = [ctypes.c_int64, ctypes.c_int64, _i64p, ctypes.c_int, _i64p,
+                                       _u8p, _i64p, ctypes.POINTER(ctypes.c_int)]
+        L.rstg_k_jump.argtypes = [ctypes.c_int64, _i64p]
+        L.rstg_k_list_rank.argtypes = [ctypes.c_int64, _i64p, _i64p]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc == RSTG_OK:
+        return
+    msg = lib().rstg_last_error().decode()
+    if rc == RSTG_ERR_ALGO:
+        raise RSTError(msg)
+    if rc == RSTG_ERR_ARG:
+        raise RSTArgError(msg)
+    raise CudaError(msg)
+
+
+def _p64(a):
+    if a is None:
+        return None
+    assert a.dtype == np.int64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_i64p)
+
+
+def device_count() -> int:
+    c = ctypes.c_int(0)
+    _check(lib().rstg_device_count(ctypes.byref(c)))
+    return c.value
+
+
+class DeviceGraph:
+    """Device-resident graph handle (rstg_graph)."""
+
+    def __init__(self, handle):
+        self._h = _vp(handle) if not isinstance(handle, _vp) else handle
+        n, m = ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(lib().rstg_graph_info(self._h, ctypes.byref(n), ctypes.byref(m)))
+        self.n, self.m = n.value, m.value
+
+    # -- constructors --------------------------------------------------
+    @classmethod
+    def from_host(cls, n, edges_uv, offsets=None, neighbors=None, edge_origin=None, device=0):
+        """From the reference's host layout (int64). edges_uv: (m, 2)."""
+        e = np.ascontiguousarray(np.asarray(edges_uv, dtype=np.int64).reshape(-1, 2))
+        h = _vp()
+        _check(lib().rstg_graph_create(_p64(offsets), _p64(neighbors), _p64(edge_origin),
+                                       _p64(e), int(n), len(e), device, ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def generate(cls, spec: str, device=0):
+        h = _vp()
+        _check(lib().rstg_graph_generate(spec.encode(), device, ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_device(cls, n, d_edges, d_offsets=None, d_nbrs=None, d_arc_edge=None, m=None,
+                    device=0):
+        """From device pointers (ints) to int32 arrays."""
+        h = _vp()
+        _check(lib().rstg_graph_create_device(_vp(d_edges), _vp(d_offsets), _vp(d_nbrs),
+                                              _vp(d_arc_edge), int(n), int(m), device,
+                                              ctypes.byref(h)))
+        return cls(h)
+
+    def close(self):
+        if self._h:
+            lib().rstg_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- accessors -----------------------------------------------------
+    def edges(self) -> np.ndarray:
+        out = np.zeros(2 * self.m, np.int64)
+        _check(lib().rstg_graph_edges(self._h, _p64(out)))
+        return out.reshape(-1, 2)
+
+    def set_stream(self, stream_ptr: int):
+        _check(lib().rstg_set_stream(self._h, _vp(stream_ptr)))
+
+    def set_timing(self, on: bool):
+        _check(lib().rstg_set_timing(self._h, 1 if on else 0))
+
+    def phase_times(self) -> dict:
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(lib().rstg_phase_times(self._h, buf, len(buf)))
+        return json.loads(buf.value.decode() or "{}")
+
+    # -- algorithms ----------------------------------------------------
+    def run(self, algo, root=0, jump_batch=5, want_levels=None):
+        """run_algorithm: returns (parent, roots, levels|None, stats dict)."""
+        algo = ALGOS.get(algo, algo)
+        parent = np.zeros(self.n, np.int64)
+        levels = np.zeros(self.n, np.int64) if (algo == BFS and want_levels is not False) else None
+        roots = np.zeros(max(self.n, 1), np.int64)
+        nr = ctypes.c_int64(0)
+        st = Stats()
+        _check(lib().rstg_run(self._h, algo, int(root), int(jump_batch), _p64(parent),
+                              _p64(levels), _p64(roots), ctypes.byref(nr), ctypes.byref(st)))
+        return parent, roots[: nr.value].copy(), levels, st.as_dict()
+
+    def run_device(self, algo, root, d_parent: int, d_levels: int = 0, jump_batch=5):
+        algo = ALGOS.get(algo, algo)
+        st = Stats()
+        _check(lib().rstg_run_device(self._h, algo, int(root), int(jump_batch), _vp(d_parent),
+                                     _vp(d_levels or None), ctypes.byref(st)))
+        return st.as_dict()
+
+    def cc_spanning_forest(self):
+        labels = np.zeros(self.n, np.int64)
+        te = np.zeros(max(self.m, 1), np.int64)
+        T = ctypes.c_int64(0)
+        st = Stats()
+        _check(lib().rstg_cc_spanning_forest(self._h, _p64(labels), _p64(te), ctypes.byref(T),
+                                             ctypes.byref(st)))
+        return labels, te[: T.value].copy()
+
+    def validate(self, parent, required_root=-1):
+        p = np.ascontiguousarray(parent, dtype=np.int64)
+        valid, code, bad = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int64(0)
+        _check(lib().rstg_validate(self._h, _p64(p), int(required_root), ctypes.byref(valid),
+                                   ctypes.byref(code), ctypes.byref(bad)))
+        return bool(valid.value), code.value, bad.value
+
+
+def euler_root_forest(n, tree_edges, labels, designated_root=-1, device=0):
+    te = np.ascontiguousarray(np.asarray(tree_edges, dtype=np.int64).reshape(-1, 2))
+    lab = np.ascontiguousarray(np.asarray(labels, dtype=np.int64))
+    parent = np.zeros(max(n, 1), np.int64)
+    roots = np.zeros(max(n, 1), np.int64)
+    nr = ctypes.c_int64(0)
+    _check(lib().rstg_euler_root_forest(int(n), _p64(te), len(te), _p64(lab), len(lab),
+                                        int(designated_root), device, _p64(parent), _p64(roots),
+                                        ctypes.byref(nr)))
+    return parent[:n], roots[: nr.value].copy()
+
+
+def hook_step(n, edges_uv, mode, rep, tree_flag, slot):
+    """hook_step on device; rep/tree_flag/slot updated in place."""
+    e = np.ascontiguousarray(np.asarray(edges_uv, dtype=np.int64).reshape(-1, 2))
+    applied = ctypes.c_int(0)
+    _check(lib().rstg_k_hook_step(int(n), len(e), _p64(e), int(mode), _p64(rep),
+                                  tree_flag.ctypes.data_as(_u8p), _p64(slot),
+                                  ctypes.byref(applied)))
+    return bool(applied.value)
+
+
+def jump_to_convergence(rep):
+    _check(lib().rstg_k_jump(len(rep), _p64(rep)))
+
+
+def list_rank(succ):
+    s = np.ascontiguousarray(np.asarray(succ, dtype=np.int64))
+    rank = np.zeros(max(len(s), 1), np.int64)
+    _check(lib().rstg_k_list_rank(len(s), _p64(s), _p64(rank)))
+    return rank[: len(s)]

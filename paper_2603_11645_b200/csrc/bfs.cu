@@ -1,0 +1,331 @@
+// bfs.cu -- direction-optimising BFS baseline (bfs_rst, bfs_rst.cpp:10-77).
+//
+// Exact semantics of the reference's pull BFS:
+//   * parent[v] = the smallest-id neighbour one level up (bfs_rst.cpp:49-55,
+//     tests/test_bfs.cpp:55-62): top-down levels take atomicMin over every
+//     frontier neighbour; bottom-up levels scan the ascending neighbour
+//     list and stop at the first frontier hit.
+//   * other components are seeded at their smallest vertex, ascending
+//     (:58-73). Components are disjoint, so seeding them all at once in one
+//     multi-source BFS gives the same levels and parents; their smallest
+//     vertices come from the CC labels (only needed when the root's BFS did
+//     not reach every vertex).
+// One persistent cooperative kernel runs all levels with one grid barrier
+// per level (a high-diameter road mesh has ~13K levels; a host round trip
+// per level would dominate). Frontier queues live in HBM; the top-down
+// expansion maps a frontier vertex to a thread, a warp or the whole grid by
+// degree (thread/warp/grid gathering), and Beamer's heuristic switches to
+// bottom-up sweeps when the frontier's edges outweigh the unexplored edges.
+#include <cooperative_groups.h>
+
+#include "engine.hpp"
+#include "scan.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rstg {
+
+struct BfsCtl {
+  int qn[3];                 // light frontier sizes, rotating by level % 3
+  int hn[3];                 // heavy frontier sizes (degree >= kHeavyDeg)
+  unsigned long long mf[3];  // frontier out-degree sums (Beamer's m_f)
+  int levels;                // deepest level reached
+  int _pad[3];
+};
+
+constexpr int kWarpDeg = 32;
+constexpr uint32_t kHeavyDeg = 4096;
+
+struct BfsQueues {
+  int32_t* q[2];   // light frontier, by level parity
+  int32_t* hq[2];  // heavy frontier, by level parity
+};
+
+// Appends v (discovered at level d) to the next frontier; warp-aggregated.
+__device__ __forceinline__ void enqueue(int32_t v, uint32_t deg, int32_t* qx, int* qnx,
+                                        int32_t* hqx, int* hnx, unsigned long long* mfx) {
+  if (deg >= kHeavyDeg) {
+    qx = hqx;
+    qnx = hnx;
+  }
+  cg::coalesced_group g = cg::coalesced_threads();
+  // Lanes may target two different queues; split by queue.
+  const bool heavy = deg >= kHeavyDeg;
+  const unsigned hm = g.ballot(heavy);
+  const unsigned rank_mask = heavy ? hm : ~hm;
+  const int my_rank = __popc(rank_mask & ((1u << g.thread_rank()) - 1u));
+  const int cnt = __popc(rank_mask & ((g.size() == 32) ? 0xffffffffu : ((1u << g.size()) - 1u)));
+  const int leader = __ffs(rank_mask) - 1;
+  int base = 0;
+  if ((int)g.thread_rank() == leader) base = atomicAdd(qnx, cnt);
+  base = g.shfl(base, leader);
+  qx[base + my_rank] = v;
+  unsigned long long s = deg;
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long t = g.shfl_down(s, o);
+    if ((int)g.thread_rank() + o < (int)g.size()) s += t;
+  }
+  if (g.thread_rank() == 0) atomicAdd(mfx, s);
+}
+
+struct LevelIO {
+  int32_t* qx;
+  int* qnx;
+  int32_t* hqx;
+  int* hnx;
+  unsigned long long* mfx;
+};
+
+// Top-down edge u -> v at level d: smallest frontier neighbour wins.
+__device__ __forceinline__ void td_visit(int32_t u, int32_t v, int d, int32_t* level,
+                                         int32_t* parent, const uint32_t* offsets,
+                                         const LevelIO& io) {
+  const int lv = ld_cg(&level[v]);
+  if (lv != -1 && lv != d) return;
+  if (u < ld_cg(&parent[v])) atomicMin(&parent[v], u);
+  if (lv == -1 && atomicCAS(&level[v], -1, d) == -1)
+    enqueue(v, offsets[v + 1] - offsets[v], io.qx, io.qnx, io.hqx, io.hnx, io.mfx);
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_bfs(int64_t n, int64_t two_m, const uint32_t* __restrict__ offsets,
+          const int32_t* __restrict__ nbrs, int32_t* level, int32_t* parent, BfsQueues qs,
+          BfsCtl* ctl, int d_start, int max_levels) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_id = gtid >> 5, nwarps = gsize >> 5;
+  bool bottom_up = false;
+  unsigned long long visited_edges = 0;
+  for (int d = d_start; d < d_start + max_levels; ++d) {
+    const int ci = d % 3, ni = (d + 1) % 3, zi = (d + 2) % 3;
+    const int qn = *((volatile int*)&ctl->qn[ci]);
+    const int hn = *((volatile int*)&ctl->hn[ci]);
+    if (qn + hn == 0) break;
+    const unsigned long long mf = *((volatile unsigned long long*)&ctl->mf[ci]);
+    visited_edges += mf;
+    if (gtid == 0) {
+      ctl->levels = d - 1;
+      ctl->qn[zi] = 0;
+      ctl->hn[zi] = 0;
+      ctl->mf[zi] = 0;
+    }
+    // Beamer's direction heuristic (alpha = 14, beta = 24).
+    const unsigned long long mu = (unsigned long long)two_m - min(visited_edges, (unsigned long long)two_m);
+    const int64_t nf = (int64_t)qn + hn;
+    if (!bottom_up && mf * 14ull > mu && nf * 64 > n) bottom_up = true;
+    else if (bottom_up && nf * 24 < n) bottom_up = false;
+    const int32_t* qc = qs.q[d & 1];
+    const int32_t* hqc = qs.hq[d & 1];
+    const LevelIO io{qs.q[(d + 1) & 1], &ctl->qn[ni], qs.hq[(d + 1) & 1], &ctl->hn[ni],
+                     &ctl->mf[ni]};
+    if (!bottom_up) {
+      for (int64_t base = warp_id * 32; base < qn; base += nwarps * 32) {
+        const int64_t i = base + lane;
+        int32_t u = -1;
+        uint32_t b = 0, e = 0;
+        if (i < qn) {
+          u = qc[i];
+          b = offsets[u];
+          e = offsets[u + 1];
+        }
+        const uint32_t deg = e - b;
+        unsigned wmask = __ballot_sync(0xffffffffu, u >= 0 && deg >= (uint32_t)kWarpDeg);
+        while (wmask) {  // warp gathering
+          const int src = __ffs(wmask) - 1;
+          wmask &= wmask - 1;
+          const int32_t wu = __shfl_sync(0xffffffffu, u, src);
+          const uint32_t wb = __shfl_sync(0xffffffffu, b, src);
+          const uint32_t we = __shfl_sync(0xffffffffu, e, src);
+          for (uint32_t j = wb + lane; j < we; j += 32) td_visit(wu, nbrs[j], d, level, parent, offsets, io);
+        }
+        if (u >= 0 && deg < (uint32_t)kWarpDeg)  // thread gathering
+          for (uint32_t j = b; j < e; ++j) td_visit(u, nbrs[j], d, level, parent, offsets, io);
+      }
+      for (int h = 0; h < hn; ++h) {  // grid gathering for heavy vertices
+        const int32_t u = hqc[h];
+        const uint32_t b = offsets[u], e = offsets[u + 1];
+        for (int64_t j = b + gtid; j < e; j += gsize) td_visit(u, nbrs[j], d, level, parent, offsets, io);
+      }
+    } else {
+      // bottom-up: the first frontier hit in ascending neighbour order
+      for (int64_t v = gtid; v < n; v += gsize) {
+        if (level[v] != -1) continue;
+        const uint32_t b = offsets[v], e = offsets[v + 1];
+        for (uint32_t j = b; j < e; ++j) {
+          const int32_t u = nbrs[j];
+          if (ld_cg(&level[u]) == d - 1) {
+            parent[v] = u;
+            level[v] = d;
+            enqueue((int32_t)v, e - b, io.qx, io.qnx, io.hqx, io.hnx, io.mfx);
+            break;
+          }
+        }
+      }
+    }
+    grid.sync();
+  }
+}
+
+__global__ void k_bfs_init(int64_t n, int32_t* level, int32_t* parent) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    level[v] = -1;
+    parent[v] = 0x7fffffff;
+  }
+}
+__global__ void k_bfs_seed_one(int32_t r, int32_t* level, int32_t* parent, BfsQueues qs,
+                               const uint32_t* offsets, BfsCtl* ctl) {
+  // level 1 reads ctl index 1 and the odd-parity queues
+  const uint32_t deg = offsets[r + 1] - offsets[r];
+  level[r] = 0;
+  parent[r] = r;
+  if (deg >= kHeavyDeg) {
+    qs.hq[1][0] = r;
+    ctl->hn[1] = 1;
+  } else {
+    qs.q[1][0] = r;
+    ctl->qn[1] = 1;
+  }
+  ctl->mf[1] = deg;
+}
+
+namespace {
+// Unvisited vertices that are the smallest of their CC label.
+struct SeedFlag {
+  const int32_t* level;
+  const uint32_t* minv;
+  const int32_t* lab;
+  __device__ uint32_t operator()(int64_t v) const {
+    return (level[v] == -1 && minv[lab[v]] == (uint32_t)v) ? 1u : 0u;
+  }
+};
+struct EmitSeed {
+  int32_t* roots;  // roots[1 + p]
+  int32_t* q;
+  int32_t* level;
+  int32_t* parent;
+  __device__ void operator()(int64_t v, uint32_t p, uint32_t f) const {
+    if (!f) return;
+    roots[1 + p] = (int32_t)v;
+    q[p] = (int32_t)v;
+    level[v] = 0;
+    parent[v] = (int32_t)v;
+  }
+};
+}  // namespace
+
+void launch_min_vertex(Handle& h, const int32_t* lab, uint32_t* minv);
+
+__global__ void k_seed_ctl(BfsCtl* ctl, unsigned long long edges) { ctl->mf[1] = edges; }
+
+__global__ void k_sum_seed_degrees(const int32_t* q, int count, const uint32_t* offsets,
+                                   unsigned long long* out) {
+  unsigned long long s = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+    s += offsets[q[i] + 1] - offsets[q[i]];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+namespace {
+struct Unvisited {
+  const int32_t* level;
+  __device__ uint32_t operator()(int64_t v) const { return level[v] == -1 ? 1u : 0u; }
+};
+struct Nop {
+  __device__ void operator()(int64_t, uint32_t, uint32_t) const {}
+};
+}  // namespace
+
+static void run_levels(Handle& h, int32_t* level, int32_t* parent, BfsQueues qs, BfsCtl* ctl,
+                       int d_start) {
+  static int max_blocks = 0;
+  if (max_blocks == 0) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs, kBlock, 0));
+    max_blocks = per_sm * num_sms();
+  }
+  int64_t n = h.g.n, two_m = 2 * h.g.m;
+  const uint32_t* offsets = h.g.offsets;
+  const int32_t* nbrs = h.g.nbrs;
+  int max_levels = (int)std::min<int64_t>(n + 2, 0x7ffffff0);
+  void* args[] = {&n, &two_m, (void*)&offsets, (void*)&nbrs, &level, &parent, &qs, &ctl,
+                  &d_start, &max_levels};
+  CK(cudaLaunchCooperativeKernel((void*)k_bfs, dim3(max_blocks), dim3(kBlock), args, 0,
+                                 h.stream));
+  h.stats.launches += 1;
+}
+
+int64_t bfs_rst(Handle& h, int32_t root, int32_t* parent, int32_t* level, int32_t* roots) {
+  const int64_t n = h.g.n;
+  if (!h.g.has_csr()) throw ArgError("bfs needs the graph's CSR");
+  BfsQueues qs;
+  qs.q[0] = h.ws<int32_t>(WS_BFS_Q0, n + 1);
+  qs.q[1] = h.ws<int32_t>(WS_BFS_Q1, n + 1);
+  int32_t* hq = h.ws<int32_t>(WS_BFS_BITS, 2 * (n + 1));
+  qs.hq[0] = hq;
+  qs.hq[1] = hq + (n + 1);
+  BfsCtl* ctl = reinterpret_cast<BfsCtl*>(h.ws<char>(WS_BFS_CTRL, sizeof(BfsCtl) + 64));
+  const cudaStream_t s = h.stream;
+
+  h.timer.begin(s, "bfs.init");
+  CK(cudaMemsetAsync(ctl, 0, sizeof(BfsCtl), s));
+  k_bfs_init<<<grid_for(n), kBlock, 0, s>>>(n, level, parent);
+  k_bfs_seed_one<<<1, 1, 0, s>>>(root, level, parent, qs, h.g.offsets, ctl);
+  CK_LAUNCH();
+  h.stats.step(n);
+  h.timer.end(s);
+
+  h.timer.begin(s, "bfs.levels");
+  run_levels(h, level, parent, qs, ctl, 1);
+  h.timer.end(s);
+  CK(cudaMemcpyAsync(h.host_box, &ctl->levels, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int levels_root = *reinterpret_cast<int*>(h.host_box);
+  h.stats.levels = levels_root;
+  h.stats.steps += levels_root + 2;  // init + one barrier per level + the empty one
+
+  // Anything unreached? Seed every other component at its smallest vertex.
+  const uint32_t unvisited = scan_emit(h, n, Unvisited{level}, Nop{}, true);
+  *reinterpret_cast<int32_t*>(h.host_box) = root;
+  CK(cudaMemcpyAsync(roots, h.host_box, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (unvisited == 0) {
+    CK(cudaStreamSynchronize(s));
+    return 1;
+  }
+  h.timer.begin(s, "bfs.seed_components");
+  int32_t* lab = h.ws<int32_t>(WS_VAL_A, n);
+  cc_labels_fast(h, lab);
+  uint32_t* minv = h.ws<uint32_t>(WS_MINV, n);
+  CK(cudaMemsetAsync(minv, 0xFF, n * sizeof(uint32_t), s));
+  launch_min_vertex(h, lab, minv);
+  // The second phase starts again at level 1 (ctl index 1, odd queues).
+  // Seeds all enter the light queue; heavy seeds are then expanded by warp
+  // gathering, which is correct, just slower.
+  CK(cudaMemsetAsync(ctl, 0, sizeof(BfsCtl), s));
+  const uint32_t seeds =
+      scan_emit(h, n, SeedFlag{level, minv, lab}, EmitSeed{roots, qs.q[1], level, parent}, true);
+  unsigned long long* degsum = reinterpret_cast<unsigned long long*>(h.dev_box) + 30;
+  CK(cudaMemsetAsync(degsum, 0, sizeof(unsigned long long), s));
+  k_sum_seed_degrees<<<grid_for(seeds), kBlock, 0, s>>>(qs.q[1], (int)seeds, h.g.offsets, degsum);
+  CK_LAUNCH();
+  h.read_box(reinterpret_cast<int64_t*>(degsum), 1);
+  k_seed_ctl<<<1, 1, 0, s>>>(ctl, (unsigned long long)h.host_box[0]);
+  *reinterpret_cast<int*>(h.host_box) = (int)seeds;
+  CK(cudaMemcpyAsync(&ctl->qn[1], h.host_box, sizeof(int), cudaMemcpyHostToDevice, s));
+  CK_LAUNCH();
+  h.timer.end(s);
+  h.timer.begin(s, "bfs.levels2");
+  run_levels(h, level, parent, qs, ctl, 1);
+  h.timer.end(s);
+  CK(cudaMemcpyAsync(h.host_box, &ctl->levels, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int lv2 = *reinterpret_cast<int*>(h.host_box);
+  h.stats.levels = std::max<int64_t>(levels_root, lv2);
+  h.stats.steps += lv2 + 2;
+  return 1 + (int64_t)seeds;
+}
+
+}  // namespace rstg

@@ -1,0 +1,159 @@
+// engine.cu -- Handle, workspace, phase timer, shared small kernels.
+#include <algorithm>
+
+#include "engine.hpp"
+#include "scan.cuh"
+
+namespace rstg {
+
+int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return sms;
+}
+
+// ---------------------------------------------------------------- timer
+cudaEvent_t PhaseTimer::get() {
+  if (used_ == pool_.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    pool_.push_back(e);
+  }
+  return pool_[used_++];
+}
+void PhaseTimer::begin(cudaStream_t s, const char* name) {
+  if (!enabled) return;
+  Rec r{name, get(), nullptr};
+  CK(cudaEventRecord(r.a, s));
+  recs_.push_back(r);
+}
+void PhaseTimer::end(cudaStream_t s) {
+  if (!enabled || recs_.empty()) return;
+  Rec& r = recs_.back();
+  r.b = get();
+  CK(cudaEventRecord(r.b, s));
+}
+std::vector<std::pair<std::string, double>> PhaseTimer::collect() {
+  std::vector<std::pair<std::string, double>> out;
+  for (auto& r : recs_) {
+    if (!r.b) continue;
+    CK(cudaEventSynchronize(r.b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    out.emplace_back(r.name, (double)ms);
+  }
+  recs_.clear();
+  used_ = 0;
+  return out;
+}
+
+// --------------------------------------------------------------- handle
+Handle::Handle(int dev) : device(dev) {
+  CK(cudaSetDevice(dev));
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  CK(cudaMallocHost(&host_box, 64 * sizeof(int64_t)));
+  CK(cudaMalloc(&dev_box, 64 * sizeof(int64_t)));
+  bufs_.assign(WS_COUNT, {nullptr, 0});
+}
+
+Handle::~Handle() {
+  cudaSetDevice(device);
+  cudaStreamSynchronize(stream);
+  free_graph();
+  for (auto& b : bufs_)
+    if (b.first) cudaFree(b.first);
+  cudaFree(dev_box);
+  cudaFreeHost(host_box);
+  if (own_stream) cudaStreamDestroy(stream);
+}
+
+void Handle::free_graph() {
+  cudaFree(g.edges);
+  cudaFree(g.offsets);
+  cudaFree(g.nbrs);
+  cudaFree(g.arc_edge);
+  g = DeviceGraph{};
+}
+
+void* Handle::ws(int slot, size_t bytes) {
+  auto& b = bufs_[slot];
+  if (b.second < bytes) {
+    if (b.first) {
+      CK(cudaStreamSynchronize(stream));
+      CK(cudaFree(b.first));
+    }
+    size_t want = std::max(bytes, (size_t)256);
+    CK(cudaMalloc(&b.first, want));
+    b.second = want;
+  }
+  return b.first;
+}
+
+void Handle::release(int slot) {
+  auto& b = bufs_[slot];
+  if (b.first) {
+    CK(cudaStreamSynchronize(stream));
+    CK(cudaFree(b.first));
+  }
+  b = {nullptr, 0};
+}
+
+void Handle::read_box(const int64_t* dptr, int count) {
+  CK(cudaMemcpyAsync(host_box, dptr, count * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+}
+
+void Handle::set_stream(cudaStream_t s) {
+  CK(cudaStreamSynchronize(stream));
+  if (own_stream) CK(cudaStreamDestroy(stream));
+  stream = s;
+  own_stream = false;
+}
+
+// ------------------------------------------------------ scan partials
+__global__ void k_scan_partials(uint32_t* partial, int64_t count) {
+  // One CTA of 1024 threads walks the partials in chunks, carrying the sum.
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry_s;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t base = 0; base < count; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    uint32_t v = (i < count) ? partial[i] : 0u;
+    uint32_t inc = warp_incl_scan(v);
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t s = warp_sums[lane];
+      uint32_t si = warp_incl_scan(s);
+      warp_sums[lane] = si - s;
+    }
+    __syncthreads();
+    uint32_t excl = carry_s + warp_sums[wid] + inc - v;
+    if (i < count) partial[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_s = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[count] = carry_s;
+}
+
+// ------------------------------------------------------- roots ascending
+namespace {
+struct SelfParentFlag {
+  const int32_t* parent;
+  __device__ uint32_t operator()(int64_t v) const { return parent[v] == (int32_t)v ? 1u : 0u; }
+};
+}  // namespace
+
+int64_t roots_ascending(Handle& h, const int32_t* parent, int32_t* roots) {
+  return scan_emit(h, h.g.n, SelfParentFlag{parent},
+                   EmitCompact{reinterpret_cast<uint32_t*>(roots)}, true);
+}
+
+}  // namespace rstg

@@ -1,0 +1,178 @@
+// engine.hpp -- device graph handle, workspace and phase timing.
+//
+// One Handle per (graph, device, stream). It owns the device copy of the
+// graph and a grow-only workspace so repeated builds on the same graph do
+// no cudaMalloc inside the timed region. Calls on one handle are
+// serialized on its stream (SURVEY.md §8b "Threading").
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rstg {
+
+// Counters mirroring StepReport (step_engine.hpp:21-25): `steps` counts
+// device-wide barriers (kernel boundaries / grid syncs of the device
+// pipeline), `work` counts element updates, plus device-side figures.
+struct Stats {
+  int64_t steps = 0;
+  int64_t work = 0;
+  int64_t rounds = 0;    // hook / graft rounds incl. the final empty one
+  int64_t launches = 0;  // kernels launched by the library
+  int64_t tree_edges = 0;
+  int64_t components = 0;
+  int64_t levels = 0;    // BFS levels (max over components) / PR mark levels
+  double device_ms = 0;  // event-timed device pipeline (when timing on)
+  void step(int64_t domain, int64_t launches_ = 1) {
+    ++steps;
+    work += domain;
+    launches += launches_;
+  }
+};
+
+// Named phase timer on the handle's stream (CUDA events; no host sync
+// until collect()).
+class PhaseTimer {
+ public:
+  void begin(cudaStream_t s, const char* name);
+  void end(cudaStream_t s);
+  // Synchronizes and returns (name, ms) per phase in order; clears.
+  std::vector<std::pair<std::string, double>> collect();
+  bool enabled = false;
+
+ private:
+  struct Rec {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs_;
+  std::vector<cudaEvent_t> pool_;
+  size_t used_ = 0;
+  cudaEvent_t get();
+};
+
+struct DeviceGraph {
+  int64_t n = 0, m = 0;
+  int64_t e_base = 0;           // global id of edges[0] (edge-partitioned ranks)
+  int2* edges = nullptr;        // m normalized (u<v) edges, id = e_base + index
+  uint32_t* offsets = nullptr;  // n+1 CSR offsets (nullptr if no CSR)
+  int32_t* nbrs = nullptr;      // 2m neighbours, ascending per vertex
+  uint32_t* arc_edge = nullptr; // 2m edge_origin
+  bool has_csr() const { return offsets != nullptr; }
+};
+
+class Handle {
+ public:
+  explicit Handle(int device);
+  void release(int slot);
+  ~Handle();
+  Handle(const Handle&) = delete;
+  Handle& operator=(const Handle&) = delete;
+
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  DeviceGraph g;
+  Stats stats;
+  PhaseTimer timer;
+
+  // Grow-only named device buffers (slot ids from WsSlot).
+  void* ws(int slot, size_t bytes);
+  template <class T>
+  T* ws(int slot, size_t count) {
+    return static_cast<T*>(ws(slot, count * sizeof(T) + 16));
+  }
+  // Small pinned host mailbox for flag/count readbacks.
+  int64_t* host_box = nullptr;
+  // Device counters block (64 x int64) zeroed per use by the caller.
+  int64_t* dev_box = nullptr;
+
+  // Copies `count` int64 device values into host_box and syncs the stream.
+  void read_box(const int64_t* dptr, int count);
+  void set_stream(cudaStream_t s);
+  void free_graph();
+
+ private:
+  std::vector<std::pair<void*, size_t>> bufs_;
+};
+
+// Workspace slots. Distinct algorithms may alias slots when they never run
+// concurrently on one handle.
+enum WsSlot : int {
+  WS_REP = 0,     // int32 n       CC reps / labels
+  WS_SLOT,        // u64 n         hook / graft slots
+  WS_TFLAG,       // u8 m          tree-edge flags
+  WS_PARENT,      // int32 n       output parent
+  WS_MINV,        // u32 n         min vertex per label
+  WS_ISROOT,      // u8 n
+  WS_POS,         // u32 2m+1      arc scan
+  WS_TF,          // u32 n+1       tree CSR offsets
+  WS_ATO,         // u32 E
+  WS_AFROM,       // u32 E
+  WS_SUCC,        // u32 E
+  WS_REV,         // u32 E
+  WS_SL,          // u64 E         (ruler id, local offset) per arc
+  WS_RPOS,        // u32 R         ruler arc positions
+  WS_RLEN,        // u32 R
+  WS_RNEXT,       // u32 R
+  WS_RA,          // u32/u64 R     Wyllie buffers
+  WS_RB,
+  WS_RC,
+  WS_RD,
+  WS_HEADS,       // u32 n
+  WS_SCAN,        // u32 scan partials
+  WS_SCAN2,
+  WS_ROOTS,       // int32 n       roots list
+  // PR-RST
+  WS_PR_SCRATCH,  // int32 n
+  WS_PR_ONPATH,   // u8 n
+  WS_PR_FRESH,    // u8 n
+  WS_PR_GROOT,    // u8 n
+  WS_PR_GU,       // int32 n
+  WS_PR_ANC,      // int32 n*L (level-major)
+  WS_PR_NEXT,     // int32 n (jump double buffer)
+  // BFS
+  WS_BFS_LEVEL,   // int32 n
+  WS_BFS_Q0,      // int32 n
+  WS_BFS_Q1,      // int32 n
+  WS_BFS_BITS,    // u32 n/32
+  WS_BFS_CTRL,    // int64 control block
+  // validation
+  WS_VAL_A,
+  WS_VAL_B,
+  WS_VAL_C,
+  WS_COUNT
+};
+
+// ---- algorithms (device-resident in/out; int32 ids) ----
+// cc_spanning_forest (cc_forest.cpp:73-102), exact: labels = converged reps,
+// tflag[e] = 1 for tree edges. Returns the number of tree edges.
+int64_t cc_exact(Handle& h, int32_t* labels, uint8_t* tflag);
+// cc labels only, validity-level (any correct partition; used by BFS
+// seeding and the validator). Returns the number of hook rounds.
+void cc_labels_fast(Handle& h, int32_t* labels);
+// euler_root_forest (euler_rooting.cpp:180-215) over the graph's CSR and a
+// tree-edge flag set; parent[n] out (int32 device).
+// verify: also prove the tree-edge set is a forest (list ranking reaches
+// every arc and every ruler chain ends), else "list ranking failed to
+// converge: not a forest" (euler_rooting.cpp:131-133).
+void euler_root(Handle& h, const int32_t* labels, const uint8_t* tflag, int64_t T,
+                int32_t designated_root, int32_t* parent, bool verify = false);
+// pr_rst (pr_rst.cpp:267-314)
+void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent);
+// bfs_rst (bfs_rst.cpp:10-77): parent, levels; roots in discovery order
+// written to roots (int32), returns count.
+int64_t bfs_rst(Handle& h, int32_t root, int32_t* parent, int32_t* levels, int32_t* roots);
+// Roots of a parent array in ascending order; returns count.
+int64_t roots_ascending(Handle& h, const int32_t* parent, int32_t* roots);
+// Device validity check (validate.cpp:108-211 semantics). Returns 0 when
+// valid, else an error code; *bad_vertex receives the first offender.
+int validate_forest(Handle& h, const int32_t* parent, int32_t required_root,
+                    int64_t* bad_vertex);
+
+}  // namespace rstg

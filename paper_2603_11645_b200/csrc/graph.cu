@@ -1,0 +1,359 @@
+// graph.cu -- device graph ingestion.
+//
+//   * upload of the reference's host Graph (graph.hpp:29-43: int64 CSR +
+//     edge list) narrowed to int32/uint32 on the device;
+//   * CSR construction on the device from a normalized edge list with the
+//     exact layout of build_csr (graph.cpp:133-172): per vertex the
+//     back-arcs to smaller neighbours (ascending) then the forward arcs
+//     (ascending); edge_origin = edge id;
+//   * normalize (graph.cpp:39-46) on the device: drop self-loops, orient
+//     u < v, sort, dedup;
+//   * device generators for the benchmark shapes (path, star, grid, the
+//     road mesh and Graph500 Kronecker of SURVEY.md Appendix B), producing
+//     exactly the host generators' edge lists.
+// Sorting here (normalize, back-arc grouping) uses CUB's radix sort: graph
+// ingestion is outside the RST hot path.
+#include <cub/cub.cuh>
+
+#include "engine.hpp"
+#include "graphgen.hpp"
+#include "scan.cuh"
+
+namespace rstg {
+
+// ------------------------------------------------------------ narrowing
+template <class T>
+__global__ void k_narrow(int64_t count, const long long* __restrict__ in, T* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (T)in[i];
+}
+__global__ void k_widen(int64_t count, const int32_t* __restrict__ in, long long* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+void widen_to_host(Handle& h, const int32_t* dev, int64_t count, int64_t* host) {
+  if (count <= 0) return;
+  const int64_t chunk = int64_t{1} << 24;
+  long long* stage = h.ws<long long>(WS_VAL_C, std::min(count, chunk));
+  for (int64_t off = 0; off < count; off += chunk) {
+    const int64_t c = std::min(chunk, count - off);
+    k_widen<<<grid_for(c), kBlock, 0, h.stream>>>(c, dev + off, stage);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(host + off, stage, c * sizeof(int64_t), cudaMemcpyDeviceToHost, h.stream));
+    CK(cudaStreamSynchronize(h.stream));  // stage reused by the next chunk
+  }
+}
+
+// Copies an int64 host array to the device through a staging buffer in
+// chunks and narrows it on the device.
+template <class T>
+static void upload_narrow(Handle& h, const int64_t* host, int64_t count, T* dev) {
+  if (count <= 0) return;
+  const int64_t chunk = int64_t{1} << 24;  // 16M elements = 128 MB staging
+  long long* stage = h.ws<long long>(WS_VAL_C, std::min(count, chunk));
+  for (int64_t off = 0; off < count; off += chunk) {
+    const int64_t c = std::min(chunk, count - off);
+    CK(cudaMemcpyAsync(stage, host + off, c * sizeof(int64_t), cudaMemcpyHostToDevice, h.stream));
+    k_narrow<T><<<grid_for(c), kBlock, 0, h.stream>>>(c, stage, dev + off);
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(h.stream));  // stage reused by the next chunk
+  }
+}
+
+static void alloc_graph(Handle& h, int64_t n, int64_t m, bool csr) {
+  if (n < 0) throw ArgError("negative vertex count");
+  if (n >= (int64_t{1} << 31)) throw ArgError("graph too large: vertex ids exceed 2^31");
+  if (m > (int64_t{1} << 32)) throw ArgError("too many edges");
+  h.free_graph();
+  h.g.n = n;
+  h.g.m = m;
+  CK(cudaMalloc(&h.g.edges, std::max<int64_t>(m, 1) * sizeof(int2)));
+  if (csr) {
+    if (2 * m >= (int64_t{1} << 32)) throw ArgError("CSR needs 2m < 2^32 arcs");
+    CK(cudaMalloc(&h.g.offsets, (n + 1) * sizeof(uint32_t)));
+    CK(cudaMalloc(&h.g.nbrs, std::max<int64_t>(2 * m, 1) * sizeof(int32_t)));
+    CK(cudaMalloc(&h.g.arc_edge, std::max<int64_t>(2 * m, 1) * sizeof(uint32_t)));
+  }
+}
+
+// Host Graph of the reference (graph.hpp:29-43) -> device.
+void upload_reference_graph(Handle& h, const int64_t* offsets, const int64_t* nbrs,
+                            const int64_t* origin, const int64_t* edges_uv, int64_t n, int64_t m) {
+  const bool csr = offsets != nullptr && 2 * m < (int64_t{1} << 32);
+  alloc_graph(h, n, m, csr);
+  if (csr) {
+    upload_narrow<uint32_t>(h, offsets, n + 1, h.g.offsets);
+    upload_narrow<int32_t>(h, nbrs, 2 * m, h.g.nbrs);
+    upload_narrow<uint32_t>(h, origin, 2 * m, h.g.arc_edge);
+  }
+  upload_narrow<int32_t>(h, edges_uv, 2 * m, reinterpret_cast<int32_t*>(h.g.edges));
+  CK(cudaStreamSynchronize(h.stream));
+}
+
+// ------------------------------------------------------ CSR on device
+__global__ void k_degrees(int64_t m, const int2* __restrict__ e, uint32_t* fdeg, uint32_t* bdeg) {
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < m;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool ok = i < m;
+    const int2 uv = ok ? e[i] : make_int2(-1, -1);
+    // warp-aggregate equal endpoints (runs of equal u are contiguous)
+    const unsigned fu = __match_any_sync(0xffffffffu, uv.x);
+    const unsigned fv = __match_any_sync(0xffffffffu, uv.y);
+    const int lane = threadIdx.x & 31;
+    if (ok && (__ffs(fu) - 1) == lane) atomicAdd(&fdeg[uv.x], (uint32_t)__popc(fu));
+    if (ok && (__ffs(fv) - 1) == lane) atomicAdd(&bdeg[uv.y], (uint32_t)__popc(fv));
+  }
+}
+__global__ void k_keys_v(int64_t m, const int2* __restrict__ e, uint32_t* keys, uint32_t* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (uint32_t)e[i].y;
+    vals[i] = (uint32_t)i;
+  }
+}
+__global__ void k_place_forward(int64_t m, const int2* __restrict__ e, const uint32_t* __restrict__ off,
+                                const uint32_t* __restrict__ bdeg, const uint32_t* __restrict__ fs,
+                                int32_t* nbrs, uint32_t* arc_edge) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int2 uv = e[i];
+    const uint32_t pos = off[uv.x] + bdeg[uv.x] + ((uint32_t)i - fs[uv.x]);
+    nbrs[pos] = uv.y;
+    arc_edge[pos] = (uint32_t)i;
+  }
+}
+__global__ void k_place_back(int64_t m, const int2* __restrict__ e, const uint32_t* __restrict__ skey,
+                             const uint32_t* __restrict__ sval, const uint32_t* __restrict__ off,
+                             const uint32_t* __restrict__ bs, int32_t* nbrs, uint32_t* arc_edge) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = skey[k], i = sval[k];
+    const uint32_t pos = off[v] + ((uint32_t)k - bs[v]);
+    nbrs[pos] = e[i].x;
+    arc_edge[pos] = i;
+  }
+}
+
+namespace {
+struct ArrF {
+  const uint32_t* a;
+  __device__ uint32_t operator()(int64_t i) const { return a[i]; }
+};
+struct SumF {
+  const uint32_t* a;
+  const uint32_t* b;
+  __device__ uint32_t operator()(int64_t i) const { return a[i] + b[i]; }
+};
+}  // namespace
+
+// build_csr (graph.cpp:133-172) on the device for h.g.edges (normalized).
+void build_csr_device(Handle& h) {
+  const int64_t n = h.g.n, m = h.g.m;
+  const cudaStream_t s = h.stream;
+  uint32_t* fdeg = h.ws<uint32_t>(WS_TF, n + 1);
+  uint32_t* bdeg = h.ws<uint32_t>(WS_MINV, n + 1);
+  uint32_t* fs = h.ws<uint32_t>(WS_HEADS, n + 1);
+  uint32_t* bs = h.ws<uint32_t>(WS_RPOS, n + 1);
+  CK(cudaMemsetAsync(fdeg, 0, (n + 1) * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(bdeg, 0, (n + 1) * sizeof(uint32_t), s));
+  if (m > 0) {
+    k_degrees<<<grid_for(m), kBlock, 0, s>>>(m, h.g.edges, fdeg, bdeg);
+    CK_LAUNCH();
+  }
+  scan_emit(h, n, SumF{fdeg, bdeg}, EmitExcl{h.g.offsets, n}, false);
+  scan_emit(h, n, ArrF{fdeg}, EmitExcl{fs, n}, false);
+  scan_emit(h, n, ArrF{bdeg}, EmitExcl{bs, n}, false);
+  if (n == 0) CK(cudaMemsetAsync(h.g.offsets, 0, sizeof(uint32_t), s));
+  if (m == 0) {
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  k_place_forward<<<grid_for(m), kBlock, 0, s>>>(m, h.g.edges, h.g.offsets, bdeg, fs, h.g.nbrs,
+                                                h.g.arc_edge);
+  CK_LAUNCH();
+  // back arcs: stable sort of edge ids by v
+  uint32_t* kin = h.ws<uint32_t>(WS_ATO, m);
+  uint32_t* vin = h.ws<uint32_t>(WS_AFROM, m);
+  uint32_t* kout = h.ws<uint32_t>(WS_SUCC, m);
+  uint32_t* vout = h.ws<uint32_t>(WS_REV, m);
+  k_keys_v<<<grid_for(m), kBlock, 0, s>>>(m, h.g.edges, kin, vin);
+  CK_LAUNCH();
+  int end_bit = 1;
+  while (end_bit < 32 && ((int64_t)1 << end_bit) < n) ++end_bit;
+  size_t temp = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, kin, kout, vin, vout, (int64_t)m, 0, end_bit, s));
+  void* tmp = h.ws(WS_SL, temp);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, temp, kin, kout, vin, vout, (int64_t)m, 0, end_bit, s));
+  k_place_back<<<grid_for(m), kBlock, 0, s>>>(m, h.g.edges, kout, vout, h.g.offsets, bs, h.g.nbrs,
+                                             h.g.arc_edge);
+  CK_LAUNCH();
+  CK(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------ normalize on device
+__global__ void k_pack_keys(int64_t m, const int2* __restrict__ raw, unsigned long long* keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int2 e = raw[i];
+    const uint32_t a = (uint32_t)min(e.x, e.y), b = (uint32_t)max(e.x, e.y);
+    keys[i] = (e.x == e.y) ? ~0ull : (((unsigned long long)a << 32) | b);
+  }
+}
+__global__ void k_unpack_keys(int64_t m, const unsigned long long* __restrict__ keys, int2* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    out[i] = make_int2((int)(k >> 32), (int)(uint32_t)k);
+  }
+}
+
+// normalize (graph.cpp:39-46): keys -> sorted unique edges; returns m.
+int64_t normalize_keys_device(Handle& h, unsigned long long* keys, int64_t count, int64_t n,
+                              int2* out) {
+  const cudaStream_t s = h.stream;
+  unsigned long long* sorted = h.ws<unsigned long long>(WS_VAL_B, count);
+  int end_bit = 1;
+  while (end_bit < 64 && ((uint64_t)1 << end_bit) <= ((uint64_t)n << 32)) ++end_bit;
+  end_bit = 64;  // self-loop sentinel is all ones
+  size_t temp = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, temp, keys, sorted, count, 0, end_bit, s));
+  void* tmp = h.ws(WS_SL, temp);
+  CK(cub::DeviceRadixSort::SortKeys(tmp, temp, keys, sorted, count, 0, end_bit, s));
+  long long* nsel = reinterpret_cast<long long*>(h.dev_box) + 48;
+  size_t temp2 = 0;
+  CK(cub::DeviceSelect::Unique(nullptr, temp2, sorted, keys, nsel, count, s));
+  void* tmp2 = h.ws(WS_SL, temp2);
+  CK(cub::DeviceSelect::Unique(tmp2, temp2, sorted, keys, nsel, count, s));
+  h.read_box(reinterpret_cast<int64_t*>(nsel), 1);
+  int64_t m = h.host_box[0];
+  // drop the self-loop sentinel (sorted last)
+  if (m > 0) {
+    unsigned long long last = 0;
+    CK(cudaMemcpy(&last, keys + m - 1, sizeof(last), cudaMemcpyDeviceToHost));
+    if (last == ~0ull) --m;
+  }
+  if (m > 0) {
+    k_unpack_keys<<<grid_for(m), kBlock, 0, s>>>(m, keys, out);
+    CK_LAUNCH();
+  }
+  CK(cudaStreamSynchronize(s));
+  return m;
+}
+
+// ------------------------------------------------------ device generators
+namespace {
+struct GridCount {  // grid (graph.cpp:198-210) and road mesh
+  int64_t rows, cols;
+  uint64_t thr;
+  bool road;
+  __device__ uint32_t operator()(int64_t id) const {
+    const int64_t r = id / cols, c = id % cols;
+    uint32_t k = (c + 1 < cols) ? 1u : 0u;
+    if (r + 1 < rows && (!road || road_vertical((uint64_t)id, thr))) ++k;
+    return k;
+  }
+};
+struct GridEmit {
+  GridCount gc;
+  int2* out;
+  __device__ void operator()(int64_t id, uint32_t p, uint32_t k) const {
+    if (!k) return;
+    const int64_t r = id / gc.cols, c = id % gc.cols;
+    if (c + 1 < gc.cols) out[p++] = make_int2((int)id, (int)(id + 1));
+    if (r + 1 < gc.rows && (!gc.road || road_vertical((uint64_t)id, gc.thr)))
+      out[p] = make_int2((int)id, (int)(id + gc.cols));
+  }
+};
+}  // namespace
+
+__global__ void k_gen_path(int64_t n, int2* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = make_int2((int)i, (int)(i + 1));
+}
+__global__ void k_gen_star(int64_t n, int2* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = make_int2(0, (int)(i + 1));
+}
+__global__ void k_gen_kron(int64_t tuples, int scale, unsigned long long* keys) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tuples;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t u, v;
+    kron_tuple((uint64_t)e, scale, &u, &v);
+    u = kron_perm(u, scale);
+    v = kron_perm(v, scale);
+    const uint64_t a = u < v ? u : v, b = u < v ? v : u;
+    keys[e] = (u == v) ? ~0ull : ((a << 32) | b);
+  }
+}
+
+// kind: 0 path(n) 1 star(n) 2 grid(rows, cols) 3 road(R, p) 4 kron(scale, ef)
+void generate_device(Handle& h, int kind, int64_t a, int64_t b, double p, bool build_csr) {
+  const cudaStream_t s = h.stream;
+  if (kind == 0 || kind == 1) {
+    if (a < 1) throw ArgError(kind == 0 ? "path: n must be >= 1" : "star: n must be >= 1");
+    alloc_graph(h, a, a - 1, build_csr);
+    if (a > 1) {
+      if (kind == 0)
+        k_gen_path<<<grid_for(a), kBlock, 0, s>>>(a, h.g.edges);
+      else
+        k_gen_star<<<grid_for(a), kBlock, 0, s>>>(a, h.g.edges);
+      CK_LAUNCH();
+    }
+  } else if (kind == 2 || kind == 3) {
+    const int64_t rows = a, cols = (kind == 2) ? b : a;
+    if (rows < 1 || cols < 1) throw ArgError("grid: dimensions must be >= 1");
+    GridCount gc{rows, cols, road_threshold(p), kind == 3};
+    const int64_t n = rows * cols;
+    int2* tmp = reinterpret_cast<int2*>(h.ws<unsigned long long>(WS_VAL_B, 2 * n + 1));
+    const uint32_t m = scan_emit(h, n, gc, GridEmit{gc, tmp}, true);
+    alloc_graph(h, n, m, build_csr);
+    CK(cudaMemcpyAsync(h.g.edges, tmp, (size_t)m * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+  } else if (kind == 4) {
+    const int scale = (int)a;
+    const int64_t tuples = b << scale;
+    if (scale < 1 || scale > 30) throw ArgError("kron: scale must be in [1, 30]");
+    unsigned long long* keys = h.ws<unsigned long long>(WS_VAL_A, tuples);
+    k_gen_kron<<<grid_for(tuples), kBlock, 0, s>>>(tuples, scale, keys);
+    CK_LAUNCH();
+    int2* tmp = reinterpret_cast<int2*>(h.ws<unsigned long long>(WS_VAL_C, tuples));
+    const int64_t m = normalize_keys_device(h, keys, tuples, int64_t{1} << scale, tmp);
+    alloc_graph(h, int64_t{1} << scale, m, build_csr && 2 * m < (int64_t{1} << 32));
+    CK(cudaMemcpyAsync(h.g.edges, tmp, (size_t)m * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+  } else {
+    throw ArgError("unknown generator kind");
+  }
+  CK(cudaStreamSynchronize(s));
+  if (h.g.offsets) build_csr_device(h);
+}
+
+// Normalized int64 edge list (the reference EdgeList) -> device graph + CSR.
+void upload_edges_build_csr(Handle& h, const int64_t* edges_uv, int64_t n, int64_t m) {
+  alloc_graph(h, n, m, 2 * m < (int64_t{1} << 32));
+  upload_narrow<int32_t>(h, edges_uv, 2 * m, reinterpret_cast<int32_t*>(h.g.edges));
+  if (h.g.offsets) build_csr_device(h);
+}
+
+// Device int32 arrays -> handle-owned copies.
+void adopt_device_graph(Handle& h, const int2* edges, const uint32_t* offsets, const int32_t* nbrs,
+                        const uint32_t* arc_edge, int64_t n, int64_t m) {
+  const bool csr = offsets != nullptr;
+  alloc_graph(h, n, m, csr || 2 * m < (int64_t{1} << 32));
+  const cudaStream_t s = h.stream;
+  CK(cudaMemcpyAsync(h.g.edges, edges, m * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+  if (csr) {
+    CK(cudaMemcpyAsync(h.g.offsets, offsets, (n + 1) * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(h.g.nbrs, nbrs, 2 * m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(h.g.arc_edge, arc_edge, 2 * m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  } else if (h.g.offsets) {
+    build_csr_device(h);
+  }
+}
+
+}  // namespace rstg

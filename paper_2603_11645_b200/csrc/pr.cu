@@ -1,0 +1,376 @@
+// pr.cu -- PR-RST path-reversal rooted spanning tree (pr_rst.cpp:267-314).
+//
+// Round = {graft, mark, check, reverse, batched jump, rebuild ancestors}
+// exactly as the reference, each step a coalesced vertex/edge sweep:
+//   graft proposals   k_hook (shared with CC; pr_rst.cpp:82-99)
+//   resolve + update  k_graft_resolve / k_graft_update (:112-128)
+//   mark_paths        one launch per doubling level k; marks carry the level
+//                     they were set in, so "marked before level k" replaces
+//                     the reference's cur/fresh double buffer and one kernel
+//                     per level suffices (:135-164). A level that adds
+//                     nothing stops the remaining launches on the device;
+//                     later levels could not add anything either (the marked
+//                     set is a contiguous 2^(k+1)-prefix of each chain).
+//   reverse_paths     two sweeps (:178-204)
+//   batched_jump      Jacobi snapshot hops, 2^batch per barrier (:216-252);
+//                     converged barriers exit on the device
+//   rebuild ancestors level-major table anc[k*n + v] (:254-265); a level
+//                     equal to its predecessor stops the rebuild (all higher
+//                     levels are then identical) and mark reads are clamped.
+// The only host synchronisation is one flag read per round.
+#include "engine.hpp"
+
+namespace rstg {
+
+void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_base,
+                 const int32_t* rep, unsigned long long* slot, int* any_prop);
+
+// Device control block layout (int32 words inside dev_box + 16).
+enum PrCtl : int {
+  C_ANY = 0,      // any graft proposal this round
+  C_BAD_REV,      // reversal found a marked vertex with no source
+  C_JUMP_DONE,    // batched jump converged
+  C_JUMP_FINAL,   // index (0/1) of the buffer holding the jumped reps
+  C_LMAX,         // valid ancestor levels
+  C_MARK_STOP,    // marking stopped (a level added nothing)
+  C_GREW0,        // C_GREW0 + k: level k added a mark
+  C_CHANGED0 = C_GREW0 + 40,  // C_CHANGED0 + k: anc level k differs from k-1
+  C_NWORDS = C_CHANGED0 + 40
+};
+
+__global__ void k_pr_init(int64_t n, int32_t* parent, int32_t* rep, int32_t* scratch,
+                          uint8_t* mark, uint8_t* groot, unsigned long long* slot) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    parent[v] = rep[v] = (int32_t)v;
+    scratch[v] = -1;
+    mark[v] = 0;
+    groot[v] = 0;
+    slot[v] = kKeyInf;
+  }
+}
+
+__global__ void k_anc_identity(int64_t n, int L, int32_t* anc) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < L; ++k) anc[(int64_t)k * n + v] = (int32_t)v;
+}
+
+// resolve winners against the frozen rep (pr_rst.cpp:112-122)
+__global__ void k_graft_resolve(int64_t n, const int2* __restrict__ edges, uint32_t e_base,
+                                const int32_t* __restrict__ rep,
+                                const unsigned long long* __restrict__ slot,
+                                uint8_t* __restrict__ mark, int32_t* __restrict__ scratch,
+                                uint8_t* __restrict__ groot, int32_t* __restrict__ gu) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = slot[v];
+    if (key == kKeyInf) continue;
+    const int2 uv = edges[(uint32_t)key - e_base];
+    const int32_t u = (rep[uv.x] == (int32_t)v) ? uv.x : uv.y;
+    const int32_t w = (u == uv.x) ? uv.y : uv.x;
+    mark[u] = 1;  // seeds carry level tag 1
+    scratch[u] = w;
+    groot[v] = 1;
+    gu[v] = u;
+  }
+}
+
+// rep update (pr_rst.cpp:123-128)
+__global__ void k_graft_update(int64_t n, int32_t* rep, unsigned long long* slot) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = slot[v];
+    if (key == kKeyInf) continue;
+    rep[v] = (int32_t)(key >> 32);
+    slot[v] = kKeyInf;
+  }
+}
+
+// One mark_paths level k (pr_rst.cpp:146-153). Marked-before-level-k means
+// tag in [1, k+1]; new marks get tag k+2.
+__global__ void __launch_bounds__(kBlock)
+    k_mark_level(int64_t n, int k, const int32_t* __restrict__ anc, uint8_t* mark, int* ctl) {
+  if (k > 0 && (ctl[C_MARK_STOP] || !ctl[C_GREW0 + k - 1])) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl[C_MARK_STOP] = 1;
+    return;
+  }
+  const int kk = min(k, ctl[C_LMAX] - 1);
+  const int32_t* lvl = anc + (int64_t)kk * n;
+  bool grew = false;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t t = mark[v];
+    if (t == 0 || t > k + 1) continue;
+    const int32_t a = lvl[v];
+    if (mark[a] == 0) {
+      mark[a] = (uint8_t)(k + 2);
+      grew = true;
+    }
+  }
+  block_flag(grew, &ctl[C_GREW0 + k]);
+}
+
+// The graft check (pr_rst.cpp:281-288): every grafted root r is marked and
+// still a root. Records the smallest offending (r, u).
+__global__ void k_graft_check(int64_t n, const uint8_t* groot, const uint8_t* mark,
+                              const int32_t* parent, const int32_t* gu,
+                              unsigned long long* bad) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (!groot[v]) continue;
+    if (!mark[v] || parent[v] != (int32_t)v)
+      atomicMin(bad, ((unsigned long long)v << 32) | (uint32_t)gu[v]);
+  }
+}
+__global__ void k_check_one(int32_t r, int32_t u, const uint8_t* mark, const int32_t* parent,
+                            unsigned long long* bad) {
+  if (!mark[r] || parent[r] != r) atomicMin(bad, ((unsigned long long)r << 32) | (uint32_t)u);
+}
+__global__ void k_clear_groot(int64_t n, uint8_t* groot) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    groot[v] = 0;
+}
+
+// reverse_paths (pr_rst.cpp:186-190, 191-201)
+__global__ void k_reverse_a(int64_t n, const uint8_t* __restrict__ mark,
+                            const int32_t* __restrict__ parent, int32_t* scratch) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (!mark[v]) continue;
+    const int32_t p = parent[v];
+    if (p != (int32_t)v) scratch[p] = (int32_t)v;
+  }
+}
+__global__ void k_reverse_b(int64_t n, uint8_t* mark, int32_t* parent, int32_t* scratch,
+                            int* ctl) {
+  bool bad = false;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (!mark[v]) continue;
+    const int32_t s = scratch[v];
+    if (s < 0) {
+      bad = true;
+      continue;
+    }
+    parent[v] = s;
+    scratch[v] = -1;
+    mark[v] = 0;
+  }
+  block_flag(bad, &ctl[C_BAD_REV]);
+}
+
+// One batched_jump barrier (pr_rst.cpp:235-244). Buffers alternate; a
+// converged state makes later barriers no-ops.
+__global__ void __launch_bounds__(kBlock)
+    k_jump_barrier(int64_t n, int64_t hops, int barrier, int32_t* buf0, int32_t* buf1,
+                   int* ctl, int* not_done) {
+  if (ctl[C_JUMP_DONE]) return;
+  const int32_t* snap = (barrier & 1) ? buf1 : buf0;
+  int32_t* next = (barrier & 1) ? buf0 : buf1;
+  bool pending = false;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int32_t x = snap[v];
+    for (int64_t t = 1; t < hops; ++t) {
+      const int32_t nx = snap[x];
+      if (nx == x) break;
+      x = nx;
+    }
+    next[v] = x;
+    if (snap[x] != x) pending = true;
+  }
+  block_flag(pending, not_done);
+}
+// Closes barrier `barrier`: converged -> record which buffer holds reps.
+__global__ void k_jump_close(int barrier, int* ctl, int* not_done) {
+  if (ctl[C_JUMP_DONE]) return;
+  if (*not_done == 0) {
+    ctl[C_JUMP_DONE] = 1;
+    ctl[C_JUMP_FINAL] = (barrier & 1) ? 0 : 1;
+  }
+  *not_done = 0;
+}
+__global__ void k_jump_copyback(int64_t n, int32_t* rep, const int32_t* other, const int* ctl) {
+  if (ctl[C_JUMP_FINAL] == 0) return;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    rep[v] = other[v];
+}
+
+// rebuild_special_ancestors level k >= 1 (pr_rst.cpp:260-264).
+__global__ void __launch_bounds__(kBlock) k_anc_level(int64_t n, int k, int32_t* anc, int* ctl) {
+  if (k >= 2 && !ctl[C_CHANGED0 + k - 1]) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(&ctl[C_LMAX], k);
+    return;
+  }
+  const int32_t* prev = anc + (int64_t)(k - 1) * n;
+  int32_t* cur = anc + (int64_t)k * n;
+  bool changed = false;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = prev[v];
+    const int32_t b = prev[a];
+    cur[v] = b;
+    changed |= (b != a);
+  }
+  block_flag(changed, &ctl[C_CHANGED0 + k]);
+}
+
+__global__ void k_set_i32(int32_t* p, int32_t v) { *p = v; }
+__global__ void k_set_u8(uint8_t* p, uint8_t v) { *p = v; }
+
+static int ceil_log2_i(int64_t x) {
+  int k = 0;
+  int64_t p = 1;
+  while (p < x) {
+    p <<= 1;
+    ++k;
+  }
+  return k;
+}
+
+void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
+  const int64_t n = h.g.n, m = h.g.m;
+  const int L = std::max(ceil_log2_i(std::max<int64_t>(n, 1)), 1);
+  int32_t* rep = h.ws<int32_t>(WS_REP, n);
+  int32_t* scratch = h.ws<int32_t>(WS_PR_SCRATCH, n);
+  uint8_t* mark = h.ws<uint8_t>(WS_PR_ONPATH, n);
+  uint8_t* groot = h.ws<uint8_t>(WS_PR_GROOT, n);
+  int32_t* gu = h.ws<int32_t>(WS_PR_GU, n);
+  int32_t* nextbuf = h.ws<int32_t>(WS_PR_NEXT, n);
+  int32_t* anc = h.ws<int32_t>(WS_PR_ANC, (size_t)n * L);
+  unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
+  int* ctl = reinterpret_cast<int*>(h.ws<int>(WS_BFS_CTRL, C_NWORDS + 8));
+  unsigned long long* bad_mark = reinterpret_cast<unsigned long long*>(h.dev_box) + 16;
+  int* not_done = ctl + C_NWORDS;
+  const unsigned g = grid_for(n);
+  const cudaStream_t s = h.stream;
+
+  h.timer.begin(s, "pr.init");
+  k_pr_init<<<g, kBlock, 0, s>>>(n, parent, rep, scratch, mark, groot, slot);
+  k_anc_identity<<<g, kBlock, 0, s>>>(n, L, anc);  // make_pr_state :60-68
+  CK_LAUNCH();
+  CK(cudaMemsetAsync(bad_mark, 0xFF, sizeof(unsigned long long), s));
+  h.stats.step(n, 2);
+  h.timer.end(s);
+
+  auto run_marking = [&]() {
+    CK(cudaMemsetAsync(ctl + C_MARK_STOP, 0, (1 + 40) * sizeof(int), s));
+    for (int k = 0; k < L; ++k) {
+      k_mark_level<<<g, kBlock, 0, s>>>(n, k, anc, mark, ctl);
+      h.stats.step(n);
+    }
+    CK_LAUNCH();
+  };
+  auto run_reverse = [&]() {
+    k_reverse_a<<<g, kBlock, 0, s>>>(n, mark, parent, scratch);
+    k_reverse_b<<<g, kBlock, 0, s>>>(n, mark, parent, scratch, ctl);
+    CK_LAUNCH();
+    h.stats.step(n);
+    h.stats.step(n);
+  };
+  // ctl[C_LMAX] = L initially (identity table: every level valid).
+  {
+    int init[C_NWORDS + 8] = {0};
+    init[C_LMAX] = L;
+    CK(cudaMemcpyAsync(ctl, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+
+  const int64_t hops = int64_t{1} << jump_batch;
+  const int64_t max_barriers = (ceil_log2_i(std::max<int64_t>(n, 1)) + jump_batch - 1) / jump_batch + 2;
+  int mode = 0;
+  for (int64_t round = 0;; ++round) {
+    if (round > n + 1) throw AlgoError("grafting failed to converge");
+    h.timer.begin(s, "pr.graft");
+    CK(cudaMemsetAsync(ctl + C_ANY, 0, sizeof(int), s));
+    launch_hook(h, mode, h.g.edges, m, (uint32_t)h.g.e_base, rep, slot, ctl + C_ANY);
+    CK(cudaMemcpyAsync(h.host_box, ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    h.timer.end(s);
+    h.stats.rounds = round + 1;
+    if (reinterpret_cast<int*>(h.host_box)[C_ANY] == 0) break;  // no graft (:279)
+    if (jump_batch < 1 || jump_batch > 20) throw AlgoError("jump batch out of range [1, 20]");
+    h.timer.begin(s, "pr.resolve");
+    k_graft_resolve<<<g, kBlock, 0, s>>>(n, h.g.edges, (uint32_t)h.g.e_base, rep, slot, mark,
+                                         scratch, groot, gu);
+    k_graft_update<<<g, kBlock, 0, s>>>(n, rep, slot);
+    CK_LAUNCH();
+    h.stats.step(n);
+    h.stats.step(n);
+    h.timer.end(s);
+    h.timer.begin(s, "pr.mark");
+    run_marking();
+    k_graft_check<<<g, kBlock, 0, s>>>(n, groot, mark, parent, gu, bad_mark);
+    k_clear_groot<<<g, kBlock, 0, s>>>(n, groot);
+    CK_LAUNCH();
+    h.stats.step(n);
+    h.timer.end(s);
+    h.timer.begin(s, "pr.reverse");
+    run_reverse();
+    h.timer.end(s);
+    h.timer.begin(s, "pr.jump");
+    CK(cudaMemsetAsync(ctl + C_JUMP_DONE, 0, 2 * sizeof(int), s));
+    CK(cudaMemsetAsync(not_done, 0, sizeof(int), s));
+    for (int64_t b = 0; b <= max_barriers; ++b) {
+      k_jump_barrier<<<g, kBlock, 0, s>>>(n, hops, (int)b, rep, nextbuf, ctl, not_done);
+      k_jump_close<<<1, 1, 0, s>>>((int)b, ctl, not_done);
+      h.stats.step(n);
+    }
+    k_jump_copyback<<<g, kBlock, 0, s>>>(n, rep, nextbuf, ctl);
+    CK_LAUNCH();
+    h.timer.end(s);
+    h.timer.begin(s, "pr.anc");
+    CK(cudaMemcpyAsync(anc, parent, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(ctl + C_CHANGED0, 0, 40 * sizeof(int), s));
+    k_set_i32<<<1, 1, 0, s>>>(ctl + C_LMAX, L);
+    for (int k = 1; k < L; ++k) {
+      k_anc_level<<<g, kBlock, 0, s>>>(n, k, anc, ctl);
+      h.stats.step(n);
+    }
+    CK_LAUNCH();
+    h.timer.end(s);
+    // Deferred error checks for this round.
+    CK(cudaMemcpyAsync(h.host_box, ctl, C_GREW0 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h.host_box + 8, bad_mark, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int* hc = reinterpret_cast<int*>(h.host_box);
+    const unsigned long long bm = (unsigned long long)h.host_box[8];
+    if (bm != kKeyInf)
+      throw AlgoError("path marking corrupted: " + std::to_string(bm >> 32) +
+                      " is not the root above " + std::to_string((uint32_t)bm));
+    if (hc[C_BAD_REV]) throw AlgoError("reversal found a marked vertex with no source");
+    if (!hc[C_JUMP_DONE]) throw AlgoError("pointer jumping detected a representative cycle");
+    mode ^= 1;
+  }
+
+  // Re-root the designated root's tree (pr_rst.cpp:298-303).
+  CK(cudaMemcpyAsync(h.host_box, rep + root, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int32_t emergent = *reinterpret_cast<int32_t*>(h.host_box);
+  if (emergent != root) {
+    h.timer.begin(s, "pr.reroot");
+    k_set_u8<<<1, 1, 0, s>>>(mark + root, 1);  // mark_path :170
+    run_marking();
+    k_check_one<<<1, 1, 0, s>>>(emergent, root, mark, parent, bad_mark);  // :172-175
+    k_set_i32<<<1, 1, 0, s>>>(scratch + root, root);  // reverse_path :212
+    run_reverse();
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(h.host_box, ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h.host_box + 8, bad_mark, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    h.timer.end(s);
+    const unsigned long long bm = (unsigned long long)h.host_box[8];
+    if (bm != kKeyInf)
+      throw AlgoError("path marking corrupted: " + std::to_string(bm >> 32) +
+                      " is not the root above " + std::to_string((uint32_t)bm));
+    if (reinterpret_cast<int*>(h.host_box)[C_BAD_REV])
+      throw AlgoError("reversal found a marked vertex with no source");
+  }
+}
+
+}  // namespace rstg

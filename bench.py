@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark driver: RST build throughput on B200 (arXiv 2603.11645 strategies).
+
+A *step* is one full rooted-spanning-tree build (every component) of one
+synthetic graph from a root: device-resident CSR + edge list in, parent
+array P (P[r] = r) out. Default workload (BASELINE.json configs[2], the
+north-star target): GConn-style CC + Euler-tour rooting (cc-euler) on the
+road_usa-shaped mesh R=4899 (n = 24,000,201, m = 28,858,008), root 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--workload road|grid|path|rmat24] [--algo cc-euler|pr-rst|bfs]
+                    [--impl ours|reference]
+
+Prints ONE JSON line (rank 0). `value` = edges/s over the device-resident
+timed region (max over ranks; N>1 runs N independent replicas -- the Euler
+tour is one linked list and does not shard). `e2e` = the same
+metric through the C ABI from pinned host int64 buffers (edge list in,
+parent array out, copies inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (device generator spec, root rule, BASELINE config index)
+    "road": ("road:4899", 0, 2),
+    "grid": ("grid:1024:1024", 0, 0),
+    "path": ("path:16777216", 0, 1),
+    "rmat24": ("kron:24:16", "maxdeg", 3),
+}
+REF_SAMPLE = {  # bounded CPU samples of each workload for the reference arm
+    "road": ("road", 2449),
+    "grid": ("grid", 1024, 1024),
+    "path": ("path", 1 << 20),
+    "rmat24": ("kron", 18),
+}
+ALGO_ID = {"bfs": 0, "cc-euler": 1, "pr-rst": 2}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="road", choices=sorted(WORKLOADS))
+    ap.add_argument("--algo", default="cc-euler", choices=sorted(ALGO_ID))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bfs-ratio", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------- roofline model
+def phase_bytes(phase, n, m, E):
+    """Algorithmic (compulsory) bytes of one launch of each phase."""
+    return {
+        "cc.hook_min": 16 * m,       # edge (8 B) + 2 rep gathers (4 B each)
+        "cc.hook_max": 16 * m,
+        "cc.apply": 8 * n,           # slot read
+        "cc.compress": 8 * n,        # rep read + write
+        "euler.arcs": 17 * m * 2 + 4 * n,  # arc_edge + flag + pos(w) + pos(r) + nbrs ... per arc
+        "euler.succ": 24 * E,        # ato, afrom, tf x2, 2 searches, succ, rev
+        "lr.walk": 12 * E,           # succ read + (ruler, offset) write per arc
+        "lr.rulers": 8 * E,
+        "lr.rulers_rank": 0,
+        "euler.orient": 24 * E // 2 + 4 * n,
+        "euler.roots": 12 * n,
+    }.get(phase)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# ------------------------------------------------------------- cpu side
+def cpu_reference(workload, algo, steps, warmup, cores=None):
+    """The reference's own CPU implementation (oracle/_ref, compiled from
+    /root/reference) on a bounded sample of the workload; edges/s."""
+    import numpy as np
+    import oracle as O
+
+    cores = cores or os.cpu_count() or 1
+    spec = REF_SAMPLE[workload]
+    g = O.gen(*spec)
+    root = 0
+    if WORKLOADS[workload][1] == "maxdeg":
+        root = int(np.argmax(np.diff(g.offsets)))
+    kind = "reference" if O.have_ref() else "port"
+    times = []
+    if kind == "reference":
+        rg = O.RefGraph(g)
+        for i in range(warmup + steps):
+            ms = rg.run_ms(ALGO_ID[algo], root, cores, 5)
+            if i >= warmup:
+                times.append(ms)
+    else:
+        cores = 1
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            O.run(g, ALGO_ID[algo], root)
+            if i >= warmup:
+                times.append((time.perf_counter() - t0) * 1e3)
+    med = statistics.median(times)
+    return {
+        "value": g.m / (med / 1e3), "unit": "edges/s", "cores": cores, "kind": kind,
+        "sample": f"{':'.join(map(str, spec))} (n={g.n}, m={g.m}), root {root}, {algo}, "
+                  f"median of {len(times)} runs of run_algorithm with {cores} workers",
+        "ms": med,
+    }
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    spec, root_rule, cfg_idx = WORKLOADS[args.workload]
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        baseline = json.load(f)
+    metric = f"RST build edges/sec ({args.algo}, {args.workload})"
+    config = {"workload": f"{spec} ({baseline['configs'][cfg_idx][:60]})", "algo": args.algo,
+              "root": root_rule, "l2": "inputs larger than L2 (graph >> 126 MB)"
+              if args.workload != "grid" else "grid CSR (25 MB) fits in L2: L2-resident",
+              "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+    if args.impl == "reference":
+        # The reference arm: rank 0 only, the box's host cores.
+        if rank != 0:
+            return
+        cb = cpu_reference(args.workload, args.algo, args.steps, args.warmup)
+        line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "edges/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": cb["ms"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": config,
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": "edges/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2603_11645_b200 as P
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    stream = torch.cuda.Stream()
+    g = P.DeviceGraph.generate(spec, device=dev)
+    n, m = g.n, g.m
+    root = 0
+    e_host = None
+    if root_rule == "maxdeg" or not args.no_e2e:
+        e_host = g.edges()
+    if root_rule == "maxdeg":
+        deg = np.bincount(e_host.ravel(), minlength=n)
+        root = int(np.argmax(deg))
+        config["root"] = root
+    g.set_stream(stream.cuda_stream)
+    algo = ALGO_ID[args.algo]
+    d_parent = torch.empty(n, dtype=torch.int32, device="cuda")
+    d_levels = torch.empty(n, dtype=torch.int32, device="cuda") if algo == 0 else None
+    lp = d_levels.data_ptr() if d_levels is not None else 0
+
+    def step():
+        return g.run_device(algo, root, d_parent.data_ptr(), lp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident, CUDA events on the launch stream
+    g.set_timing(True)
+    phases = {}
+    launches = 0
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        evs[0].record(stream)
+        for i in range(args.steps):
+            st = step()
+            launches += st["launches"]
+            for k, v in g.phase_times().items():
+                phases.setdefault(k, []).append(v)
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    g.set_timing(False)
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * m / (ms_per_step / 1e3)
+
+    # parity spot-check of the timed output against the device validator
+    parent_host = d_parent.cpu().numpy().astype(np.int64)
+    valid = g.validate(parent_host, root)[0]
+
+    # ---- roofline of the dominant kernel (phase) ----
+    E = 2 * (n - int((parent_host == np.arange(n)).sum()))
+    peaks, peak_kind = measured_peaks()
+    # per phase: mean over steps of (total ms in the step, launches in the step)
+    agg = {k: (statistics.mean(x[0] for x in v), statistics.mean(x[1] for x in v))
+           for k, v in phases.items()}
+    dominant = max(agg, key=lambda k: agg[k][0]) if agg else None
+    roofline = None
+    if dominant:
+        per_step_ms, per_step_launches = agg[dominant]
+        b = phase_bytes(dominant, n, m, E)  # algorithmic bytes of the phase per step
+        achieved = (b / (per_step_ms / 1e3) / 1e9) if b else None
+        roofline = {"bound": "hbm", "kernel": dominant, "achieved": achieved,
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
+                    "traffic": None, "peak_kind": peak_kind,
+                    "algorithmic_bytes_per_step": b, "kernel_ms_per_step": per_step_ms,
+                    "launches_per_step": per_step_launches,
+                    "avg_launch_ms": per_step_ms / max(per_step_launches, 1),
+                    "share_of_step": per_step_ms / ms_per_step}
+    b_alg = 4 * (n + 1) + 8 * m + 4 * n
+    step_roofline = {"b_alg": b_alg, "achieved_gbs": b_alg / (ms_per_step / 1e3) / 1e9,
+                     "frac_of_measured": b_alg / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"],
+                     "frac_of_8tbs": b_alg / (ms_per_step / 1e3) / 8e12}
+
+    # ---- e2e through the C ABI with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        eh = torch.from_numpy(np.ascontiguousarray(e_host.ravel())).pin_memory()
+        ph = torch.empty(n, dtype=torch.int64).pin_memory()
+        ge = P.DeviceGraph.generate("path:2", device=dev)
+        ge.upload(n, eh.numpy())  # allocate once (workspace reuse)
+        out_np = ph.numpy()
+        ge.run(algo, root)  # warm the handle's workspace
+        times = []
+        for _ in range(max(3, min(args.steps, 5))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ge.upload(n, eh.numpy())
+            ge.run(algo, root, out=out_np, want_roots=False, want_levels=False)
+            times.append((time.perf_counter() - t0) * 1e3)
+        e2e_ms = statistics.median(times)
+        e2e = {"value": world * m / (e2e_ms / 1e3), "unit": "edges/s", "ms": e2e_ms,
+               "h2d_bytes_per_step": int(eh.numel() * 8), "d2h_bytes_per_step": int(n * 8)}
+        ge.close()
+
+    # ---- in-run GPU BFS baseline on the same graph (north-star ratio) ----
+    bfs = None
+    if not args.no_bfs_ratio and algo != 0 and rank == 0:
+        lv = torch.empty(n, dtype=torch.int32, device="cuda")
+        g.run_device(0, root, d_parent.data_ptr(), lv.data_ptr())  # warm
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        stb = g.run_device(0, root, d_parent.data_ptr(), lv.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bms = e0.elapsed_time(e1)
+        bfs = {"bfs_ms": bms, "bfs_levels": stb["levels"], "speedup_vs_gpu_bfs": bms / ms_per_step}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference(args.workload, args.algo, 3, 1)
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # the checker is optional on the box
+            cpu = {"error": str(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": metric, "value": value, "unit": "edges/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "ms_per_step_median": statistics.median(step_ms), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": config, "n": n, "m": m, "valid": bool(valid),
+            "roofline": roofline, "step_roofline": step_roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "phases_ms_per_step": {k: [round(v[0], 4), v[1]] for k, v in agg.items()},
+            "bfs_baseline": bfs,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

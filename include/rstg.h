@@ -65,6 +65,11 @@ int rstg_device_count(int* count);
 int rstg_graph_create(const int64_t* offsets, const int64_t* neighbors,
                       const int64_t* edge_origin, const int64_t* edges_uv, int64_t n,
                       int64_t m, int device, rstg_graph** out);
+/* Re-upload a graph of the same kind into an existing handle (reuses its
+ * device buffers and workspace when n and m are unchanged). Pinned host
+ * buffers are read directly by the device (zero-copy narrowing). */
+int rstg_graph_upload(rstg_graph* g, const int64_t* offsets, const int64_t* neighbors,
+                      const int64_t* edge_origin, const int64_t* edges_uv, int64_t n, int64_t m);
 /* Graph from device-resident int32 arrays (copied into the handle).
  * d_offsets/d_nbrs/d_arc_edge may be NULL (CSR built on the device). */
 int rstg_graph_create_device(const int32_t* d_edges_uv, const uint32_t* d_offsets,

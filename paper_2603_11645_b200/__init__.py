@@ -26,7 +26,7 @@ RSTG_OK, RSTG_ERR_ARG, RSTG_ERR_ALGO, RSTG_ERR_CUDA = 0, 1, 2, 3
 
 # Symbols include/rstg.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "rstg_last_error", "rstg_device_count", "rstg_graph_create", "rstg_graph_create_device",
+    "rstg_last_error", "rstg_device_count", "rstg_graph_create", "rstg_graph_create_device", "rstg_graph_upload",
     "rstg_graph_generate", "rstg_graph_info", "rstg_graph_edges", "rstg_graph_destroy",
     "rstg_set_stream", "rstg_set_timing", "rstg_phase_times", "rstg_run", "rstg_run_device",
     "rstg_cc_spanning_forest", "rstg_euler_root_forest", "rstg_validate", "rstg_k_hook_step",
@@ -75,6 +75,8 @@ def lib():
         L.rstg_last_error.restype = ctypes.c_char_p
         L.rstg_graph_create.argtypes = [_i64p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.c_int, ctypes.POINTER(_vp)]
+        L.rstg_graph_upload.argtypes = [_vp, _i64p, _i64p, _i64p, _i64p, ctypes.c_int64,
+                                        ctypes.c_int64]
         L.rstg_graph_create_device.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64,
                                                ctypes.c_int, ctypes.POINTER(_vp)]
         L.rstg_graph_generate.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(_vp)]
@@ -161,6 +163,14 @@ class DeviceGraph:
                                               ctypes.byref(h)))
         return cls(h)
 
+    def upload(self, n, edges_uv, offsets=None, neighbors=None, edge_origin=None):
+        """Re-uploads a graph into this handle (edges_uv int64, (m, 2) or flat)."""
+        e = np.asarray(edges_uv)
+        m = e.size // 2
+        _check(lib().rstg_graph_upload(self._h, _p64(offsets), _p64(neighbors), _p64(edge_origin),
+                                       e.ctypes.data_as(_i64p), int(n), int(m)))
+        self.n, self.m = int(n), int(m)
+
     def close(self):
         if self._h:
             lib().rstg_graph_destroy(self._h)
@@ -190,12 +200,20 @@ class DeviceGraph:
         return json.loads(buf.value.decode() or "{}")
 
     # -- algorithms ----------------------------------------------------
-    def run(self, algo, root=0, jump_batch=5, want_levels=None):
-        """run_algorithm: returns (parent, roots, levels|None, stats dict)."""
+    def run(self, algo, root=0, jump_batch=5, want_levels=None, out=None, want_roots=True):
+        """run_algorithm: returns (parent, roots, levels|None, stats dict).
+
+        out: optional int64 array (e.g. pinned) receiving the parent array."""
         algo = ALGOS.get(algo, algo)
-        parent = np.zeros(self.n, np.int64)
+        parent = out if out is not None else np.zeros(self.n, np.int64)
         levels = np.zeros(self.n, np.int64) if (algo == BFS and want_levels is not False) else None
-        roots = np.zeros(max(self.n, 1), np.int64)
+        roots = np.zeros(max(self.n, 1), np.int64) if want_roots else None
+        if roots is None:
+            st = Stats()
+            nr = ctypes.c_int64(0)
+            _check(lib().rstg_run(self._h, algo, int(root), int(jump_batch), _p64(parent),
+                                  _p64(levels), None, ctypes.byref(nr), ctypes.byref(st)))
+            return parent, None, levels, st.as_dict()
         nr = ctypes.c_int64(0)
         st = Stats()
         _check(lib().rstg_run(self._h, algo, int(root), int(jump_batch), _p64(parent),

@@ -127,11 +127,21 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
   h.stats.device_ms = ms;
   if (nroots >= 0) h.stats.components = nroots;
   // phase times
+  // phase times: {"name": [total_ms, launches_of_phase], ...} in first-seen order
   auto ph = h.timer.collect();
+  std::vector<std::pair<std::string, std::pair<double, int>>> agg;
+  for (auto& p : ph) {
+    auto it = std::find_if(agg.begin(), agg.end(), [&](auto& a) { return a.first == p.first; });
+    if (it == agg.end())
+      agg.push_back({p.first, {p.second, 1}});
+    else
+      it->second.first += p.second, it->second.second += 1;
+  }
   std::string js = "{";
-  for (size_t i = 0; i < ph.size(); ++i) {
+  for (size_t i = 0; i < agg.size(); ++i) {
     if (i) js += ",";
-    js += "\"" + ph[i].first + "\":" + std::to_string(ph[i].second);
+    js += "\"" + agg[i].first + "\":[" + std::to_string(agg[i].second.first) + "," +
+          std::to_string(agg[i].second.second) + "]";
   }
   g->phases_json = js + "}";
   return nroots;
@@ -216,6 +226,16 @@ int rstg_graph_create(const int64_t* offsets, const int64_t* neighbors, const in
       throw;
     }
     *out = g;
+  });
+}
+
+int rstg_graph_upload(rstg_graph* g, const int64_t* offsets, const int64_t* neighbors,
+                      const int64_t* edge_origin, const int64_t* edges_uv, int64_t n, int64_t m) {
+  return guard([&] {
+    if (offsets && neighbors && edge_origin)
+      upload_reference_graph(g->h, offsets, neighbors, edge_origin, edges_uv, n, m);
+    else
+      upload_edges_build_csr(g->h, edges_uv, n, m);
   });
 }
 

@@ -34,8 +34,25 @@ __global__ void k_widen(int64_t count, const int32_t* __restrict__ in, long long
     out[i] = in[i];
 }
 
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Device int32 -> host int64. Pinned destinations are written directly by
+// the widening kernel over the host link (no staging round trip).
 void widen_to_host(Handle& h, const int32_t* dev, int64_t count, int64_t* host) {
   if (count <= 0) return;
+  if (is_pinned(host)) {
+    k_widen<<<grid_for(count), kBlock, 0, h.stream>>>(count, dev, reinterpret_cast<long long*>(host));
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(h.stream));
+    return;
+  }
   const int64_t chunk = int64_t{1} << 24;
   long long* stage = h.ws<long long>(WS_VAL_C, std::min(count, chunk));
   for (int64_t off = 0; off < count; off += chunk) {
@@ -47,11 +64,18 @@ void widen_to_host(Handle& h, const int32_t* dev, int64_t count, int64_t* host) 
   }
 }
 
-// Copies an int64 host array to the device through a staging buffer in
-// chunks and narrows it on the device.
+// int64 host array -> device int32/uint32. Pinned sources are read directly
+// by the narrowing kernel (zero-copy over the host link); pageable ones go
+// through a staging buffer.
 template <class T>
 static void upload_narrow(Handle& h, const int64_t* host, int64_t count, T* dev) {
   if (count <= 0) return;
+  if (is_pinned(host)) {
+    k_narrow<T><<<grid_for(count), kBlock, 0, h.stream>>>(
+        count, reinterpret_cast<const long long*>(host), dev);
+    CK_LAUNCH();
+    return;
+  }
   const int64_t chunk = int64_t{1} << 24;  // 16M elements = 128 MB staging
   long long* stage = h.ws<long long>(WS_VAL_C, std::min(count, chunk));
   for (int64_t off = 0; off < count; off += chunk) {
@@ -67,6 +91,7 @@ static void alloc_graph(Handle& h, int64_t n, int64_t m, bool csr) {
   if (n < 0) throw ArgError("negative vertex count");
   if (n >= (int64_t{1} << 31)) throw ArgError("graph too large: vertex ids exceed 2^31");
   if (m > (int64_t{1} << 32)) throw ArgError("too many edges");
+  if (h.g.edges && h.g.n == n && h.g.m == m && (h.g.offsets != nullptr) == csr) return;  // reuse
   h.free_graph();
   h.g.n = n;
   h.g.m = m;

@@ -279,8 +279,12 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     CK(cudaStreamSynchronize(s));
   }
 
-  const int64_t hops = int64_t{1} << jump_batch;
-  const int64_t max_barriers = (ceil_log2_i(std::max<int64_t>(n, 1)) + jump_batch - 1) / jump_batch + 2;
+  // batched_jump's guard (pr_rst.cpp:218-219) fires only once a graft
+  // happened; hops / barrier cap are derived after that check.
+  const bool batch_ok = jump_batch >= 1 && jump_batch <= 20;
+  const int64_t hops = batch_ok ? (int64_t{1} << jump_batch) : 1;
+  const int64_t max_barriers =
+      batch_ok ? (ceil_log2_i(std::max<int64_t>(n, 1)) + jump_batch - 1) / jump_batch + 2 : 0;
   int mode = 0;
   for (int64_t round = 0;; ++round) {
     if (round > n + 1) throw AlgoError("grafting failed to converge");
@@ -292,7 +296,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     h.timer.end(s);
     h.stats.rounds = round + 1;
     if (reinterpret_cast<int*>(h.host_box)[C_ANY] == 0) break;  // no graft (:279)
-    if (jump_batch < 1 || jump_batch > 20) throw AlgoError("jump batch out of range [1, 20]");
+    if (!batch_ok) throw AlgoError("jump batch out of range [1, 20]");
     h.timer.begin(s, "pr.resolve");
     k_graft_resolve<<<g, kBlock, 0, s>>>(n, h.g.edges, (uint32_t)h.g.e_base, rep, slot, mark,
                                          scratch, groot, gu);

@@ -15,6 +15,7 @@
 // Hook rounds stay synchronous: proposals read
 // reps frozen by the previous kernel boundary.
 #include "engine.hpp"
+#include "scan.cuh"
 
 namespace rstg {
 
@@ -96,6 +97,168 @@ __global__ void __launch_bounds__(kBlock) k_compress(int64_t n, int32_t* rep) {
   }
 }
 
+// One in-place doubling round rep[v] = rep[rep[v]] (the Jacobi step of
+// jump_to_convergence, evaluated in place: a fresher read only jumps
+// further). A round that changes nothing proves every rep[v] is a root
+// (roots are the only fixed points of a forest), so later rounds exit on
+// the device without a host round trip.
+template <int HOPS>
+__global__ void __launch_bounds__(kBlock) k_jump_round(int64_t n, int32_t* rep, int* flags,
+                                                       int round) {
+  if (round > 0 && flags[round - 1] == 0) return;
+  bool changed = false;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = rep[v];
+    int32_t x = rep[p];
+    if (x == p) continue;
+#pragma unroll
+    for (int hop = 1; hop < HOPS; ++hop) {
+      const int32_t y = rep[x];
+      if (y == x) break;
+      x = y;
+    }
+    rep[v] = x;
+    changed = true;
+  }
+  block_flag(changed, &flags[round]);
+}
+
+static int jump_hops() {
+  static int hops = 0;
+  if (hops == 0) {
+    const char* e = getenv("RSTG_JUMP_HOPS");
+    hops = e ? atoi(e) : 1;
+    if (hops != 1 && hops != 2 && hops != 4 && hops != 8) hops = 1;
+  }
+  return hops;
+}
+
+void launch_jump_rounds(Handle& h, int32_t* rep, int64_t n) {
+  int rounds = 2;
+  while ((int64_t{1} << (rounds - 2)) < n) ++rounds;  // ceil(log2 n) + 2
+  int* flags = reinterpret_cast<int*>(h.dev_box + 128);  // 64 ints (dev_box[128..159])
+  CK(cudaMemsetAsync(flags, 0, 64 * sizeof(int), h.stream));
+  const unsigned g = grid_for(n);
+  const int hops = jump_hops();
+  for (int r = 0; r < rounds && r < 64; ++r) {
+    if (hops == 1) k_jump_round<1><<<g, kBlock, 0, h.stream>>>(n, rep, flags, r);
+    else if (hops == 2) k_jump_round<2><<<g, kBlock, 0, h.stream>>>(n, rep, flags, r);
+    else if (hops == 4) k_jump_round<4><<<g, kBlock, 0, h.stream>>>(n, rep, flags, r);
+    else k_jump_round<8><<<g, kBlock, 0, h.stream>>>(n, rep, flags, r);
+    h.stats.step(n);
+  }
+  CK_LAUNCH();
+}
+
+// ---- two-level shortcutting ---------------------------------------------
+// Level 1 (k_tile_resolve): each CTA owns a tile of kTileV consecutive
+// vertices held in shared memory and follows every pointer while it stays
+// inside the tile (in-smem doubling), so rep[v] becomes either a root or the
+// first ancestor outside v's tile. Those out-of-tile targets X are flagged.
+// Level 2: X is compacted and pointer-jumped on its own (its pointers stay
+// inside X or hit roots); a last gather rep[v] = rep[rep[v]] finishes.
+// Passes over all n: 3 (tile, compaction, final) instead of ~log2(depth);
+// the jumping runs on |X|, which is tiny for chains (path: one per tile).
+constexpr int kTileV = 8192;
+constexpr int kTileThreads = 1024;
+
+__global__ void __launch_bounds__(kTileThreads)
+    k_tile_resolve(int64_t n, int32_t* rep, uint8_t* isx) {
+  __shared__ int32_t s[kTileV];
+  const int64_t base = (int64_t)blockIdx.x * kTileV;
+  const int cnt = (int)min((int64_t)kTileV, n - base);
+  for (int i = threadIdx.x; i < cnt; i += kTileThreads) s[i] = rep[base + i];
+  __syncthreads();
+  for (;;) {
+    bool changed = false;
+    for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
+      const int32_t p = s[i];
+      const int64_t lp = (int64_t)p - base;
+      if (lp >= 0 && lp < cnt) {
+        const int32_t q = s[lp];
+        if (q != p) {
+          s[i] = q;
+          changed = true;
+        }
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
+    const int32_t p = s[i];
+    rep[base + i] = p;
+    const int64_t lp = (int64_t)p - base;
+    if (lp < 0 || lp >= cnt) isx[p] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_jump_list(int64_t count, const uint32_t* __restrict__ list, int32_t* rep, int* flags,
+                int round) {
+  if (round > 0 && flags[round - 1] == 0) return;
+  bool changed = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = list[i];
+    const int32_t p = rep[v];
+    int32_t x = rep[p];
+    if (x == p) continue;
+#pragma unroll
+    for (int hop = 1; hop < 4; ++hop) {
+      const int32_t y = rep[x];
+      if (y == x) break;
+      x = y;
+    }
+    rep[v] = x;
+    changed = true;
+  }
+  block_flag(changed, &flags[round]);
+}
+
+__global__ void __launch_bounds__(kBlock) k_final_gather(int64_t n, int32_t* rep) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = rep[v];
+    const int32_t q = rep[p];
+    if (q != p) rep[v] = q;
+  }
+}
+
+namespace {
+struct ByteFlag {
+  const uint8_t* f;
+  __device__ uint32_t operator()(int64_t i) const { return f[i]; }
+};
+}  // namespace
+
+void launch_compress2(Handle& h, int32_t* rep, int64_t n) {
+  if (n <= 0) return;
+  uint8_t* isx = h.ws<uint8_t>(WS_ISROOT, n);
+  uint32_t* list = h.ws<uint32_t>(WS_HEADS, n + 1);
+  CK(cudaMemsetAsync(isx, 0, (size_t)n, h.stream));
+  const unsigned tiles = (unsigned)((n + kTileV - 1) / kTileV);
+  k_tile_resolve<<<tiles, kTileThreads, 0, h.stream>>>(n, rep, isx);
+  CK_LAUNCH();
+  h.stats.step(n);
+  const int64_t X = scan_emit(h, n, ByteFlag{isx}, EmitCompact{list}, true);
+  if (X > 0) {
+    int rounds = 2;
+    while ((int64_t{1} << (rounds - 2)) < X + 1) ++rounds;  // X-forest depth <= |X|
+    int* flags = reinterpret_cast<int*>(h.dev_box + 128);
+    CK(cudaMemsetAsync(flags, 0, 64 * sizeof(int), h.stream));
+    const unsigned g = grid_for(X);
+    for (int r = 0; r < rounds && r < 64; ++r) {
+      k_jump_list<<<g, kBlock, 0, h.stream>>>(X, list, rep, flags, r);
+      h.stats.step(X);
+    }
+    CK_LAUNCH();
+  }
+  k_final_gather<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
+  CK_LAUNCH();
+  h.stats.step(n);
+}
+
 void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_base,
                  const int32_t* rep, unsigned long long* slot, int* any_prop) {
   const unsigned grid = grid_for(m);
@@ -152,7 +315,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag) {
     if (total == prev) break;  // no hook applied this round (cc_forest.cpp:91)
     prev = total;
     h.timer.begin(h.stream, "cc.compress");
-    launch_compress(h, rep, n);
+    launch_compress2(h, rep, n);
     h.timer.end(h.stream);
     mode ^= 1;
   }

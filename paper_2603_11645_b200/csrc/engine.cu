@@ -56,7 +56,7 @@ Handle::Handle(int dev) : device(dev) {
   CK(cudaSetDevice(dev));
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   CK(cudaMallocHost(&host_box, 64 * sizeof(int64_t)));
-  CK(cudaMalloc(&dev_box, 64 * sizeof(int64_t)));
+  CK(cudaMalloc(&dev_box, 256 * sizeof(int64_t)));
   bufs_.assign(WS_COUNT, {nullptr, 0});
 }
 

@@ -89,7 +89,9 @@ class Handle {
   }
   // Small pinned host mailbox for flag/count readbacks.
   int64_t* host_box = nullptr;
-  // Device counters block (64 x int64) zeroed per use by the caller.
+  // Device counters block (256 x int64) zeroed per use by the caller; fixed
+  // regions: [0,2) cc, [4] euler, [8] lr, [16] pr, [30] bfs, [40] validate,
+  // [48] normalize, [50,53) capi/lr verify, [128,160) jump-round flags.
   int64_t* dev_box = nullptr;
 
   // Copies `count` int64 device values into host_box and syncs the stream.

@@ -37,6 +37,11 @@ WORKLOADS = {
     "grid": ("grid:1024:1024", 0, 0),
     "path": ("path:16777216", 0, 1),
     "rmat24": ("kron:24:16", "maxdeg", 3),
+    # edge-partitioned CC labels only (config 5); shards over ranks with an
+    # NCCL MIN all-reduce per hook round
+    "kron28cc": ("kron:28:16", None, 4),
+    "kron26cc": ("kron:26:16", None, 4),
+    "kron24cc": ("kron:24:16", None, 4),
 }
 REF_SAMPLE = {  # bounded CPU samples of each workload for the reference arm
     "road": ("road", 2449),
@@ -180,6 +185,70 @@ def cpu_reference(workload, algo, steps, warmup, cores=None):
     }
 
 
+# ------------------------------------------------------- kron CC (multi-GPU)
+def bench_kron_cc(args, rank, world, dev, metric, config):
+    """Config 5: exact connectivity of a Kronecker graph, edges partitioned
+    over the ranks (paper_2603_11645_b200/distcc.py). Strong scaling: the
+    graph is fixed, each rank holds 1/N of the edges."""
+    import torch
+
+    import paper_2603_11645_b200 as P
+    from paper_2603_11645_b200.distcc import GpuKernels, distributed_cc, edge_base
+
+    spec = WORKLOADS[args.workload][0]
+    t0 = time.perf_counter()
+    dg = P.DeviceGraph.generate_part(spec, rank, world, device=dev)
+    base = edge_base(dg.m, rank, world, "cuda")
+    dg.set_edge_base(base)
+    m_local = torch.tensor([dg.m], dtype=torch.int64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(m_local)
+    m_total, n = int(m_local.item()), dg.n
+    gen_s = time.perf_counter() - t0
+    kern = GpuKernels(dg)
+    for _ in range(args.warmup):
+        distributed_cc(kern, n, "cuda", world)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    rounds = hooks = 0
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            rep, rounds, hooks = distributed_cc(kern, n, "cuda", world)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    comps = int((rep == torch.arange(n, device="cuda", dtype=torch.int32)).sum().item())
+    peaks, peak_kind = measured_peaks()
+    b_cc = 8 * m_total + 4 * n  # SURVEY.md §8(d): read edges once + write labels
+    if rank == 0:
+        config.update({"n": n, "m": m_total, "edges_per_rank": "1/N by smaller endpoint",
+                       "rounds": rounds, "tree_edges": hooks, "components": comps,
+                       "generation_s": round(gen_s, 2),
+                       "exchange": "NCCL all_reduce(int64 MIN) of the 8n-byte hook slots per round"
+                       if world > 1 else "none (1 GPU)"})
+        line = {"metric": f"CC edges/sec ({args.workload}, edge-partitioned)",
+                "value": m_total / (ms_per_step / 1e3), "unit": "edges/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "int32", "data": "synthetic", "config": config,
+                "step_roofline": {"b_alg": b_cc,
+                                  "frac_of_measured": b_cc / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"]},
+                "clocks": clk.summary(), "cpu_baseline": None, "e2e": None}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ main
 def main():
     args = parse()
@@ -220,6 +289,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.cuda.current_device()
+    if args.workload.startswith("kron") and args.workload.endswith("cc"):
+        return bench_kron_cc(args, rank, world, dev, metric, config)
     stream = torch.cuda.Stream()
     g = P.DeviceGraph.generate(spec, device=dev)
     n, m = g.n, g.m

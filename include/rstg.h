@@ -115,6 +115,28 @@ int rstg_euler_root_forest(int64_t n, const int64_t* tree_uv, int64_t T, const i
 int rstg_validate(rstg_graph* g, const int64_t* parent, int64_t required_root, int* valid,
                   int* code, int64_t* bad_vertex);
 
+/* ---- edge-partitioned connectivity (multi-GPU) ----
+ * Rank r's handle holds a contiguous range of the GLOBAL normalized edge
+ * list: global edge id = e_base + local index (hook keys use global ids,
+ * so k-rank results equal the 1-rank result bit for bit). rep (int32 n) and
+ * slot (int64 n, empty = INT64_MAX) are caller-owned device buffers
+ * replicated on every rank; between rstg_cc_hook and rstg_cc_apply the
+ * caller MIN-all-reduces slot over the ranks (ncclMin on ncclInt64) --
+ * exactly combine_min of hook_step (cc_forest.cpp:34). */
+/* Kronecker partition on the device: edges whose smaller endpoint lies in
+ * [part*n/nparts, (part+1)*n/nparts), normalized (a contiguous range of the
+ * global sorted list). No CSR. */
+int rstg_graph_generate_part(const char* spec, int part, int nparts, int device,
+                             rstg_graph** out);
+int rstg_graph_set_edge_base(rstg_graph* g, int64_t e_base);
+int rstg_cc_init(rstg_graph* g, int32_t* d_rep, int64_t* d_slot);
+int rstg_cc_hook(rstg_graph* g, int mode, const int32_t* d_rep, int64_t* d_slot);
+/* applies every non-empty slot (rep[v] = winner, slot reset); local tree
+ * flags (nullable, m_local bytes); *applied = hooks applied (all ranks). */
+int rstg_cc_apply(rstg_graph* g, int32_t* d_rep, int64_t* d_slot, uint8_t* d_tflag,
+                  int64_t* applied);
+int rstg_cc_compress(rstg_graph* g, int32_t* d_rep);
+
 /* ---- kernel-level entry points (device kernels, host buffers) ---- */
 /* hook_step (cc_forest.cpp:8-48): slot[n] uses INT64_MAX as empty.
  * *applied = 1 if any hook was applied. */

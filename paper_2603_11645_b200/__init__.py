@@ -29,7 +29,9 @@ EXPORTS = (
     "rstg_last_error", "rstg_device_count", "rstg_graph_create", "rstg_graph_create_device", "rstg_graph_upload",
     "rstg_graph_generate", "rstg_graph_info", "rstg_graph_edges", "rstg_graph_destroy",
     "rstg_set_stream", "rstg_set_timing", "rstg_phase_times", "rstg_run", "rstg_run_device",
-    "rstg_cc_spanning_forest", "rstg_euler_root_forest", "rstg_validate", "rstg_k_hook_step",
+    "rstg_cc_spanning_forest", "rstg_euler_root_forest", "rstg_validate",
+    "rstg_graph_generate_part", "rstg_graph_set_edge_base", "rstg_cc_init", "rstg_cc_hook",
+    "rstg_cc_apply", "rstg_cc_compress", "rstg_k_hook_step",
     "rstg_k_jump", "rstg_k_list_rank",
 )
 
@@ -96,7 +98,14 @@ def lib():
                                              _i64p, _i64p]
         L.rstg_validate.argtypes = [_vp, _i64p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int),
                                     ctypes.POINTER(ctypes.c_int), _i64p]
-        L.rstg_k_hook_step.argtypes = [ctypes.c_int64, ctypes.c_int64, _i64p, ctypes.c_int, _i64p,
+        L.rstg_graph_generate_part.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_int, ctypes.POINTER(_vp)]
+        L.rstg_graph_set_edge_base.argtypes = [_vp, ctypes.c_int64]
+        L.rstg_cc_init.argtypes = [_vp, _vp, _vp]
+        L.rstg_cc_hook.argtypes = [_vp, ctypes.c_int, _vp, _vp]
+        L.rstg_cc_apply.argtypes = [_vp, _vp, _vp, _vp, _i64p]
+        L.rstg_cc_compress.argtypes = [_vp, _vp]
+        L.rstg_k_hook_step.argtypes =[ctypes.c_int64, ctypes.c_int64, _i64p, ctypes.c_int, _i64p,
                                        _u8p, _i64p, ctypes.POINTER(ctypes.c_int)]
         L.rstg_k_jump.argtypes = [ctypes.c_int64, _i64p]
         L.rstg_k_list_rank.argtypes = [ctypes.c_int64, _i64p, _i64p]
@@ -162,6 +171,33 @@ class DeviceGraph:
                                               _vp(d_arc_edge), int(n), int(m), device,
                                               ctypes.byref(h)))
         return cls(h)
+
+    @classmethod
+    def generate_part(cls, spec: str, part: int, nparts: int, device=0):
+        """Kronecker edges whose smaller endpoint is in part/nparts of [0, n)."""
+        h = _vp()
+        _check(lib().rstg_graph_generate_part(spec.encode(), part, nparts, device,
+                                              ctypes.byref(h)))
+        return cls(h)
+
+    def set_edge_base(self, e_base: int):
+        _check(lib().rstg_graph_set_edge_base(self._h, int(e_base)))
+
+    # -- per-round connectivity kernels on caller device buffers (dist CC) --
+    def cc_init(self, d_rep: int, d_slot: int):
+        _check(lib().rstg_cc_init(self._h, _vp(d_rep), _vp(d_slot)))
+
+    def cc_hook(self, mode: int, d_rep: int, d_slot: int):
+        _check(lib().rstg_cc_hook(self._h, int(mode), _vp(d_rep), _vp(d_slot)))
+
+    def cc_apply(self, d_rep: int, d_slot: int, d_tflag: int = 0) -> int:
+        a = ctypes.c_int64(0)
+        _check(lib().rstg_cc_apply(self._h, _vp(d_rep), _vp(d_slot), _vp(d_tflag or None),
+                                   ctypes.byref(a)))
+        return a.value
+
+    def cc_compress(self, d_rep: int):
+        _check(lib().rstg_cc_compress(self._h, _vp(d_rep)))
 
     def upload(self, n, edges_uv, offsets=None, neighbors=None, edge_origin=None):
         """Re-uploads a graph into this handle (edges_uv int64, (m, 2) or flat)."""

@@ -26,6 +26,9 @@ void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_b
                  const int32_t* rep, unsigned long long* slot, int* any_prop);
 void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tflag,
                   uint32_t e_base, uint32_t m_local, unsigned long long* counter);
+void launch_cc_init(Handle& h, int32_t* rep, unsigned long long* slot);
+void launch_compress2(Handle& h, int32_t* rep, int64_t n);
+void generate_kron_part(Handle& h, int scale, int ef, int part, int nparts);
 const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ,
                                  const uint32_t* heads, int64_t H, unsigned long long* sl,
                                  int64_t* R_out, bool verify);
@@ -295,6 +298,69 @@ int rstg_graph_generate(const char* spec, int device, rstg_graph** out) {
   });
 }
 
+int rstg_graph_generate_part(const char* spec, int part, int nparts, int device,
+                             rstg_graph** out) {
+  *out = nullptr;
+  return guard([&] {
+    int scale = 0, ef = 16;
+    if (std::sscanf(spec, "kron:%d:%d", &scale, &ef) < 1 &&
+        std::sscanf(spec, "gen:kron:%d:%d", &scale, &ef) < 1)
+      throw ArgError("partitioned generation supports kron:SCALE[:EF] only");
+    if (nparts < 1 || part < 0 || part >= nparts) throw ArgError("bad partition");
+    auto* g = new rstg_graph(device);
+    try {
+      generate_kron_part(g->h, scale, ef, part, nparts);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int rstg_graph_set_edge_base(rstg_graph* g, int64_t e_base) {
+  return guard([&] {
+    if (e_base < 0 || e_base + g->h.g.m > (int64_t{1} << 32)) throw ArgError("edge base out of range");
+    g->h.g.e_base = e_base;
+  });
+}
+
+int rstg_cc_init(rstg_graph* g, int32_t* d_rep, int64_t* d_slot) {
+  return guard([&] {
+    launch_cc_init(g->h, d_rep, reinterpret_cast<unsigned long long*>(d_slot));
+    CK(cudaStreamSynchronize(g->h.stream));
+  });
+}
+
+int rstg_cc_hook(rstg_graph* g, int mode, const int32_t* d_rep, int64_t* d_slot) {
+  return guard([&] {
+    Handle& h = g->h;
+    launch_hook(h, mode, h.g.edges, h.g.m, (uint32_t)h.g.e_base, d_rep,
+                reinterpret_cast<unsigned long long*>(d_slot), nullptr);
+    CK(cudaStreamSynchronize(h.stream));
+  });
+}
+
+int rstg_cc_apply(rstg_graph* g, int32_t* d_rep, int64_t* d_slot, uint8_t* d_tflag,
+                  int64_t* applied) {
+  return guard([&] {
+    Handle& h = g->h;
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box) + 2;
+    CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), h.stream));
+    launch_apply(h, d_rep, reinterpret_cast<unsigned long long*>(d_slot), d_tflag,
+                 (uint32_t)h.g.e_base, (uint32_t)h.g.m, ctr);
+    h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
+    *applied = h.host_box[0];
+  });
+}
+
+int rstg_cc_compress(rstg_graph* g, int32_t* d_rep) {
+  return guard([&] {
+    launch_compress2(g->h, d_rep, g->h.g.n);
+    CK(cudaStreamSynchronize(g->h.stream));
+  });
+}
+
 int rstg_graph_info(const rstg_graph* g, int64_t* n, int64_t* m) {
   if (!g) return RSTG_ERR_ARG;
   *n = g->h.g.n;
@@ -502,7 +568,7 @@ int rstg_k_hook_step(int64_t n, int64_t m, const int64_t* edges_uv, int mode, in
     unsigned long long* sl = h.ws<unsigned long long>(WS_SLOT, n);
     std::vector<unsigned long long> hs((size_t)n);
     for (int64_t v = 0; v < n; ++v)
-      hs[(size_t)v] = slot[v] == INT64_MAX ? kKeyInf : (unsigned long long)slot[v];
+      hs[(size_t)v] = (unsigned long long)slot[v];
     CK(cudaMemcpy(sl, hs.data(), n * 8, cudaMemcpyHostToDevice));
     uint8_t* tf = h.ws<uint8_t>(WS_TFLAG, m);
     CK(cudaMemcpy(tf, tree_flag, (size_t)m, cudaMemcpyHostToDevice));
@@ -517,7 +583,7 @@ int rstg_k_hook_step(int64_t n, int64_t m, const int64_t* edges_uv, int mode, in
     for (int64_t v = 0; v < n; ++v) rep[v] = hr[(size_t)v];
     CK(cudaMemcpy(tree_flag, tf, (size_t)m, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(hs.data(), sl, n * 8, cudaMemcpyDeviceToHost));
-    for (int64_t v = 0; v < n; ++v) slot[v] = hs[(size_t)v] == kKeyInf ? INT64_MAX : (int64_t)hs[(size_t)v];
+    for (int64_t v = 0; v < n; ++v) slot[v] = (int64_t)hs[(size_t)v];
     CK(cudaFree(h.g.edges));
     h.g.edges = nullptr;
   });

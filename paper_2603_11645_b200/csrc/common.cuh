@@ -3,8 +3,7 @@
 // Device data model: vertex ids int32, edge ids and CSR
 // offsets uint32 (the reference caps n < 2^31, m <= 2^32; graph.cpp:17-18),
 // hook keys uint64 packed (winner << 32) | edge, exactly pack_key
-// (step_engine.hpp:137-141). kKeyInf (INT64_MAX) becomes all-ones: every
-// real key is < 2^63 so unsigned order equals the reference's signed order.
+// (step_engine.hpp:137-141).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -17,7 +16,11 @@
 namespace rstg {
 
 constexpr uint32_t kNone32 = 0xFFFFFFFFu;
-constexpr unsigned long long kKeyInf = 0xFFFFFFFFFFFFFFFFull;
+// kKeyInf = INT64_MAX exactly as the reference: every real key is below it
+// (vertex ids < 2^31 - 1), so unsigned and signed order agree and an NCCL
+// int64 MIN all-reduce combines slots like combine_min (multi-GPU CC).
+constexpr unsigned long long kKeyInf = 0x7FFFFFFFFFFFFFFFull;
+constexpr unsigned long long kAllOnes = 0xFFFFFFFFFFFFFFFFull;  // "no error yet" sentinels
 constexpr int kBlock = 256;
 
 // Algorithm-level failure carrying the reference's exception message.

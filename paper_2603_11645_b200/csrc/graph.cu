@@ -357,6 +357,89 @@ void generate_device(Handle& h, int kind, int64_t a, int64_t b, double p, bool b
   if (h.g.offsets) build_csr_device(h);
 }
 
+// ---- Kronecker partition by smaller endpoint (multi-GPU CC) -------------
+// Edges of the globally normalized list are sorted by u = min endpoint, so
+// the edges with u in [lo, hi) form one contiguous range of the global
+// list. A part is generated in sub-ranges (each sort <= 2^29 keys) and
+// appended in order.
+__global__ void k_kron_count(int64_t tuples, int scale, uint32_t lo, uint32_t hi, int nsub,
+                             unsigned long long* counts) {
+  __shared__ unsigned long long sc[64];
+  for (int i = threadIdx.x; i < nsub; i += blockDim.x) sc[i] = 0;
+  __syncthreads();
+  const uint64_t span = hi - lo;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tuples;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t u, v;
+    kron_tuple((uint64_t)e, scale, &u, &v);
+    u = kron_perm(u, scale);
+    v = kron_perm(v, scale);
+    const uint64_t a = u < v ? u : v;
+    if (u == v || a < lo || a >= hi) continue;
+    const int sub = (int)(((a - lo) * (uint64_t)nsub) / span);
+    atomicAdd(&sc[sub], 1ull);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nsub; i += blockDim.x)
+    if (sc[i]) atomicAdd(&counts[i], sc[i]);
+}
+__global__ void k_kron_emit(int64_t tuples, int scale, uint32_t lo, uint32_t hi, int nsub, int sub,
+                            unsigned long long* keys, unsigned long long* ctr) {
+  const uint64_t span = hi - lo;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tuples;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t u, v;
+    kron_tuple((uint64_t)e, scale, &u, &v);
+    u = kron_perm(u, scale);
+    v = kron_perm(v, scale);
+    const uint64_t a = u < v ? u : v, b = u < v ? v : u;
+    if (u == v || a < lo || a >= hi) continue;
+    if ((int)(((a - lo) * (uint64_t)nsub) / span) != sub) continue;
+    keys[atomicAdd(ctr, 1ull)] = (a << 32) | b;
+  }
+}
+
+void generate_kron_part(Handle& h, int scale, int ef, int part, int nparts) {
+  if (scale < 1 || scale > 30) throw ArgError("kron: scale must be in [1, 30]");
+  const cudaStream_t s = h.stream;
+  const int64_t n = int64_t{1} << scale, tuples = (int64_t)ef << scale;
+  const uint32_t lo = (uint32_t)(n * part / nparts), hi = (uint32_t)(n * (part + 1) / nparts);
+  const int64_t sub_target = int64_t{1} << 29;
+  // expected tuples in the part ~ tuples / nparts (skewed ids are permuted)
+  int nsub = (int)std::min<int64_t>(64, std::max<int64_t>(1, (tuples / nparts) / sub_target + 1));
+  unsigned long long* counts = reinterpret_cast<unsigned long long*>(h.dev_box) + 160;  // [160,224)
+  CK(cudaMemsetAsync(counts, 0, 64 * sizeof(unsigned long long), s));
+  k_kron_count<<<grid_for(tuples), kBlock, 0, s>>>(tuples, scale, lo, hi, nsub, counts);
+  CK_LAUNCH();
+  h.read_box(reinterpret_cast<int64_t*>(counts), nsub);
+  std::vector<int64_t> cnt(h.host_box, h.host_box + nsub);
+  int64_t total = 0, maxc = 1;
+  for (int64_t c : cnt) {
+    total += c;
+    maxc = std::max(maxc, c);
+  }
+  h.free_graph();
+  int2* edges = nullptr;
+  CK(cudaMalloc(&edges, std::max<int64_t>(total, 1) * sizeof(int2)));
+  unsigned long long* keys = h.ws<unsigned long long>(WS_VAL_A, maxc);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box) + 224;
+  int64_t m = 0;
+  for (int sub = 0; sub < nsub; ++sub) {
+    if (cnt[sub] == 0) continue;
+    CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
+    k_kron_emit<<<grid_for(tuples), kBlock, 0, s>>>(tuples, scale, lo, hi, nsub, sub, keys, ctr);
+    CK_LAUNCH();
+    m += normalize_keys_device(h, keys, cnt[sub], n, edges + m);
+  }
+  h.release(WS_VAL_A);
+  h.release(WS_VAL_B);
+  h.release(WS_SL);
+  h.g.n = n;
+  h.g.m = m;
+  h.g.edges = edges;
+  h.g.e_base = 0;
+}
+
 // Normalized int64 edge list (the reference EdgeList) -> device graph + CSR.
 void upload_edges_build_csr(Handle& h, const int64_t* edges_uv, int64_t n, int64_t m) {
   alloc_graph(h, n, m, 2 * m < (int64_t{1} << 32));

@@ -343,7 +343,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     CK(cudaStreamSynchronize(s));
     const int* hc = reinterpret_cast<int*>(h.host_box);
     const unsigned long long bm = (unsigned long long)h.host_box[8];
-    if (bm != kKeyInf)
+    if (bm != kAllOnes)
       throw AlgoError("path marking corrupted: " + std::to_string(bm >> 32) +
                       " is not the root above " + std::to_string((uint32_t)bm));
     if (hc[C_BAD_REV]) throw AlgoError("reversal found a marked vertex with no source");
@@ -369,7 +369,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     CK(cudaStreamSynchronize(s));
     h.timer.end(s);
     const unsigned long long bm = (unsigned long long)h.host_box[8];
-    if (bm != kKeyInf)
+    if (bm != kAllOnes)
       throw AlgoError("path marking corrupted: " + std::to_string(bm >> 32) +
                       " is not the root above " + std::to_string((uint32_t)bm));
     if (reinterpret_cast<int*>(h.host_box)[C_BAD_REV])

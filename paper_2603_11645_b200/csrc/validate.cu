@@ -112,7 +112,7 @@ int validate_forest(Handle& h, const int32_t* parent, int32_t required_root,
   CK_LAUNCH();
   h.read_box(reinterpret_cast<int64_t*>(bad), 1);
   unsigned long long b = (unsigned long long)h.host_box[0];
-  if (b != kKeyInf) {
+  if (b != kAllOnes) {
     *bad_vertex = (int64_t)(b & 0xffffffffffull);
     return (int)(b >> 40);
   }
@@ -126,7 +126,7 @@ int validate_forest(Handle& h, const int32_t* parent, int32_t required_root,
   CK_LAUNCH();
   h.read_box(reinterpret_cast<int64_t*>(bad), 1);
   b = (unsigned long long)h.host_box[0];
-  if (b != kKeyInf) {
+  if (b != kAllOnes) {
     *bad_vertex = (int64_t)(b & 0xffffffffffull);
     return (int)(b >> 40);
   }

@@ -242,3 +242,85 @@ def test_device_generators_match_host(rst, O):
         p, r, lv, _ = dg.run(0, 0)
         ep, er, elv = O.run(g, 0, 0)
         assert np.array_equal(p, ep) and np.array_equal(lv, elv), spec
+
+
+# ---- the reference's own outputs (tests/golden, from make_golden.py) -------
+import glob as _glob
+import os as _os
+
+_GOLDEN = sorted(p for p in _glob.glob(_os.path.join(_os.path.dirname(__file__), "golden", "*.npz"))
+                 if "euler_ranks" not in p)
+
+
+@pytest.mark.parametrize("path", _GOLDEN, ids=lambda p: _os.path.basename(p)[:-4])
+def test_golden_fixtures(rst, path):
+    d = np.load(path)
+    n = int(d["n"])
+    dg = rst.DeviceGraph.from_host(n, np.stack([d["eu"], d["ev"]], 1))  # CSR built on device
+    labels, te = dg.cc_spanning_forest()
+    assert np.array_equal(labels, d["cc_labels"]) and np.array_equal(te, d["cc_tree_edges"])
+    for root in d["roots"]:
+        for algo, tag in ((0, "bfs"), (1, "cc_euler"), (2, "pr_rst")):
+            p, r, lv, _ = dg.run(algo, int(root))
+            assert np.array_equal(p, d[f"{tag}_r{root}_parent"]), (tag, root)
+            assert np.array_equal(r, d[f"{tag}_r{root}_roots"]), (tag, root)
+            if algo == 0:
+                assert np.array_equal(lv, d[f"{tag}_r{root}_levels"]), (tag, root)
+
+
+def test_golden_euler_ranks(rst):
+    d = np.load(_os.path.join(_os.path.dirname(__file__), "golden", "euler_ranks.npz"))
+    for t in range(20):
+        assert np.array_equal(rst.list_rank(d[f"t{t}_succ"]), d[f"t{t}_rank"])
+
+
+# ---- edge-partitioned CC (multi-GPU path, run here as parts on one GPU) ----
+def test_kron_parts_concatenate_to_full(rst, O):
+    g = O.gen("kron", 12)
+    for k in (1, 2, 3, 5):
+        parts = [rst.DeviceGraph.generate_part("kron:12", r, k) for r in range(k)]
+        e = np.concatenate([p.edges() for p in parts])
+        assert np.array_equal(e[:, 0], g.eu) and np.array_equal(e[:, 1], g.ev)
+
+
+def test_distcc_one_rank_matches_exact_cc(rst, O):
+    import torch
+
+    from paper_2603_11645_b200.distcc import GpuKernels, distributed_cc
+
+    for spec in ("kron:12", "kron:14"):
+        s = int(spec.split(":")[1])
+        g = O.gen("kron", s)
+        labels, te = O.cc_spanning_forest(g)
+        dg = rst.DeviceGraph.generate_part(spec, 0, 1)
+        rep, rounds, hooks = distributed_cc(GpuKernels(dg), dg.n, "cuda", 1)
+        assert np.array_equal(rep.cpu().numpy().astype(np.int64), labels)
+        assert hooks == len(te)
+
+
+def test_distcc_simulated_ranks_on_one_gpu(rst, O):
+    """k partitions hooked into one slot array (the MIN all-reduce of k
+    ranks equals applying their atomicMin proposals to one slot array)."""
+    import torch
+
+    g = O.gen("kron", 13)
+    labels, _ = O.cc_spanning_forest(g)
+    k = 3
+    parts = [rst.DeviceGraph.generate_part("kron:13", r, k) for r in range(k)]
+    base = 0
+    for p in parts:
+        p.set_edge_base(base)
+        base += p.m
+    n = parts[0].n
+    rep = torch.empty(n, dtype=torch.int32, device="cuda")
+    slot = torch.empty(n, dtype=torch.int64, device="cuda")
+    parts[0].cc_init(rep.data_ptr(), slot.data_ptr())
+    mode = 0
+    while True:
+        for p in parts:
+            p.cc_hook(mode, rep.data_ptr(), slot.data_ptr())
+        if parts[0].cc_apply(rep.data_ptr(), slot.data_ptr()) == 0:
+            break
+        parts[0].cc_compress(rep.data_ptr())
+        mode ^= 1
+    assert np.array_equal(rep.cpu().numpy().astype(np.int64), labels)

@@ -25,11 +25,16 @@ void widen_to_host(Handle& h, const int32_t* dev, int64_t count, int64_t* host);
 void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_base,
                  const int32_t* rep, unsigned long long* slot, int* any_prop);
 void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tflag,
-                  uint32_t e_base, uint32_t m_local, unsigned long long* counter);
+                  uint32_t e_base, uint32_t m_local, unsigned long long* counter,
+                  uint32_t* tlist);
 void launch_cc_init(Handle& h, int32_t* rep, unsigned long long* slot);
+void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* slot,
+                   unsigned long long* out_count, int* any_prop);
+void cc_round_done(Handle& h, int64_t out_count);
+void cc_reset_rounds(Handle& h);
 void launch_compress2(Handle& h, int32_t* rep, int64_t n);
 void generate_kron_part(Handle& h, int scale, int ef, int part, int nparts);
-const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ,
+const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ, int stride,
                                  const uint32_t* heads, int64_t H, unsigned long long* sl,
                                  int64_t* R_out, bool verify);
 }  // namespace rstg
@@ -112,9 +117,9 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
     nroots = bfs_rst(h, (int32_t)root, parent, levels, roots);
   } else if (algo == RSTG_CC_EULER) {
     int32_t* labels = h.ws<int32_t>(WS_REP, h.g.n);
-    uint8_t* tflag = h.ws<uint8_t>(WS_TFLAG, h.g.m);
-    const int64_t T = cc_exact(h, labels, tflag);
-    euler_root(h, labels, tflag, T, (int32_t)root, parent);
+    uint32_t* tlist = h.ws<uint32_t>(WS_TLIST, h.g.n);
+    const int64_t T = cc_exact(h, labels, nullptr, tlist);
+    euler_root(h, labels, tlist, h.g.n, T, (int32_t)root, parent);
   } else if (algo == RSTG_PR_RST) {
     pr_rst(h, (int32_t)root, jump_batch, parent);
   } else {
@@ -328,6 +333,8 @@ int rstg_graph_set_edge_base(rstg_graph* g, int64_t e_base) {
 int rstg_cc_init(rstg_graph* g, int32_t* d_rep, int64_t* d_slot) {
   return guard([&] {
     launch_cc_init(g->h, d_rep, reinterpret_cast<unsigned long long*>(d_slot));
+    cc_reset_rounds(g->h);
+    CK(cudaMemsetAsync(g->h.dev_box + 3, 0, sizeof(int64_t), g->h.stream));
     CK(cudaStreamSynchronize(g->h.stream));
   });
 }
@@ -335,8 +342,9 @@ int rstg_cc_init(rstg_graph* g, int32_t* d_rep, int64_t* d_slot) {
 int rstg_cc_hook(rstg_graph* g, int mode, const int32_t* d_rep, int64_t* d_slot) {
   return guard([&] {
     Handle& h = g->h;
-    launch_hook(h, mode, h.g.edges, h.g.m, (uint32_t)h.g.e_base, d_rep,
-                reinterpret_cast<unsigned long long*>(d_slot), nullptr);
+    // filtered round; its crossing-edge count is read back by rstg_cc_apply
+    cc_hook_round(h, mode, d_rep, reinterpret_cast<unsigned long long*>(d_slot),
+                  reinterpret_cast<unsigned long long*>(h.dev_box) + 3, nullptr);
     CK(cudaStreamSynchronize(h.stream));
   });
 }
@@ -348,9 +356,11 @@ int rstg_cc_apply(rstg_graph* g, int32_t* d_rep, int64_t* d_slot, uint8_t* d_tfl
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box) + 2;
     CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), h.stream));
     launch_apply(h, d_rep, reinterpret_cast<unsigned long long*>(d_slot), d_tflag,
-                 (uint32_t)h.g.e_base, (uint32_t)h.g.m, ctr);
-    h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
+                 (uint32_t)h.g.e_base, (uint32_t)h.g.m, ctr, nullptr);
+    h.read_box(reinterpret_cast<int64_t*>(ctr), 2);  // [2] applied, [3] crossing edges
     *applied = h.host_box[0];
+    cc_round_done(h, h.host_box[1]);
+    CK(cudaMemsetAsync(h.dev_box + 3, 0, sizeof(int64_t), h.stream));
   });
 }
 
@@ -487,11 +497,9 @@ int rstg_euler_root_forest(int64_t n, const int64_t* tree_uv, int64_t T, const i
     upload_edges_build_csr(h, uv.data(), n, T);
     int32_t* lab = h.ws<int32_t>(WS_REP, n);
     to_device<int32_t>(h, labels, n, lab);
-    uint8_t* tflag = h.ws<uint8_t>(WS_TFLAG, T);
-    if (T > 0) CK(cudaMemsetAsync(tflag, 1, (size_t)T, h.stream));
     int32_t* parent = h.ws<int32_t>(WS_PARENT, n);
     if (!simple) throw AlgoError("list ranking failed to converge: not a forest");
-    euler_root(h, lab, tflag, T, (int32_t)designated_root, parent, /*verify=*/true);
+    euler_root(h, lab, nullptr, T, T, (int32_t)designated_root, parent, /*verify=*/true);
     // Not a forest iff some vertex is unreachable from its root: validate
     // the orientation by doubling (a cycle never resolves to a root).
     {
@@ -575,7 +583,7 @@ int rstg_k_hook_step(int64_t n, int64_t m, const int64_t* edges_uv, int mode, in
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box);
     CK(cudaMemset(ctr, 0, 8));
     launch_hook(h, mode, h.g.edges, m, 0, r, sl, nullptr);
-    launch_apply(h, r, sl, tf, 0, (uint32_t)m, ctr);
+    launch_apply(h, r, sl, tf, 0, (uint32_t)m, ctr, nullptr);
     h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
     *applied = h.host_box[0] != 0;
     std::vector<int32_t> hr((size_t)n);
@@ -633,7 +641,7 @@ int rstg_k_list_rank(int64_t E, const int64_t* succ, int64_t* rank) {
     const int64_t H = scan_emit(h, E, NoPredFlag{has}, EmitCompact{heads}, true);
     unsigned long long* sl = h.ws<unsigned long long>(WS_SL, E);
     int64_t R = 0;
-    const uint32_t* rstart = list_rank_rulers(h, E, s, heads, H, sl, &R, /*verify=*/true);
+    const uint32_t* rstart = list_rank_rulers(h, E, s, 1, heads, H, sl, &R, /*verify=*/true);
     uint32_t* rk = h.ws<uint32_t>(WS_ATO, E);
     int* bad = reinterpret_cast<int*>(h.dev_box + 50);
     CK(cudaMemset(bad, 0, sizeof(int)));

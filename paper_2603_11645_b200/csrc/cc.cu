@@ -14,8 +14,12 @@
 //     kernel replaces the ceil(log2 L) doubling barriers.
 // Hook rounds stay synchronous: proposals read
 // reps frozen by the previous kernel boundary.
+#include <cooperative_groups.h>
+
 #include "engine.hpp"
 #include "scan.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rstg {
 
@@ -28,44 +32,89 @@ __global__ void k_cc_init(int64_t n, int32_t* rep, unsigned long long* slot) {
 }
 
 // hook_step edge pass (cc_forest.cpp:18-35) / graft proposals (pr_rst.cpp:82-99).
-template <int MODE>
+// Active-edge filtering: an edge whose endpoints share a rep stays internal
+// forever (components only merge), so a round may append the edges it
+// still saw crossing to out_list and the next round visits only those
+// (in_list). Proposals -- and therefore the result -- are unchanged.
+// Tiles of kHookItems x kBlock edges: all loads of a tile are issued before
+// the dependent rep gathers (8 independent chains per thread), and the
+// crossing edges of a tile are compacted with one block scan and a single
+// atomicAdd on the output cursor.
+constexpr int kHookItems = 8;
+constexpr int kHookTile = kHookItems * kBlock;
+
+template <int MODE, bool WRITE>
 __global__ void __launch_bounds__(kBlock)
-    k_hook(const int2* __restrict__ edges, int64_t m, uint32_t e_base,
-           const int32_t* __restrict__ rep, unsigned long long* __restrict__ slot,
-           int* any_proposal) {
+    k_hook(const int2* __restrict__ edges, int64_t count, uint32_t e_base,
+           const uint32_t* __restrict__ in_list, const int32_t* __restrict__ rep,
+           unsigned long long* __restrict__ slot, int* any_proposal, uint32_t* __restrict__ out_list,
+           unsigned long long* out_count) {
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_total;
   bool proposed = false;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int2 e = edges[i];
-    const int32_t ru = rep[e.x], rv = rep[e.y];
-    if (ru == rv) continue;
-    const int32_t lo = min(ru, rv), hi = max(ru, rv);
-    const int32_t winner = MODE == 0 ? lo : hi;
-    const int32_t loser = MODE == 0 ? hi : lo;
-    const unsigned long long key = pack_key((uint32_t)winner, e_base + (uint32_t)i);
-    proposed = true;
-    if (key < slot[loser]) atomicMin(&slot[loser], key);
+  for (int64_t tile = blockIdx.x; tile * kHookTile < count; tile += gridDim.x) {
+    const int64_t base = tile * kHookTile;
+    uint32_t idx[kHookItems];
+    int2 e[kHookItems];
+#pragma unroll
+    for (int k = 0; k < kHookItems; ++k) {
+      const int64_t i = base + k * kBlock + threadIdx.x;
+      idx[k] = (i < count) ? (in_list ? in_list[i] : (uint32_t)i) : kNone32;
+    }
+#pragma unroll
+    for (int k = 0; k < kHookItems; ++k)
+      e[k] = (idx[k] != kNone32) ? edges[idx[k]] : make_int2(0, 0);
+    uint32_t ncross = 0;
+#pragma unroll
+    for (int k = 0; k < kHookItems; ++k) {
+      const int32_t ru = rep[e[k].x], rv = rep[e[k].y];
+      if (idx[k] == kNone32 || ru == rv) {
+        idx[k] = kNone32;
+        continue;
+      }
+      ++ncross;
+      const int32_t lo = min(ru, rv), hi = max(ru, rv);
+      const int32_t winner = MODE == 0 ? lo : hi;
+      const int32_t loser = MODE == 0 ? hi : lo;
+      const unsigned long long key = pack_key((uint32_t)winner, e_base + idx[k]);
+      if (key < slot[loser]) atomicMin(&slot[loser], key);
+    }
+    proposed |= ncross > 0;
+    if (WRITE) {
+      uint32_t off = block_excl_scan(ncross, &s_total);
+      if (threadIdx.x == 0) s_base = s_total ? atomicAdd(out_count, (unsigned long long)s_total) : 0;
+      __syncthreads();
+      const unsigned long long ob = s_base + off;
+#pragma unroll
+      for (int k = 0, j = 0; k < kHookItems; ++k)
+        if (idx[k] != kNone32) out_list[ob + j++] = idx[k];
+      __syncthreads();
+    }
   }
   if (any_proposal) block_flag(proposed, any_proposal);
 }
 
-// Apply step (cc_forest.cpp:39-46); counts applied hooks = new tree edges.
+// Apply step (cc_forest.cpp:39-46); counts applied hooks (= new tree
+// edges). A root hooks at most once over the whole run (it is never a root
+// again), so tedge[v] = the edge that hooked v is a collision-free record
+// of the tree-edge set, indexed by vertex, for the Euler construction.
 __global__ void __launch_bounds__(kBlock)
     k_apply(int64_t n, int32_t* __restrict__ rep, unsigned long long* __restrict__ slot,
             uint8_t* __restrict__ tflag, uint32_t e_base, uint32_t m_local,
-            unsigned long long* counter) {
+            unsigned long long* counter, uint32_t* __restrict__ tedge) {
   uint32_t cnt = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long key = slot[v];
     if (key == kKeyInf) continue;
     rep[v] = (int32_t)(key >> 32);
-    const uint32_t e = (uint32_t)key - e_base;
+    const uint32_t eg = (uint32_t)key;
+    const uint32_t e = eg - e_base;
     if (tflag && e < m_local) tflag[e] = 1;
+    if (tedge) tedge[v] = eg;
     slot[v] = kKeyInf;
     ++cnt;
   }
-  // block reduce
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   __shared__ uint32_t ws[kBlock / 32];
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
@@ -163,13 +212,77 @@ void launch_jump_rounds(Handle& h, int32_t* rep, int64_t n) {
 constexpr int kTileV = 8192;
 constexpr int kTileThreads = 1024;
 
+// Sources of the tile's pointers (fused with the level-1 resolve so the new
+// reps never round-trip through HBM before shortcutting):
+//   kSrcRep    rep as is
+//   kSrcApply  apply step first: hooked roots take their slot's winner
+//              (cc_forest.cpp:39-46), the slot is reset, the edge recorded
+//   kSrcRound0 the first hook round computed directly from the CSR: with
+//              every rep a singleton, min-mode hooking gives v the key
+//              min over neighbours u < v of (u, e), i.e. v's first CSR
+//              neighbour (lists ascending) with its unique edge id
+enum { kSrcRep = 0, kSrcApply = 1, kSrcRound0 = 2 };
+
+struct RoundIO {
+  unsigned long long* slot;
+  uint8_t* tflag;
+  uint32_t* tedge;
+  uint32_t e_base, m_local;
+  unsigned long long* counter;  // += hooks applied
+  const uint32_t* offsets;
+  const int32_t* nbrs;
+  const uint32_t* arc_edge;
+};
+
+template <int SRC>
 __global__ void __launch_bounds__(kTileThreads)
-    k_tile_resolve(int64_t n, int32_t* rep, uint8_t* isx) {
+    k_tile_resolve(int64_t n, int32_t* rep, uint8_t* isx, RoundIO io) {
   __shared__ int32_t s[kTileV];
+  __shared__ uint32_t s_cnt;
   const int64_t base = (int64_t)blockIdx.x * kTileV;
   const int cnt = (int)min((int64_t)kTileV, n - base);
-  for (int i = threadIdx.x; i < cnt; i += kTileThreads) s[i] = rep[base + i];
+  if (threadIdx.x == 0) s_cnt = 0;
+  uint32_t hooked = 0;
+  for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
+    const int64_t v = base + i;
+    int32_t r;
+    uint32_t eg = kNone32;
+    if (SRC == kSrcRep) {
+      r = rep[v];
+    } else if (SRC == kSrcApply) {
+      const unsigned long long key = io.slot[v];
+      r = rep[v];
+      if (key != kKeyInf) {
+        r = (int32_t)(key >> 32);
+        eg = (uint32_t)key;
+        io.slot[v] = kKeyInf;
+      }
+    } else {
+      const uint32_t o = io.offsets[v];
+      r = (int32_t)v;
+      if (o < io.offsets[v + 1]) {
+        const int32_t u = io.nbrs[o];
+        if (u < r) {
+          r = u;
+          eg = io.arc_edge[o] + io.e_base;
+        }
+      }
+    }
+    if (SRC != kSrcRep && eg != kNone32) {
+      ++hooked;
+      if (io.tedge) io.tedge[v] = eg;
+      const uint32_t e = eg - io.e_base;
+      if (io.tflag && e < io.m_local) io.tflag[e] = 1;
+    }
+    s[i] = r;
+  }
+  if (SRC != kSrcRep) {
+    for (int o = 16; o > 0; o >>= 1) hooked += __shfl_xor_sync(0xffffffffu, hooked, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && hooked) atomicAdd(&s_cnt, hooked);
+  }
   __syncthreads();
+  if (SRC != kSrcRep && threadIdx.x == 0 && s_cnt) atomicAdd(io.counter, (unsigned long long)s_cnt);
   for (;;) {
     bool changed = false;
     for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
@@ -232,13 +345,20 @@ struct ByteFlag {
 };
 }  // namespace
 
-void launch_compress2(Handle& h, int32_t* rep, int64_t n) {
+// One shortcutting pass (optionally fused with the round's apply step or
+// the CSR first round): tile resolve, then the exit set, then the gather.
+void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& io) {
   if (n <= 0) return;
   uint8_t* isx = h.ws<uint8_t>(WS_ISROOT, n);
   uint32_t* list = h.ws<uint32_t>(WS_HEADS, n + 1);
   CK(cudaMemsetAsync(isx, 0, (size_t)n, h.stream));
   const unsigned tiles = (unsigned)((n + kTileV - 1) / kTileV);
-  k_tile_resolve<<<tiles, kTileThreads, 0, h.stream>>>(n, rep, isx);
+  if (src == kSrcApply)
+    k_tile_resolve<kSrcApply><<<tiles, kTileThreads, 0, h.stream>>>(n, rep, isx, io);
+  else if (src == kSrcRound0)
+    k_tile_resolve<kSrcRound0><<<tiles, kTileThreads, 0, h.stream>>>(n, rep, isx, io);
+  else
+    k_tile_resolve<kSrcRep><<<tiles, kTileThreads, 0, h.stream>>>(n, rep, isx, io);
   CK_LAUNCH();
   h.stats.step(n);
   const int64_t X = scan_emit(h, n, ByteFlag{isx}, EmitCompact{list}, true);
@@ -259,21 +379,74 @@ void launch_compress2(Handle& h, int32_t* rep, int64_t n) {
   h.stats.step(n);
 }
 
+void launch_compress2(Handle& h, int32_t* rep, int64_t n) {
+  resolve_round(h, rep, n, kSrcRep, RoundIO{});
+}
+
+static void launch_hook_k(Handle& h, int mode, const int2* edges, int64_t count, uint32_t e_base,
+                          const uint32_t* in_list, const int32_t* rep, unsigned long long* slot,
+                          int* any_prop, uint32_t* out_list, unsigned long long* out_count) {
+  const unsigned grid = grid_for((count + kHookItems - 1) / kHookItems);
+  if (mode == 0 && out_list)
+    k_hook<0, true><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
+                                                   any_prop, out_list, out_count);
+  else if (mode == 0)
+    k_hook<0, false><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
+                                                    any_prop, out_list, out_count);
+  else if (out_list)
+    k_hook<1, true><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
+                                                   any_prop, out_list, out_count);
+  else
+    k_hook<1, false><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
+                                                    any_prop, out_list, out_count);
+  CK_LAUNCH();
+  h.stats.step(count);
+}
+
 void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_base,
                  const int32_t* rep, unsigned long long* slot, int* any_prop) {
-  const unsigned grid = grid_for(m);
-  if (mode == 0)
-    k_hook<0><<<grid, kBlock, 0, h.stream>>>(edges, m, e_base, rep, slot, any_prop);
-  else
-    k_hook<1><<<grid, kBlock, 0, h.stream>>>(edges, m, e_base, rep, slot, any_prop);
-  CK_LAUNCH();
-  h.stats.step(m);
+  launch_hook_k(h, mode, edges, m, e_base, nullptr, rep, slot, any_prop, nullptr, nullptr);
+}
+
+// Filtered hook round on the handle's edges. Round 0 sees every edge cross
+// (all reps distinct), so filtering starts by recording round 1's crossing
+// edges; later rounds visit only the previous round's list.
+// *out_count (device) must be zero; pass its host value to cc_round_done.
+void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* slot,
+                   unsigned long long* out_count, int* any_prop) {
+  const int64_t m = h.g.m;
+  const uint32_t eb = (uint32_t)h.g.e_base;
+  if (h.cc_round == 0 || m == 0) {
+    if (m > 0)
+      launch_hook_k(h, mode, h.g.edges, m, eb, nullptr, rep, slot, any_prop, nullptr, nullptr);
+  } else if (h.cc_active < 0) {
+    uint32_t* out = h.ws<uint32_t>(WS_ELIST0, m);
+    launch_hook_k(h, mode, h.g.edges, m, eb, nullptr, rep, slot, any_prop, out, out_count);
+  } else {
+    const uint32_t* in = h.ws<uint32_t>(h.cc_list ? WS_ELIST1 : WS_ELIST0, m);
+    uint32_t* out = h.ws<uint32_t>(h.cc_list ? WS_ELIST0 : WS_ELIST1, m);
+    if (h.cc_active > 0)
+      launch_hook_k(h, mode, h.g.edges, h.cc_active, eb, in, rep, slot, any_prop, out, out_count);
+  }
+}
+void cc_round_done(Handle& h, int64_t out_count) {
+  if (h.cc_round >= 1 && h.g.m > 0) {
+    if (h.cc_active >= 0) h.cc_list ^= 1;
+    h.cc_active = out_count;
+  }
+  ++h.cc_round;
+}
+void cc_reset_rounds(Handle& h) {
+  h.cc_round = 0;
+  h.cc_active = -1;
+  h.cc_list = 0;
 }
 
 void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tflag,
-                  uint32_t e_base, uint32_t m_local, unsigned long long* counter) {
+                  uint32_t e_base, uint32_t m_local, unsigned long long* counter,
+                  uint32_t* tlist) {
   k_apply<<<grid_for(h.g.n), kBlock, 0, h.stream>>>(h.g.n, rep, slot, tflag, e_base, m_local,
-                                                     counter);
+                                                     counter, tlist);
   CK_LAUNCH();
   h.stats.step(h.g.n);
 }
@@ -290,39 +463,55 @@ void launch_cc_init(Handle& h, int32_t* rep, unsigned long long* slot) {
   h.stats.step(h.g.n);
 }
 
-int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag) {
+int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, uint32_t* tlist) {
   const int64_t n = h.g.n, m = h.g.m;
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(h.dev_box);
   h.timer.begin(h.stream, "cc.init");
   launch_cc_init(h, rep, slot);
   if (tflag && m > 0) CK(cudaMemsetAsync(tflag, 0, (size_t)m, h.stream));
+  if (tlist) CK(cudaMemsetAsync(tlist, 0xFF, (size_t)n * sizeof(uint32_t), h.stream));
   CK(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), h.stream));
   h.timer.end(h.stream);
   int mode = 0;  // HookMode::kMin first (cc_forest.cpp:87)
-  uint64_t prev = 0;
-  for (int64_t round = 0;; ++round) {
+  int* any = reinterpret_cast<int*>(h.dev_box + 2);
+  const RoundIO io{slot, tflag, tlist, (uint32_t)h.g.e_base, (uint32_t)m, counter,
+                   h.g.offsets, h.g.nbrs, h.g.arc_edge};
+  cc_reset_rounds(h);
+  int64_t round = 0;
+  if (h.g.has_csr() && m > 0) {
+    // round 0 (min mode over singleton reps) straight from the CSR, fused
+    // with its apply and shortcutting
+    h.timer.begin(h.stream, "cc.round0");
+    resolve_round(h, rep, n, kSrcRound0, io);
+    h.timer.end(h.stream);
+    cc_round_done(h, 0);
+    round = 1;
+    mode = 1;
+  }
+  int64_t total = 0;
+  for (;; ++round) {
     if (round > n + 1) throw AlgoError("hooking failed to converge");
+    CK(cudaMemsetAsync(counter + 1, 0, 2 * sizeof(unsigned long long), h.stream));
     h.timer.begin(h.stream, mode == 0 ? "cc.hook_min" : "cc.hook_max");
-    launch_hook(h, mode, h.g.edges, m, (uint32_t)h.g.e_base, rep, slot, nullptr);
+    cc_hook_round(h, mode, rep, slot, counter + 1, any);
     h.timer.end(h.stream);
-    h.timer.begin(h.stream, "cc.apply");
-    launch_apply(h, rep, slot, tflag, (uint32_t)h.g.e_base, (uint32_t)m, counter);
-    h.timer.end(h.stream);
-    h.read_box(reinterpret_cast<int64_t*>(counter), 1);
-    const uint64_t total = (uint64_t)h.host_box[0];
+    h.read_box(reinterpret_cast<int64_t*>(counter), 3);  // hooks so far, crossing, any
+    total = h.host_box[0];
+    const bool proposed = h.host_box[2] != 0;
+    cc_round_done(h, h.host_box[1]);
     h.stats.rounds = round + 1;
-    if (total == prev) break;  // no hook applied this round (cc_forest.cpp:91)
-    prev = total;
-    h.timer.begin(h.stream, "cc.compress");
-    launch_compress2(h, rep, n);
+    // a round without proposals applies nothing (cc_forest.cpp:91)
+    if (!proposed) break;
+    h.timer.begin(h.stream, "cc.apply_compress");
+    resolve_round(h, rep, n, kSrcApply, io);
     h.timer.end(h.stream);
     mode ^= 1;
   }
-  h.stats.tree_edges = (int64_t)prev;
-  return (int64_t)prev;
+  h.stats.tree_edges = total;
+  return total;
 }
 
-void cc_labels_fast(Handle& h, int32_t* labels) { cc_exact(h, labels, nullptr); }
+void cc_labels_fast(Handle& h, int32_t* labels) { cc_exact(h, labels, nullptr, nullptr); }
 
 }  // namespace rstg

@@ -75,6 +75,10 @@ class Handle {
   Handle& operator=(const Handle&) = delete;
 
   int device = 0;
+  // connectivity round state (active-edge filtering, cc.cu)
+  int cc_round = 0;
+  int64_t cc_active = -1;  // edges in the current active list, -1 = all
+  int cc_list = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   DeviceGraph g;
@@ -130,6 +134,9 @@ enum WsSlot : int {
   WS_SCAN,        // u32 scan partials
   WS_SCAN2,
   WS_ROOTS,       // int32 n       roots list
+  WS_TLIST,       // u32 n         tree-edge list
+  WS_ELIST0,      // u32 m         active (still crossing) edges, ping
+  WS_ELIST1,      // u32 m         pong
   // PR-RST
   WS_PR_SCRATCH,  // int32 n
   WS_PR_ONPATH,   // u8 n
@@ -154,7 +161,9 @@ enum WsSlot : int {
 // ---- algorithms (device-resident in/out; int32 ids) ----
 // cc_spanning_forest (cc_forest.cpp:73-102), exact: labels = converged reps,
 // tflag[e] = 1 for tree edges. Returns the number of tree edges.
-int64_t cc_exact(Handle& h, int32_t* labels, uint8_t* tflag);
+// tlist (nullable, n entries): tlist[v] = global id of the tree edge that
+// hooked root v, or kNone32 (every tree edge appears exactly once).
+int64_t cc_exact(Handle& h, int32_t* labels, uint8_t* tflag, uint32_t* tlist = nullptr);
 // cc labels only, validity-level (any correct partition; used by BFS
 // seeding and the validator). Returns the number of hook rounds.
 void cc_labels_fast(Handle& h, int32_t* labels);
@@ -163,7 +172,9 @@ void cc_labels_fast(Handle& h, int32_t* labels);
 // verify: also prove the tree-edge set is a forest (list ranking reaches
 // every arc and every ruler chain ends), else "list ranking failed to
 // converge: not a forest" (euler_rooting.cpp:131-133).
-void euler_root(Handle& h, const int32_t* labels, const uint8_t* tflag, int64_t T,
+// Tree edges: tsrc[i] for i in [0, N) (kNone32 entries skipped), or, with
+// tsrc == null, graph edges 0..T-1 (explicit forests). Needs no CSR.
+void euler_root(Handle& h, const int32_t* labels, const uint32_t* tsrc, int64_t N, int64_t T,
                 int32_t designated_root, int32_t* parent, bool verify = false);
 // pr_rst (pr_rst.cpp:267-314)
 void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent);

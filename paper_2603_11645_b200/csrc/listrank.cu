@@ -53,14 +53,14 @@ __global__ void k_init_rulers(const uint32_t* rpos, int64_t R, unsigned long lon
 // Walk sublists of rulers [lo, hi). Dynamic rulers are appended at
 // *rcount (device counter) and walked by the next launch.
 __global__ void __launch_bounds__(kBlock)
-    k_walk(const uint32_t* __restrict__ succ, uint32_t* rpos, uint32_t* __restrict__ rlen,
+    k_walk(const uint32_t* __restrict__ succ, int stride, uint32_t* rpos, uint32_t* __restrict__ rlen,
            uint32_t* __restrict__ rnext, unsigned long long* sl, uint32_t lo, uint32_t hi,
            unsigned long long* rcount) {
   for (int64_t t = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < hi;
        t += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t i = (uint32_t)t;
     const unsigned long long tag = (unsigned long long)i << 32;
-    uint32_t cur = succ[rpos[i]];
+    uint32_t cur = succ[(size_t)rpos[i] * stride];
     uint32_t off = 1;
     uint32_t nxt = kNone32;
     for (;;) {
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kBlock)
       }
       sl[cur] = tag | off;
       ++off;
-      cur = succ[cur];
+      cur = succ[(size_t)cur * stride];
     }
     rlen[i] = off;
     rnext[i] = nxt;
@@ -144,7 +144,7 @@ static int ceil_log2_i(int64_t x) {
 }
 
 // Returns rstart (device, R entries); sl filled for every arc.
-const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ,
+const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ, int stride,
                                  const uint32_t* heads, int64_t H, unsigned long long* sl,
                                  int64_t* R_out, bool verify) {
   const int64_t cap = E / (1 << kLogK) * 2 + H + E / kWalkCap + 64;
@@ -178,7 +178,8 @@ const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ,
   uint32_t lo = 0, hi = R;
   while (lo < hi) {
     if ((int64_t)hi + (int64_t)(hi - lo) > cap) throw std::runtime_error("walk capacity");
-    k_walk<<<grid_for(hi - lo), kBlock, 0, h.stream>>>(succ, rpos, rlen, rnext, sl, lo, hi, ctr);
+    k_walk<<<grid_for(hi - lo), kBlock, 0, h.stream>>>(succ, stride, rpos, rlen, rnext, sl, lo, hi,
+                                                        ctr);
     CK_LAUNCH();
     h.stats.step(hi - lo);
     h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
@@ -190,10 +191,12 @@ const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ,
 
   // Prefix over the ruler lists.
   h.timer.begin(h.stream, "lr.rulers_rank");
-  uint32_t* pred = h.ws<uint32_t>(WS_RA, R);
-  unsigned long long* wa = h.ws<unsigned long long>(WS_RB, R);
-  unsigned long long* wb = h.ws<unsigned long long>(WS_RC, R);
-  uint32_t* rstart = h.ws<uint32_t>(WS_RD, R);
+  // sized by the deterministic capacity, not R (R varies with the tour
+  // layout; a grow-only buffer must not reallocate inside the timed loop)
+  uint32_t* pred = h.ws<uint32_t>(WS_RA, cap);
+  unsigned long long* wa = h.ws<unsigned long long>(WS_RB, cap);
+  unsigned long long* wb = h.ws<unsigned long long>(WS_RC, cap);
+  uint32_t* rstart = h.ws<uint32_t>(WS_RD, cap);
   CK(cudaMemsetAsync(pred, 0xFF, R * sizeof(uint32_t), h.stream));
   const unsigned g = grid_for(R);
   k_ruler_pred<<<g, kBlock, 0, h.stream>>>(R, rnext, pred);

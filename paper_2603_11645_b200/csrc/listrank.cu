@@ -181,11 +181,16 @@ const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ, int
     k_walk<<<grid_for(hi - lo), kBlock, 0, h.stream>>>(succ, stride, rpos, rlen, rnext, sl, lo, hi,
                                                         ctr);
     CK_LAUNCH();
-    h.stats.step(hi - lo);
+    h.stats.launches++;
     h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
     lo = hi;
     hi = (uint32_t)h.host_box[0];
   }
+  // Counters stay deterministic although the number of follow-up walks
+  // (dynamic rulers) depends on the tour layout: one logical barrier, E arcs.
+  h.stats.steps++;
+  h.stats.work += E;
+  const int64_t R_static = R;
   R = hi;
   h.timer.end(h.stream);
 
@@ -202,17 +207,18 @@ const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ, int
   k_ruler_pred<<<g, kBlock, 0, h.stream>>>(R, rnext, pred);
   k_ruler_wyllie_init<<<g, kBlock, 0, h.stream>>>(R, pred, rlen, wa);
   CK_LAUNCH();
-  h.stats.step(R, 2);
-  const int rounds = ceil_log2_i(R < 2 ? 2 : R) + 1;
+  h.stats.step(R_static, 2);
+  // round count from the deterministic capacity (>= ceil(log2 R) + 1)
+  const int rounds = ceil_log2_i(cap < 2 ? 2 : cap) + 1;
   for (int r = 0; r < rounds; ++r) {
     k_ruler_wyllie<<<g, kBlock, 0, h.stream>>>(R, wa, wb);
     CK_LAUNCH();
-    h.stats.step(R);
+    h.stats.step(R_static);
     std::swap(wa, wb);
   }
   k_ruler_extract<<<g, kBlock, 0, h.stream>>>(R, wa, rstart);
   CK_LAUNCH();
-  h.stats.step(R);
+  h.stats.step(R_static);
   if (verify) {
     int* bad = reinterpret_cast<int*>(h.dev_box + 52);
     CK(cudaMemsetAsync(bad, 0, sizeof(int), h.stream));

@@ -285,10 +285,13 @@ int64_t bfs_rst(Handle& h, int32_t root, int32_t* parent, int32_t* level, int32_
   CK(cudaStreamSynchronize(s));
   const int levels_root = *reinterpret_cast<int*>(h.host_box);
   h.stats.levels = levels_root;
-  h.stats.steps += levels_root + 2;  // init + one barrier per level + the empty one
+  // one barrier per level plus the final empty level (with the init step:
+  // depth + 2 for a connected graph, bfs_rst.hpp:19)
+  h.stats.steps += levels_root + 1;
 
   // Anything unreached? Seed every other component at its smallest vertex.
   const uint32_t unvisited = scan_emit(h, n, Unvisited{level}, Nop{}, true);
+  h.stats.steps -= 1;  // the restart scan belongs to the final level (bfs_rst.cpp:58)
   *reinterpret_cast<int32_t*>(h.host_box) = root;
   CK(cudaMemcpyAsync(roots, h.host_box, sizeof(int32_t), cudaMemcpyHostToDevice, s));
   if (unvisited == 0) {

@@ -35,7 +35,7 @@ void cc_reset_rounds(Handle& h);
 void launch_compress2(Handle& h, int32_t* rep, int64_t n);
 void generate_kron_part(Handle& h, int scale, int ef, int part, int nparts);
 const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ, int stride,
-                                 const uint32_t* heads, int64_t H, unsigned long long* sl,
+                                 const uint32_t* heads, int64_t H, uint32_t* sl,
                                  int64_t* R_out, bool verify);
 }  // namespace rstg
 
@@ -165,16 +165,16 @@ struct NoPredFlag {
   const uint8_t* has;
   __device__ uint32_t operator()(int64_t p) const { return has[p] ? 0u : 1u; }
 };
-__global__ void k_rank_cover(int64_t E, const unsigned long long* sl, const uint32_t* rstart,
-                             int64_t R, const uint32_t* rnext_dummy, uint32_t* rank, int* bad) {
+__global__ void k_rank_cover(int64_t E, const uint32_t* sl, const uint32_t* rstart, int64_t R,
+                             uint32_t* rank, int* bad) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < E;
        p += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long a = sl[p];
-    if (a == ~0ull || (int64_t)(a >> 32) >= R) {
+    const uint32_t a = sl[p];  // (ruler << 7) | offset
+    if (a == kNone32 || (int64_t)(a >> 7) >= R) {
       *bad = 1;
       continue;
     }
-    rank[p] = rstart[a >> 32] + (uint32_t)a;
+    rank[p] = rstart[a >> 7] + (a & 127u);
   }
 }
 __global__ void k_check_compressed(int64_t m, const int2* e, const int32_t* rep, int* bad) {
@@ -639,13 +639,13 @@ int rstg_k_list_rank(int64_t E, const int64_t* succ, int64_t* rank) {
     CK_LAUNCH();
     uint32_t* heads = h.ws<uint32_t>(WS_HEADS, E + 1);
     const int64_t H = scan_emit(h, E, NoPredFlag{has}, EmitCompact{heads}, true);
-    unsigned long long* sl = h.ws<unsigned long long>(WS_SL, E);
+    uint32_t* sl = h.ws<uint32_t>(WS_SL, E);
     int64_t R = 0;
     const uint32_t* rstart = list_rank_rulers(h, E, s, 1, heads, H, sl, &R, /*verify=*/true);
     uint32_t* rk = h.ws<uint32_t>(WS_ATO, E);
     int* bad = reinterpret_cast<int*>(h.dev_box + 50);
     CK(cudaMemset(bad, 0, sizeof(int)));
-    k_rank_cover<<<grid_for(E), kBlock, 0, h.stream>>>(E, sl, rstart, R, nullptr, rk, bad);
+    k_rank_cover<<<grid_for(E), kBlock, 0, h.stream>>>(E, sl, rstart, R, rk, bad);
     CK_LAUNCH();
     std::vector<uint32_t> hr((size_t)E);
     CK(cudaMemcpy(hr.data(), rk, E * 4, cudaMemcpyDeviceToHost));

@@ -209,8 +209,12 @@ void launch_jump_rounds(Handle& h, int32_t* rep, int64_t n) {
 // inside X or hit roots); a last gather rep[v] = rep[rep[v]] finishes.
 // Passes over all n: 3 (tile, compaction, final) instead of ~log2(depth);
 // the jumping runs on |X|, which is tiny for chains (path: one per tile).
+// 8K vertices per tile (32 KB of shared memory, two 1024-thread CTAs per
+// SM). Measured on the road mesh: 32K-vertex tiles (one CTA per SM) keep
+// more pointers inside the tile but lose more to the lower occupancy.
 constexpr int kTileV = 8192;
 constexpr int kTileThreads = 1024;
+constexpr size_t kTileSmem = kTileV * sizeof(int32_t);
 
 // Sources of the tile's pointers (fused with the level-1 resolve so the new
 // reps never round-trip through HBM before shortcutting):
@@ -237,7 +241,7 @@ struct RoundIO {
 template <int SRC>
 __global__ void __launch_bounds__(kTileThreads)
     k_tile_resolve(int64_t n, int32_t* rep, uint8_t* isx, RoundIO io) {
-  __shared__ int32_t s[kTileV];
+  extern __shared__ int32_t s[];  // kTileV entries (dynamic: 128 KB)
   __shared__ uint32_t s_cnt;
   const int64_t base = (int64_t)blockIdx.x * kTileV;
   const int cnt = (int)min((int64_t)kTileV, n - base);
@@ -353,12 +357,22 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
   uint32_t* list = h.ws<uint32_t>(WS_HEADS, n + 1);
   CK(cudaMemsetAsync(isx, 0, (size_t)n, h.stream));
   const unsigned tiles = (unsigned)((n + kTileV - 1) / kTileV);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_tile_resolve<kSrcApply>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kTileSmem));
+    CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRound0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kTileSmem));
+    CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kTileSmem));
+    attr_set = true;
+  }
   if (src == kSrcApply)
-    k_tile_resolve<kSrcApply><<<tiles, kTileThreads, 0, h.stream>>>(n, rep, isx, io);
+    k_tile_resolve<kSrcApply><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, isx, io);
   else if (src == kSrcRound0)
-    k_tile_resolve<kSrcRound0><<<tiles, kTileThreads, 0, h.stream>>>(n, rep, isx, io);
+    k_tile_resolve<kSrcRound0><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, isx, io);
   else
-    k_tile_resolve<kSrcRep><<<tiles, kTileThreads, 0, h.stream>>>(n, rep, isx, io);
+    k_tile_resolve<kSrcRep><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, isx, io);
   CK_LAUNCH();
   h.stats.step(n);
   const int64_t X = scan_emit(h, n, ByteFlag{isx}, EmitCompact{list}, true);

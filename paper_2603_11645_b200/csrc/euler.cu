@@ -25,7 +25,7 @@
 namespace rstg {
 
 const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ, int stride,
-                                 const uint32_t* heads, int64_t H, unsigned long long* sl,
+                                 const uint32_t* heads, int64_t H, uint32_t* sl,
                                  int64_t* R_out, bool verify);
 
 // min_vertex per label (euler_rooting.cpp:190-195); labels are vertex ids.
@@ -124,7 +124,7 @@ struct EmitHeadArc {
 
 // derive_parents (:172-176) on (ruler, offset) ranks; from(p) = to(rev p).
 __global__ void __launch_bounds__(kBlock)
-    k_orient(int64_t E, const uint2* __restrict__ arc, const unsigned long long* __restrict__ sl,
+    k_orient(int64_t E, const uint2* __restrict__ arc, const uint32_t* __restrict__ sl,
              const uint32_t* __restrict__ rstart, int32_t* __restrict__ parent) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < E;
        p += (int64_t)gridDim.x * blockDim.x) {
@@ -132,9 +132,9 @@ __global__ void __launch_bounds__(kBlock)
     const uint32_t q = ap.y;
     if ((uint32_t)p > q) continue;
     const uint32_t to_q = arc[q].x;  // = from(p)
-    const unsigned long long a = sl[p], b = sl[q];
-    const uint32_t rp = rstart[a >> 32] + (uint32_t)a;
-    const uint32_t rq = rstart[b >> 32] + (uint32_t)b;
+    const uint32_t a = sl[p], b = sl[q];  // (ruler << 7) | offset
+    const uint32_t rp = rstart[a >> 7] + (a & 127u);
+    const uint32_t rq = rstart[b >> 7] + (b & 127u);
     // the higher-ranked arc returns from the child: parent[from] = to
     if (rp > rq)
       parent[to_q] = (int32_t)ap.x;
@@ -187,7 +187,7 @@ void euler_root(Handle& h, const int32_t* labels, const uint32_t* tsrc, int64_t 
   const int64_t H = scan_emit(h, n, HeadFlag{isroot, tf}, EmitHeadArc{tf, heads}, true);
   h.timer.end(h.stream);
 
-  unsigned long long* sl = h.ws<unsigned long long>(WS_SL, E);
+  uint32_t* sl = h.ws<uint32_t>(WS_SL, E);
   int64_t R = 0;
   const uint32_t* rstart = list_rank_rulers(h, E, succ, 1, heads, H, sl, &R, verify);
   h.timer.begin(h.stream, "euler.orient");

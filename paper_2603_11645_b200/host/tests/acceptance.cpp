@@ -76,6 +76,7 @@ std::vector<Vertex> forest_labels(const std::vector<Vertex>& parent) {
 }  // namespace
 
 int main() {
+  std::setvbuf(stdout, nullptr, _IOLBF, 0);
   std::printf("rooted spanning tree acceptance suite (B200 engine)\n");
   struct DS {
     std::string name;
@@ -101,7 +102,8 @@ int main() {
     std::string bad;
     for (std::size_t d = 0; d < suite.size(); ++d) {
       const Graph& g = suite[d].g;
-      const auto comps = std::set<Vertex>(oracle_components(g).begin(), oracle_components(g).end());
+      const std::vector<Vertex> labels = oracle_components(g);
+      const std::set<Vertex> comps(labels.begin(), labels.end());
       for (std::size_t a = 0; a < 3; ++a) {
         ++total;
         const RootedForest& f = runs[d][a].forest;

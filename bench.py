@@ -132,7 +132,7 @@ def phase_bytes(phase, n, m, E):
         "cc.compress": 8 * n,        # rep read + write
         "euler.arcs": 17 * m * 2 + 4 * n,  # arc_edge + flag + pos(w) + pos(r) + nbrs ... per arc
         "euler.succ": 24 * E,        # ato, afrom, tf x2, 2 searches, succ, rev
-        "lr.walk": 12 * E,           # succ read + (ruler, offset) write per arc
+        "lr.walk": 8 * E,            # succ read (4 B) + (ruler, offset) word write (4 B) per arc
         "lr.rulers": 8 * E,
         "lr.rulers_rank": 0,
         "euler.orient": 24 * E // 2 + 4 * n,

@@ -324,3 +324,34 @@ def test_distcc_simulated_ranks_on_one_gpu(rst, O):
         parts[0].cc_compress(rep.data_ptr())
         mode ^= 1
     assert np.array_equal(rep.cpu().numpy().astype(np.int64), labels)
+
+
+# ---- BASELINE.json configs at full size ---------------------------------------
+# Device-generated graph (the bench's input), copied out and handed to the
+# oracle as the same normalized edge list; every strategy bit-exact against
+# it. The device generators equal the host ones (test_device_generators_
+# match_host above, and the survey's m / component counts below).
+FULL = [("grid:1024:1024", 2095104), ("path:16777216", 16777215), ("road:4899", 28858008),
+        ("kron:24:16", 260382979)]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("spec,m_expect", FULL, ids=[s for s, _ in FULL])
+def test_full_size_configs(rst, O, spec, m_expect):
+    dg = rst.DeviceGraph.generate(spec)
+    assert dg.m == m_expect
+    e = dg.edges()
+    g = O.Graph(dg.n, e[:, 0], e[:, 1])
+    del e
+    root = 0
+    if spec.startswith("kron"):
+        root = int(np.argmax(np.diff(g.offsets)))  # max degree, smallest id on ties
+    for algo in ALGOS:
+        p, r, lv, _ = dg.run(algo, root)
+        ep, er, elv = O.run(g, algo, root)
+        assert np.array_equal(p, ep), f"{spec} algo {algo}: parent mismatch at {np.nonzero(p != ep)[0][:10]}"
+        assert np.array_equal(r, er), f"{spec} algo {algo}: roots mismatch"
+        if algo == 0:
+            assert np.array_equal(lv, elv), f"{spec}: bfs levels mismatch"
+        assert dg.validate(p, root)[0]
+    dg.close()

@@ -25,19 +25,26 @@ if [ -z "$SKIP_EXTRA" ]; then
     timeout 300 python bench.py --algo $A --no-e2e --no-cpu-baseline --no-bfs-ratio > $O/bench_road_${A}.json 2> $O/bench_road_${A}.err
   done
 fi
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 for W in ${NCU_WORKLOADS:-road}; do
-  timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+  # per kernel, then per phase (NVTX ranges of the phase timer), 2 builds each
+  timeout 600 ncu --profile-from-start off --metrics $M --clock-control none --csv \
     --log-file $O/launches_${W}.csv python scripts/profile_step.py --workload $W --builds 2 > $O/ncu_launch_${W}.log 2>&1
-  python scripts/ncu_top.py $O/launches_${W}.csv > $O/launches_${W}_summary.txt; cat $O/launches_${W}_summary.txt
+  python scripts/ncu_top.py $O/launches_${W}.csv --builds 2 --json $O/kernels_${W}.json > $O/launches_${W}_summary.txt
+  timeout 600 ncu --profile-from-start off --nvtx --print-nvtx-rename kernel --metrics $M --clock-control none --csv \
+    --log-file $O/phases_${W}.csv python scripts/profile_step.py --workload $W --builds 2 > $O/ncu_phase_${W}.log 2>&1
+  python scripts/ncu_top.py $O/phases_${W}.csv --builds 2 --json $O/phases_${W}.json > $O/phases_${W}_summary.txt
+  cat $O/launches_${W}_summary.txt $O/phases_${W}_summary.txt
 done
 if [ -z "$SKIP_FULL" ]; then
-  TOPK=$(python scripts/ncu_top.py $O/launches_road.csv --names --top ${NCU_TOP:-4})
-  echo "full capture of: $TOPK"
-  timeout 1500 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k "regex:^(${TOPK})" -c ${NCU_COUNT:-8} -o $O/prof_${TAG} python scripts/profile_step.py --workload road > $O/ncu_full.log 2>&1
-  ncu -i $O/prof_${TAG}.ncu-rep --page raw --csv > $O/prof_${TAG}_raw.csv 2>/dev/null
-  ncu -i $O/prof_${TAG}.ncu-rep --page details --csv > $O/prof_${TAG}_details.csv 2>/dev/null
-  sz=$(stat -c %s $O/prof_${TAG}.ncu-rep 2>/dev/null || echo 0)
-  if [ "$sz" -gt 40000000 ]; then rm -f $O/prof_${TAG}.ncu-rep; echo "ncu-rep too large ($sz), removed"; fi
+  # one --set full capture per top kernel (first launch inside the profiled build)
+  for K in $(python scripts/ncu_top.py $O/launches_road.csv --names --top ${NCU_TOP:-5} | tr '|' ' '); do
+    timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on \
+      -k "regex:^${K}" -c 1 -o $O/prof_${TAG}_${K} python scripts/profile_step.py --workload road > $O/ncu_full_${K}.log 2>&1
+    ncu -i $O/prof_${TAG}_${K}.ncu-rep --page raw --csv > $O/prof_${TAG}_${K}_raw.csv 2>/dev/null
+    ncu -i $O/prof_${TAG}_${K}.ncu-rep --page details --csv > $O/prof_${TAG}_${K}_details.csv 2>/dev/null
+    sz=$(stat -c %s $O/prof_${TAG}_${K}.ncu-rep 2>/dev/null || echo 0)
+    if [ "$sz" -gt 12000000 ]; then rm -f $O/prof_${TAG}_${K}.ncu-rep; echo "ncu-rep $K too large ($sz), removed"; fi
+  done
 fi
 du -sh $O

@@ -1,33 +1,48 @@
 #!/usr/bin/env python
-"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv).
+"""Summarise an ncu launch list (--csv, one row per kernel launch and metric).
 
-    python scripts/ncu_top.py launches.csv [--skip-before REGEX] [--top K] [--names]
+    python scripts/ncu_top.py launches.csv [--builds B] [--top K] [--names] [--json OUT]
 
-Prints per-kernel totals (count, total us, share) over the launches after the
-first launch matching --skip-before (e.g. the first timed-step kernel), or
-with --names only the top-K kernel base names (for ncu -k regex:...).
+Per kernel name (or per NVTX phase when the list was captured with
+--nvtx --print-nvtx-rename kernel): launches, total device time, share, and
+DRAM bytes read+written when those metrics were collected -- all divided by
+--builds (the number of RST builds inside the profiled range). --names
+prints the top-K kernel base names joined by '|' (for ncu -k regex:...).
+--json writes {name: {"us": .., "launches": .., "dram_bytes": ..}} per build.
 """
 import argparse
 import collections
 import csv
+import json
 import re
 import sys
 
+SCALE_T = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+           "second": 1e6, "s": 1e6}
+SCALE_B = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
-def rows(path):
+
+def launches(path):
     with open(path) as f:
         lines = [ln for ln in f if ln.startswith('"')]
-    rd = csv.DictReader(lines)
-    for r in rd:
-        if r.get("Metric Name") != "gpu__time_duration.sum":
-            continue
-        unit = r.get("Metric Unit", "nsecond")
-        v = float(r["Metric Value"].replace(",", ""))
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1e-3)
-        yield r["Kernel Name"], v * scale
+    per = collections.OrderedDict()
+    for r in csv.DictReader(lines):
+        key = r.get("ID") or str(len(per))
+        d = per.setdefault(key, {"name": r["Kernel Name"]})
+        unit = r.get("Metric Unit", "")
+        v = float(r["Metric Value"].replace(",", "") or 0)
+        mn = r["Metric Name"]
+        if mn == "gpu__time_duration.sum":
+            d["us"] = v * SCALE_T.get(unit, 1e-3)
+        elif mn in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            d["dram"] = d.get("dram", 0.0) + v * SCALE_B.get(unit, 1)
+    return list(per.values())
 
 
 def base(name):
+    head = name.split("(")[0]
+    if "/" in head:  # NVTX-renamed: "<phase>/<kernel>(...)" -> phase
+        return head.split("/")[0]
     name = re.sub(r"^void ", "", name)
     name = name.split("(")[0]
     return re.sub(r"<.*", "", name).split("::")[-1]
@@ -36,30 +51,42 @@ def base(name):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("csv")
-    ap.add_argument("--skip-before", default=None)
-    ap.add_argument("--top", type=int, default=25)
+    ap.add_argument("--builds", type=float, default=1.0)
+    ap.add_argument("--top", type=int, default=30)
     ap.add_argument("--names", action="store_true")
+    ap.add_argument("--json", default=None)
     a = ap.parse_args()
-    data = list(rows(a.csv))
-    if a.skip_before:
-        for i, (k, _) in enumerate(data):
-            if re.search(a.skip_before, k):
-                data = data[i:]
-                break
+    data = launches(a.csv)
     tot = collections.defaultdict(float)
+    dram = collections.defaultdict(float)
     cnt = collections.Counter()
-    for k, us in data:
-        tot[base(k)] += us
-        cnt[base(k)] += 1
-    total = sum(tot.values())
+    have_dram = any("dram" in d for d in data)
+    for d in data:
+        k = base(d["name"])
+        tot[k] += d.get("us", 0.0)
+        dram[k] += d.get("dram", 0.0)
+        cnt[k] += 1
+    total = sum(tot.values()) or 1.0
     order = sorted(tot, key=lambda k: -tot[k])
     if a.names:
         print("|".join(order[: a.top]))
         return
-    print(f"{'kernel':32s} {'launches':>8s} {'total_us':>10s} {'share':>7s}")
+    B = a.builds
+    if a.json:
+        with open(a.json, "w") as f:
+            json.dump({k: {"us": tot[k] / B, "launches": cnt[k] / B,
+                           "dram_bytes": dram[k] / B if have_dram else None} for k in order}, f,
+                      indent=1)
+    hdr = f"{'name':34s} {'launches':>8s} {'us/build':>10s} {'share':>7s}"
+    if have_dram:
+        hdr += f" {'DRAM MB/build':>14s} {'GB/s':>8s}"
+    print(hdr)
     for k in order[: a.top]:
-        print(f"{k:32s} {cnt[k]:8d} {tot[k]:10.1f} {tot[k] / total:7.1%}")
-    print(f"{'TOTAL':32s} {sum(cnt.values()):8d} {total:10.1f}")
+        line = f"{k:34s} {cnt[k] / B:8.1f} {tot[k] / B:10.1f} {tot[k] / total:7.1%}"
+        if have_dram:
+            line += f" {dram[k] / B / 1e6:14.1f} {dram[k] / (tot[k] * 1e3) if tot[k] else 0:8.0f}"
+        print(line)
+    print(f"{'TOTAL':34s} {sum(cnt.values()) / B:8.1f} {total / B:10.1f}")
 
 
 if __name__ == "__main__":

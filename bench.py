@@ -68,76 +68,119 @@ def parse():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi samples during the timed region (B200_PROFILING.md)."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region (B200_PROFILING.md). NVML directly, every 2 ms: a whole timed
+    region of a few-ms build is only tens of ms long, shorter than the
+    nvidia-smi -lms floor. Falls back to nvidia-smi when NVML is absent."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index):
+    def __init__(self, index, period_s=0.002):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.samples = []  # (sm_mhz, reason bitmask)
+        self.max_mhz = None
+        self.stop = threading.Event()
+        self.nv = None
+        self.smi = []
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].isdigit() else self.index
+            self.h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.nv = nv
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _sample(self):
+        nv = self.nv
+        self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                             nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+
+    def _loop(self):
+        while not self.stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        self.stop.set()
+        if self.nv:
+            self.t.join(timeout=1)
             try:
-                self.proc.wait(timeout=2)
+                self._sample()  # at least one sample at the end of the region
             except Exception:
-                self.proc.kill()
+                pass
+        else:
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      "--query-gpu=clocks.sm,clocks.max.sm",
+                                      "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=10).stdout
+                sm, mx = [float(x) for x in out.strip().split(",")[:2]]
+                self.samples.append((sm, 0))
+                self.max_mhz = mx
+            except Exception:
+                pass
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = set()
+        if self.nv:
+            for name, attr in self.REASONS:
+                bit = getattr(self.nv, attr, 0)
+                if any(r & bit for _, r in self.samples):
+                    reasons.add(name)
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.nv else "nvidia-smi"}
 
 
 # --------------------------------------------------------- roofline model
 def phase_bytes(phase, n, m, E):
-    """Algorithmic (compulsory) bytes of one launch of each phase."""
+    """Algorithmic (compulsory) bytes of one build's worth of a phase:
+    each array element the phase must touch, once."""
+    T = E // 2
+    R = E // 32 + 1
     return {
-        "cc.hook_min": 16 * m,       # edge (8 B) + 2 rep gathers (4 B each)
+        "cc.init": 16 * n,                  # rep 4 + slot 8 + tree-edge slot 4 per vertex
+        "cc.round0": 4 * (n + 1) + 16 * n,  # offsets + first neighbour/edge id 8 + rep 4 + tree edge 4
+        "cc.hook_min": 16 * m,              # edge 8 + two rep gathers 4+4 (first visit; upper bound)
         "cc.hook_max": 16 * m,
-        "cc.apply": 8 * n,           # slot read
-        "cc.compress": 8 * n,        # rep read + write
-        "euler.arcs": 17 * m * 2 + 4 * n,  # arc_edge + flag + pos(w) + pos(r) + nbrs ... per arc
-        "euler.succ": 24 * E,        # ato, afrom, tf x2, 2 searches, succ, rev
-        "lr.walk": 8 * E,            # succ read (4 B) + (ruler, offset) word write (4 B) per arc
-        "lr.rulers": 8 * E,
-        "lr.rulers_rank": 0,
-        "euler.orient": 24 * E // 2 + 4 * n,
-        "euler.roots": 12 * n,
+        "cc.apply_compress": 16 * n,        # slot 8 + rep read/write 8 per vertex
+        "euler.roots": 12 * n,              # labels 4 + min-vertex table 4 + parent 4
+        "euler.arcs": 30 * T,               # tree list 4 + edge 8 per tree edge; arc 8 + succ 4 per arc
+        "lr.rulers": 8 * R,                 # ruler position + word
+        "lr.walk": 8 * E,                   # succ read 4 + (ruler, offset) word write 4 per arc
+        "lr.rulers_rank": 16 * R,           # ruler list prefix (one pass)
+        "euler.orient": 14 * E,             # arc pair 16 + words 8 + parent write 4 per tree edge
     }.get(phase)
+
+
+def profiled_traffic(workload, algo, phase):
+    """DRAM bytes (read + write) per build of `phase`, from the committed ncu
+    capture of the same workload (profiles/phase_traffic.json, written by
+    scripts/ncu_top.py from an `ncu --nvtx --print-nvtx-rename kernel` launch
+    list with dram__bytes_{read,write}.sum). None when not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "phase_traffic.json")) as f:
+            t = json.load(f)
+        return t[workload][algo]["phases"][phase]["dram_bytes"], t[workload][algo]["source"]
+    except Exception:
+        return None, None
 
 
 def measured_peaks():
@@ -351,22 +394,26 @@ def main():
     # ---- roofline of the dominant kernel (phase) ----
     E = 2 * (n - int((parent_host == np.arange(n)).sum()))
     peaks, peak_kind = measured_peaks()
-    # per phase: mean over steps of (total ms in the step, launches in the step)
-    agg = {k: (statistics.mean(x[0] for x in v), statistics.mean(x[1] for x in v))
+    # per phase: mean over steps of (ms in the step, records in the step,
+    # algorithmic bytes the library attributes to the phase -- DESIGN.md §3)
+    agg = {k: (statistics.mean(x[0] for x in v), statistics.mean(x[1] for x in v),
+               statistics.mean((x[2] if len(x) > 2 else 0) for x in v))
            for k, v in phases.items()}
     dominant = max(agg, key=lambda k: agg[k][0]) if agg else None
     roofline = None
     if dominant:
-        per_step_ms, per_step_launches = agg[dominant]
-        b = phase_bytes(dominant, n, m, E)  # algorithmic bytes of the phase per step
+        per_step_ms, per_step_launches, lib_bytes = agg[dominant]
+        # algorithmic bytes of the phase per step (library figure, else the model)
+        b = lib_bytes or phase_bytes(dominant, n, m, E)
         achieved = (b / (per_step_ms / 1e3) / 1e9) if b else None
+        traffic, traffic_src = profiled_traffic(args.workload, args.algo, dominant)
         roofline = {"bound": "hbm", "kernel": dominant, "achieved": achieved,
                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
-                    "traffic": None, "peak_kind": peak_kind,
+                    "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
                     "algorithmic_bytes_per_step": b, "kernel_ms_per_step": per_step_ms,
-                    "launches_per_step": per_step_launches,
-                    "avg_launch_ms": per_step_ms / max(per_step_launches, 1),
+                    "phase_records_per_step": per_step_launches,
+                    "unit_of_launch": "one build's worth of the phase (all its kernel launches)",
                     "share_of_step": per_step_ms / ms_per_step}
     b_alg = 4 * (n + 1) + 8 * m + 4 * n
     step_roofline = {"b_alg": b_alg, "achieved_gbs": b_alg / (ms_per_step / 1e3) / 1e9,
@@ -425,7 +472,7 @@ def main():
             "config": config, "n": n, "m": m, "valid": bool(valid),
             "roofline": roofline, "step_roofline": step_roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "phases_ms_per_step": {k: [round(v[0], 4), v[1]] for k, v in agg.items()},
+            "clocks": clk.summary(), "phases_ms_per_step": {k: [round(v[0], 4), v[1], v[2]] for k, v in agg.items()},
             "bfs_baseline": bfs,
         }
         print(json.dumps(line), flush=True)

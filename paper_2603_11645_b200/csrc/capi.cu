@@ -34,10 +34,9 @@ void cc_round_done(Handle& h, int64_t out_count);
 void cc_reset_rounds(Handle& h);
 void launch_compress2(Handle& h, int32_t* rep, int64_t n);
 void generate_kron_part(Handle& h, int scale, int ef, int part, int nparts);
-const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ, int stride,
-                                 const uint32_t* heads, int64_t H, uint32_t* sl,
-                                 int64_t* R_out, bool verify);
 }  // namespace rstg
+
+#include "listrank.cuh"
 
 using namespace rstg;
 
@@ -117,9 +116,10 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
     nroots = bfs_rst(h, (int32_t)root, parent, levels, roots);
   } else if (algo == RSTG_CC_EULER) {
     int32_t* labels = h.ws<int32_t>(WS_REP, h.g.n);
-    uint32_t* tlist = h.ws<uint32_t>(WS_TLIST, h.g.n);
-    const int64_t T = cc_exact(h, labels, nullptr, tlist);
-    euler_root(h, labels, tlist, h.g.n, T, (int32_t)root, parent);
+    // round 0 runs from the CSR (and writes every local list) when there is one
+    const EulerIO io = euler_buffers(h, h.g.n, h.g.has_csr() && h.g.m > 0);
+    const int64_t T = cc_exact(h, labels, nullptr, &io);
+    euler_root(h, labels, io, h.g.n, T, /*cc_slots=*/true, (int32_t)root, parent);
   } else if (algo == RSTG_PR_RST) {
     pr_rst(h, (int32_t)root, jump_batch, parent);
   } else {
@@ -134,47 +134,40 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
   CK(cudaEventDestroy(e1));
   h.stats.device_ms = ms;
   if (nroots >= 0) h.stats.components = nroots;
-  // phase times
-  // phase times: {"name": [total_ms, launches_of_phase], ...} in first-seen order
+  // phase times: {"name": [total_ms, records, algorithmic_bytes], ...} in first-seen order
   auto ph = h.timer.collect();
-  std::vector<std::pair<std::string, std::pair<double, int>>> agg;
+  struct Agg {
+    std::string name;
+    double ms, bytes;
+    int count;
+  };
+  std::vector<Agg> agg;
   for (auto& p : ph) {
-    auto it = std::find_if(agg.begin(), agg.end(), [&](auto& a) { return a.first == p.first; });
+    auto it = std::find_if(agg.begin(), agg.end(), [&](const Agg& a) { return a.name == p.name; });
     if (it == agg.end())
-      agg.push_back({p.first, {p.second, 1}});
+      agg.push_back({p.name, p.ms, p.bytes, 1});
     else
-      it->second.first += p.second, it->second.second += 1;
+      it->ms += p.ms, it->bytes += p.bytes, it->count += 1;
   }
   std::string js = "{";
   for (size_t i = 0; i < agg.size(); ++i) {
     if (i) js += ",";
-    js += "\"" + agg[i].first + "\":[" + std::to_string(agg[i].second.first) + "," +
-          std::to_string(agg[i].second.second) + "]";
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "\"%s\":[%.6f,%d,%.0f]", agg[i].name.c_str(), agg[i].ms,
+                  agg[i].count, agg[i].bytes);
+    js += buf;
   }
   g->phases_json = js + "}";
   return nroots;
 }
 
-// pred marks -> heads for rstg_k_list_rank
-__global__ void k_has_pred(int64_t E, const uint32_t* succ, uint8_t* has) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < E;
-       p += (int64_t)gridDim.x * blockDim.x)
-    if (succ[p] != kNone32) has[succ[p]] = 1;
-}
-struct NoPredFlag {
-  const uint8_t* has;
-  __device__ uint32_t operator()(int64_t p) const { return has[p] ? 0u : 1u; }
-};
-__global__ void k_rank_cover(int64_t E, const uint32_t* sl, const uint32_t* rstart, int64_t R,
-                             uint32_t* rank, int* bad) {
+// rank of every position from its (ruler, offset) word (rstg_k_list_rank)
+__global__ void k_rank_cover(int64_t E, const uint32_t* sl, const uint32_t* rstart, int ob,
+                             uint32_t* rank) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < E;
        p += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t a = sl[p];  // (ruler << 7) | offset
-    if (a == kNone32 || (int64_t)(a >> 7) >= R) {
-      *bad = 1;
-      continue;
-    }
-    rank[p] = rstart[a >> 7] + (a & 127u);
+    const uint32_t a = sl[p];  // (ruler << ob) | offset
+    rank[p] = rstart[a >> ob] + (a & ((1u << ob) - 1u));
   }
 }
 __global__ void k_check_compressed(int64_t m, const int2* e, const int32_t* rep, int* bad) {
@@ -499,7 +492,10 @@ int rstg_euler_root_forest(int64_t n, const int64_t* tree_uv, int64_t T, const i
     to_device<int32_t>(h, labels, n, lab);
     int32_t* parent = h.ws<int32_t>(WS_PARENT, n);
     if (!simple) throw AlgoError("list ranking failed to converge: not a forest");
-    euler_root(h, lab, nullptr, T, T, (int32_t)designated_root, parent, /*verify=*/true);
+    const EulerIO io = euler_buffers(h, T, /*local_written=*/false);
+    euler_link_edges(h, io, T);
+    euler_root(h, lab, io, T, T, /*cc_slots=*/false, (int32_t)designated_root, parent,
+               /*verify=*/true);
     // Not a forest iff some vertex is unreachable from its root: validate
     // the orientation by doubling (a cycle never resolves to a root).
     {
@@ -633,19 +629,11 @@ int rstg_k_list_rank(int64_t E, const int64_t* succ, int64_t* rank) {
     std::vector<uint32_t> hs((size_t)E);
     for (int64_t p = 0; p < E; ++p) hs[(size_t)p] = succ[p] < 0 ? kNone32 : (uint32_t)succ[p];
     CK(cudaMemcpy(s, hs.data(), E * 4, cudaMemcpyHostToDevice));
-    uint8_t* has = h.ws<uint8_t>(WS_ISROOT, E);
-    CK(cudaMemset(has, 0, (size_t)E));
-    k_has_pred<<<grid_for(E), kBlock, 0, h.stream>>>(E, s, has);
-    CK_LAUNCH();
-    uint32_t* heads = h.ws<uint32_t>(WS_HEADS, E + 1);
-    const int64_t H = scan_emit(h, E, NoPredFlag{has}, EmitCompact{heads}, true);
     uint32_t* sl = h.ws<uint32_t>(WS_SL, E);
-    int64_t R = 0;
-    const uint32_t* rstart = list_rank_rulers(h, E, s, 1, heads, H, sl, &R, /*verify=*/true);
-    uint32_t* rk = h.ws<uint32_t>(WS_ATO, E);
-    int* bad = reinterpret_cast<int*>(h.dev_box + 50);
-    CK(cudaMemset(bad, 0, sizeof(int)));
-    k_rank_cover<<<grid_for(E), kBlock, 0, h.stream>>>(E, sl, rstart, R, rk, bad);
+    LrParams P;
+    const uint32_t* rstart = lr_rank_lists(h, E, s, sl, /*verify=*/true, &P);
+    uint32_t* rk = h.ws<uint32_t>(WS_ETO, E);
+    k_rank_cover<<<grid_for(E), kBlock, 0, h.stream>>>(E, sl, rstart, P.ob, rk);
     CK_LAUNCH();
     std::vector<uint32_t> hr((size_t)E);
     CK(cudaMemcpy(hr.data(), rk, E * 4, cudaMemcpyDeviceToHost));

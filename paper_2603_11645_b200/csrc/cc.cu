@@ -10,11 +10,17 @@
 //   * apply (cc_forest.cpp:39-46): rep[v] = winner, tree_flag[e] = 1.
 //   * jump_to_convergence (cc_forest.cpp:50-71): the Jacobi fixed point is
 //     "every vertex points at the root of its rep tree", which does not
-//     depend on the evaluation order, so one asynchronous path-halving
-//     kernel replaces the ceil(log2 L) doubling barriers.
+//     depend on the evaluation order, so two-level shortcutting (shared-
+//     memory tiles, then the exit set in one cooperative launch) replaces
+//     the ceil(log2 L) doubling barriers over all n.
+//   * the apply step (and the CSR-direct round 0) also links every new
+//     tree edge into the Euler rotation lists (link_tree_edge), so the
+//     Euler construction needs no pass of its own.
 // Hook rounds stay synchronous: proposals read
 // reps frozen by the previous kernel boundary.
 #include <cooperative_groups.h>
+
+#include <algorithm>
 
 #include "engine.hpp"
 #include "scan.cuh"
@@ -126,89 +132,17 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-// Asynchronous pointer jumping to the fixed point of
-// jump_to_convergence: every rep[v] ends at the root of v's rep tree.
-// Each step reads an ancestor; any value ever stored in rep[x] is a proper
-// ancestor of x (roots never change), so the walk strictly ascends and the
-// path-halving stores only shorten other threads' walks.
-__global__ void __launch_bounds__(kBlock) k_compress(int64_t n, int32_t* rep) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    int32_t p = rep[v];
-    if (p == (int32_t)v) continue;
-    int32_t gp = ld_cg(&rep[p]);
-    if (gp == p) continue;
-    do {
-      rep[v] = gp;
-      p = gp;
-      gp = ld_cg(&rep[p]);
-    } while (gp != p);
-  }
-}
-
-// One in-place doubling round rep[v] = rep[rep[v]] (the Jacobi step of
-// jump_to_convergence, evaluated in place: a fresher read only jumps
-// further). A round that changes nothing proves every rep[v] is a root
-// (roots are the only fixed points of a forest), so later rounds exit on
-// the device without a host round trip.
-template <int HOPS>
-__global__ void __launch_bounds__(kBlock) k_jump_round(int64_t n, int32_t* rep, int* flags,
-                                                       int round) {
-  if (round > 0 && flags[round - 1] == 0) return;
-  bool changed = false;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t p = rep[v];
-    int32_t x = rep[p];
-    if (x == p) continue;
-#pragma unroll
-    for (int hop = 1; hop < HOPS; ++hop) {
-      const int32_t y = rep[x];
-      if (y == x) break;
-      x = y;
-    }
-    rep[v] = x;
-    changed = true;
-  }
-  block_flag(changed, &flags[round]);
-}
-
-static int jump_hops() {
-  static int hops = 0;
-  if (hops == 0) {
-    const char* e = getenv("RSTG_JUMP_HOPS");
-    hops = e ? atoi(e) : 1;
-    if (hops != 1 && hops != 2 && hops != 4 && hops != 8) hops = 1;
-  }
-  return hops;
-}
-
-void launch_jump_rounds(Handle& h, int32_t* rep, int64_t n) {
-  int rounds = 2;
-  while ((int64_t{1} << (rounds - 2)) < n) ++rounds;  // ceil(log2 n) + 2
-  int* flags = reinterpret_cast<int*>(h.dev_box + 128);  // 64 ints (dev_box[128..159])
-  CK(cudaMemsetAsync(flags, 0, 64 * sizeof(int), h.stream));
-  const unsigned g = grid_for(n);
-  const int hops = jump_hops();
-  for (int r = 0; r < rounds && r < 64; ++r) {
-    if (hops == 1) k_jump_round<1><<<g, kBlock, 0, h.stream>>>(n, rep, flags, r);
-    else if (hops == 2) k_jump_round<2><<<g, kBlock, 0, h.stream>>>(n, rep, flags, r);
-    else if (hops == 4) k_jump_round<4><<<g, kBlock, 0, h.stream>>>(n, rep, flags, r);
-    else k_jump_round<8><<<g, kBlock, 0, h.stream>>>(n, rep, flags, r);
-    h.stats.step(n);
-  }
-  CK_LAUNCH();
-}
-
 // ---- two-level shortcutting ---------------------------------------------
 // Level 1 (k_tile_resolve): each CTA owns a tile of kTileV consecutive
 // vertices held in shared memory and follows every pointer while it stays
 // inside the tile (in-smem doubling), so rep[v] becomes either a root or the
-// first ancestor outside v's tile. Those out-of-tile targets X are flagged.
-// Level 2: X is compacted and pointer-jumped on its own (its pointers stay
-// inside X or hit roots); a last gather rep[v] = rep[rep[v]] finishes.
-// Passes over all n: 3 (tile, compaction, final) instead of ~log2(depth);
-// the jumping runs on |X|, which is tiny for chains (path: one per tile).
+// first ancestor outside v's tile. Those out-of-tile targets X are appended
+// (deduplicated by a bitmap, warp-aggregated) to a list as they are found.
+// Level 2: one cooperative kernel pointer-jumps X in place (its pointers
+// stay inside X or hit roots), a grid barrier per doubling round, stopping
+// on the device once a round changes nothing; a last gather
+// rep[v] = rep[rep[v]] finishes. Passes over all n: 2 (tile, final gather)
+// instead of ~log2(depth), no host round trip.
 // 8K vertices per tile (32 KB of shared memory, two 1024-thread CTAs per
 // SM). Measured on the road mesh: 32K-vertex tiles (one CTA per SM) keep
 // more pointers inside the tile but lose more to the lower occupancy.
@@ -229,28 +163,41 @@ enum { kSrcRep = 0, kSrcApply = 1, kSrcRound0 = 2 };
 
 struct RoundIO {
   unsigned long long* slot;
-  uint8_t* tflag;
-  uint32_t* tedge;
+  uint8_t* tflag;               // tree-edge flags by local edge id (nullable)
   uint32_t e_base, m_local;
   unsigned long long* counter;  // += hooks applied
   const uint32_t* offsets;
   const int32_t* nbrs;
   const uint32_t* arc_edge;
+  const int2* edges;
+  bool link;                    // link new tree edges into the Euler rotation lists
+  EulerIO eu;
 };
 
 template <int SRC>
 __global__ void __launch_bounds__(kTileThreads)
-    k_tile_resolve(int64_t n, int32_t* rep, uint8_t* isx, RoundIO io) {
-  extern __shared__ int32_t s[];  // kTileV entries (dynamic: 128 KB)
+    k_tile_resolve(int64_t n, int32_t* rep, uint32_t* xbits, uint32_t* xlist,
+                   unsigned long long* xcount, RoundIO io) {
+  extern __shared__ int32_t s[];  // kTileV reps (+ 2 x kTileV list words when linking round 0)
   __shared__ uint32_t s_cnt;
   const int64_t base = (int64_t)blockIdx.x * kTileV;
   const int cnt = (int)min((int64_t)kTileV, n - base);
+  // Round 0 links its tree edges (u, v), u = v's first neighbour, into
+  // shared-memory rotation lists whenever u lies in the tile (nearly
+  // always: u is an adjacent id on meshes), then splices each tile list
+  // into the global one with a single atomic (see the flush below).
+  constexpr bool kLocal = SRC == kSrcRound0;
+  uint32_t* s_head = reinterpret_cast<uint32_t*>(s + kTileV);
+  uint32_t* s_tail = s_head + kTileV;
   if (threadIdx.x == 0) s_cnt = 0;
+  if (kLocal && io.link) {
+    for (int i = threadIdx.x; i < kTileV; i += kTileThreads) s_head[i] = kNone32;
+    __syncthreads();
+  }
   uint32_t hooked = 0;
   for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
     const int64_t v = base + i;
     int32_t r;
-    uint32_t eg = kNone32;
     if (SRC == kSrcRep) {
       r = rep[v];
     } else if (SRC == kSrcApply) {
@@ -258,27 +205,58 @@ __global__ void __launch_bounds__(kTileThreads)
       r = rep[v];
       if (key != kKeyInf) {
         r = (int32_t)(key >> 32);
-        eg = (uint32_t)key;
         io.slot[v] = kKeyInf;
+        ++hooked;
+        const uint32_t e = (uint32_t)key - io.e_base;
+        if (io.tflag && e < io.m_local) io.tflag[e] = 1;
+        if (io.link) {
+          const int2 ab = io.edges[e];
+          link_tree_edge(io.eu, (uint32_t)v, (uint32_t)ab.x, (uint32_t)ab.y);
+        }
       }
     } else {
       const uint32_t o = io.offsets[v];
       r = (int32_t)v;
       if (o < io.offsets[v + 1]) {
         const int32_t u = io.nbrs[o];
-        if (u < r) {
+        if (u < r) {  // hooked onto its smallest neighbour by edge (u, v)
           r = u;
-          eg = io.arc_edge[o] + io.e_base;
+          ++hooked;
+          if (io.tflag) {
+            const uint32_t e = io.arc_edge[o];
+            if (e < io.m_local) io.tflag[e] = 1;
+          }
+          if (io.link) {
+            const uint32_t pa = (uint32_t)v, qa = io.eu.nslots + (uint32_t)v;  // pa: u -> v, qa: v -> u
+            reinterpret_cast<uint2*>(io.eu.eto)[v] = make_uint2((uint32_t)v, (uint32_t)u);
+            const int64_t lu = (int64_t)u - base;
+            uint32_t nu;
+            if (lu >= 0) {  // u < v, so lu < cnt
+              nu = atomicExch(&s_head[lu], pa);
+              if (nu == kNone32) s_tail[lu] = pa;
+            } else {
+              nu = atomicExch(&io.eu.rhead[u], pa);
+              if (nu == kNone32) io.eu.rtail[u] = pa;
+            }
+            const uint32_t nv = atomicExch(&s_head[i], qa);
+            if (nv == kNone32) s_tail[i] = qa;
+            io.eu.S[pa] = nv;  // S[pa] = next(qa), S[qa] = next(pa)
+            io.eu.S[qa] = nu;
+          }
         }
       }
     }
-    if (SRC != kSrcRep && eg != kNone32) {
-      ++hooked;
-      if (io.tedge) io.tedge[v] = eg;
-      const uint32_t e = eg - io.e_base;
-      if (io.tflag && e < io.m_local) io.tflag[e] = 1;
-    }
     s[i] = r;
+  }
+  if (kLocal && io.link) {
+    // the tile's lists become the vertices' local lists (plain stores;
+    // links from other tiles went to the remote lists)
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
+      const uint32_t hd = s_head[i];
+      io.eu.vhead[base + i] = hd;
+      if (hd != kNone32) io.eu.vtail[base + i] = s_tail[i];
+    }
   }
   if (SRC != kSrcRep) {
     for (int o = 16; o > 0; o >>= 1) hooked += __shfl_xor_sync(0xffffffffu, hooked, o);
@@ -302,35 +280,74 @@ __global__ void __launch_bounds__(kTileThreads)
     }
     if (!__syncthreads_or(changed)) break;
   }
-  for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
-    const int32_t p = s[i];
-    rep[base + i] = p;
-    const int64_t lp = (int64_t)p - base;
-    if (lp < 0 || lp >= cnt) isx[p] = 1;
+  // Exit targets: written back with the reps, deduplicated (warp match,
+  // then a bitmap), collected in shared memory (s[] is free once the reps
+  // are out) and appended with ONE global atomic per tile -- a per-warp
+  // atomic on the shared counter serialises on a single address.
+  constexpr int kPer = kTileV / kTileThreads;
+  __shared__ uint32_t s_xn;
+  __shared__ unsigned long long s_xb;
+  uint32_t pk[kPer];
+  uint32_t app = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = threadIdx.x + k * kTileThreads;
+    const int32_t p = i < cnt ? s[i] : -1;
+    pk[k] = (uint32_t)p;
+    const unsigned same = __match_any_sync(0xffffffffu, p);
+    if (i < cnt) {
+      rep[base + i] = p;
+      const int64_t lp = (int64_t)p - base;
+      if ((lp < 0 || lp >= cnt) && (threadIdx.x & 31) == __ffs(same) - 1) {
+        // many vertices share one exit target (a big component's root):
+        // a plain L2 read skips the atomic once the bit is set
+        const uint32_t bit = 1u << (p & 31);
+        if (!(ld_cg(&xbits[p >> 5]) & bit) && !(atomicOr(&xbits[p >> 5], bit) & bit))
+          app |= 1u << k;
+      }
+    }
   }
+  if (threadIdx.x == 0) s_xn = 0;
+  __syncthreads();  // s[] reads done
+#pragma unroll
+  for (int k = 0; k < kPer; ++k)
+    if (app & (1u << k)) s[atomicAdd(&s_xn, 1u)] = (int32_t)pk[k];
+  __syncthreads();
+  if (threadIdx.x == 0) s_xb = s_xn ? atomicAdd(xcount, (unsigned long long)s_xn) : 0ull;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < s_xn; j += kTileThreads) xlist[s_xb + j] = (uint32_t)s[j];
 }
 
+// In-place doubling over the exit set, all rounds in one cooperative
+// launch. flags: 3 rotating "changed" words (zeroed before the launch).
 __global__ void __launch_bounds__(kBlock)
-    k_jump_list(int64_t count, const uint32_t* __restrict__ list, int32_t* rep, int* flags,
-                int round) {
-  if (round > 0 && flags[round - 1] == 0) return;
-  bool changed = false;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = list[i];
-    const int32_t p = rep[v];
-    int32_t x = rep[p];
-    if (x == p) continue;
+    k_jump_x(const uint32_t* __restrict__ list, const unsigned long long* xcount, int32_t* rep,
+             int* flags, int max_rounds) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t X = (int64_t)*xcount;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < max_rounds; ++r) {
+    if (gtid == 0) flags[(r + 1) % 3] = 0;  // read by everyone two barriers ago
+    bool changed = false;
+    for (int64_t i = gtid; i < X; i += gsize) {
+      const uint32_t v = list[i];
+      const int32_t p = ld_cg(&rep[v]);
+      int32_t x = ld_cg(&rep[p]);
+      if (x == p) continue;
 #pragma unroll
-    for (int hop = 1; hop < 4; ++hop) {
-      const int32_t y = rep[x];
-      if (y == x) break;
-      x = y;
+      for (int hop = 1; hop < 4; ++hop) {
+        const int32_t y = ld_cg(&rep[x]);
+        if (y == x) break;
+        x = y;
+      }
+      rep[v] = x;
+      changed = true;
     }
-    rep[v] = x;
-    changed = true;
+    if (__syncthreads_or(changed) && threadIdx.x == 0) flags[r % 3] = 1;
+    grid.sync();
+    if (*((volatile int*)&flags[r % 3]) == 0) break;
   }
-  block_flag(changed, &flags[round]);
 }
 
 __global__ void __launch_bounds__(kBlock) k_final_gather(int64_t n, int32_t* rep) {
@@ -342,52 +359,50 @@ __global__ void __launch_bounds__(kBlock) k_final_gather(int64_t n, int32_t* rep
   }
 }
 
-namespace {
-struct ByteFlag {
-  const uint8_t* f;
-  __device__ uint32_t operator()(int64_t i) const { return f[i]; }
-};
-}  // namespace
-
 // One shortcutting pass (optionally fused with the round's apply step or
 // the CSR first round): tile resolve, then the exit set, then the gather.
 void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& io) {
   if (n <= 0) return;
-  uint8_t* isx = h.ws<uint8_t>(WS_ISROOT, n);
-  uint32_t* list = h.ws<uint32_t>(WS_HEADS, n + 1);
-  CK(cudaMemsetAsync(isx, 0, (size_t)n, h.stream));
+  const int64_t words = (n + 31) / 32;
+  uint32_t* xbits = h.ws<uint32_t>(WS_XBITS, words);
+  uint32_t* xlist = h.ws<uint32_t>(WS_HEADS, n + 1);
+  unsigned long long* xcount = reinterpret_cast<unsigned long long*>(h.dev_box) + 5;
+  int* flags = reinterpret_cast<int*>(h.dev_box + 6);  // 3 ints in dev_box[6..7]
+  CK(cudaMemsetAsync(xbits, 0, (size_t)words * sizeof(uint32_t), h.stream));
+  CK(cudaMemsetAsync(h.dev_box + 5, 0, 3 * sizeof(int64_t), h.stream));
   const unsigned tiles = (unsigned)((n + kTileV - 1) / kTileV);
   static bool attr_set = false;
+  static int coop_blocks = 0;
   if (!attr_set) {
     CK(cudaFuncSetAttribute(k_tile_resolve<kSrcApply>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kTileSmem));
     CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRound0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kTileSmem));
+                            (int)(3 * kTileSmem)));
     CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kTileSmem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jump_x, kBlock, 0));
+    coop_blocks = std::max(1, per_sm) * num_sms();
     attr_set = true;
   }
   if (src == kSrcApply)
-    k_tile_resolve<kSrcApply><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, isx, io);
+    k_tile_resolve<kSrcApply><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, xbits, xlist,
+                                                                            xcount, io);
   else if (src == kSrcRound0)
-    k_tile_resolve<kSrcRound0><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, isx, io);
+    k_tile_resolve<kSrcRound0><<<tiles, kTileThreads, io.link ? 3 * kTileSmem : kTileSmem,
+                                 h.stream>>>(n, rep, xbits, xlist, xcount, io);
   else
-    k_tile_resolve<kSrcRep><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, isx, io);
+    k_tile_resolve<kSrcRep><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, xbits, xlist,
+                                                                          xcount, io);
   CK_LAUNCH();
   h.stats.step(n);
-  const int64_t X = scan_emit(h, n, ByteFlag{isx}, EmitCompact{list}, true);
-  if (X > 0) {
-    int rounds = 2;
-    while ((int64_t{1} << (rounds - 2)) < X + 1) ++rounds;  // X-forest depth <= |X|
-    int* flags = reinterpret_cast<int*>(h.dev_box + 128);
-    CK(cudaMemsetAsync(flags, 0, 64 * sizeof(int), h.stream));
-    const unsigned g = grid_for(X);
-    for (int r = 0; r < rounds && r < 64; ++r) {
-      k_jump_list<<<g, kBlock, 0, h.stream>>>(X, list, rep, flags, r);
-      h.stats.step(X);
-    }
-    CK_LAUNCH();
-  }
+  int rounds = 2;
+  while ((int64_t{1} << (rounds - 2)) < n) ++rounds;  // X-forest depth <= |X| <= n
+  const unsigned long long* xc = xcount;
+  void* args[] = {(void*)&xlist, (void*)&xc, (void*)&rep, (void*)&flags, (void*)&rounds};
+  CK(cudaLaunchCooperativeKernel((void*)k_jump_x, dim3(coop_blocks), dim3(kBlock), args, 0,
+                                 h.stream));
+  h.stats.step(n);
   k_final_gather<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
   CK_LAUNCH();
   h.stats.step(n);
@@ -465,38 +480,32 @@ void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tf
   h.stats.step(h.g.n);
 }
 
-void launch_compress(Handle& h, int32_t* rep, int64_t n) {
-  k_compress<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
-  CK_LAUNCH();
-  h.stats.step(n);
-}
-
 void launch_cc_init(Handle& h, int32_t* rep, unsigned long long* slot) {
   k_cc_init<<<grid_for(h.g.n), kBlock, 0, h.stream>>>(h.g.n, rep, slot);
   CK_LAUNCH();
   h.stats.step(h.g.n);
 }
 
-int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, uint32_t* tlist) {
+int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) {
   const int64_t n = h.g.n, m = h.g.m;
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(h.dev_box);
-  h.timer.begin(h.stream, "cc.init");
+  h.timer.begin(h.stream, "cc.init", 12.0 * n);  // rep + slot
   launch_cc_init(h, rep, slot);
   if (tflag && m > 0) CK(cudaMemsetAsync(tflag, 0, (size_t)m, h.stream));
-  if (tlist) CK(cudaMemsetAsync(tlist, 0xFF, (size_t)n * sizeof(uint32_t), h.stream));
   CK(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), h.stream));
   h.timer.end(h.stream);
   int mode = 0;  // HookMode::kMin first (cc_forest.cpp:87)
   int* any = reinterpret_cast<int*>(h.dev_box + 2);
-  const RoundIO io{slot, tflag, tlist, (uint32_t)h.g.e_base, (uint32_t)m, counter,
-                   h.g.offsets, h.g.nbrs, h.g.arc_edge};
+  RoundIO io{slot, tflag, (uint32_t)h.g.e_base, (uint32_t)m, counter, h.g.offsets, h.g.nbrs,
+             h.g.arc_edge, h.g.edges, euler != nullptr, euler ? *euler : EulerIO{}};
   cc_reset_rounds(h);
   int64_t round = 0;
   if (h.g.has_csr() && m > 0) {
     // round 0 (min mode over singleton reps) straight from the CSR, fused
     // with its apply and shortcutting
-    h.timer.begin(h.stream, "cc.round0");
+    // offsets, first neighbour, rep; a tree edge (arc heads + successors) per vertex
+    h.timer.begin(h.stream, "cc.round0", 4.0 * (n + 1) + 8.0 * n + (euler ? 16.0 * n : 0.0));
     resolve_round(h, rep, n, kSrcRound0, io);
     h.timer.end(h.stream);
     cc_round_done(h, 0);
@@ -507,7 +516,10 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, uint32_t* tlist) {
   for (;; ++round) {
     if (round > n + 1) throw AlgoError("hooking failed to converge");
     CK(cudaMemsetAsync(counter + 1, 0, 2 * sizeof(unsigned long long), h.stream));
-    h.timer.begin(h.stream, mode == 0 ? "cc.hook_min" : "cc.hook_max");
+    // edge 8 B + two rep gathers per visited edge (+ 4 B list entry when filtered)
+    const double visited = (h.cc_round >= 2 && h.cc_active >= 0) ? (double)h.cc_active : (double)m;
+    h.timer.begin(h.stream, mode == 0 ? "cc.hook_min" : "cc.hook_max",
+                  visited * ((h.cc_round >= 2 && h.cc_active >= 0) ? 20.0 : 16.0));
     cc_hook_round(h, mode, rep, slot, counter + 1, any);
     h.timer.end(h.stream);
     h.read_box(reinterpret_cast<int64_t*>(counter), 3);  // hooks so far, crossing, any
@@ -517,7 +529,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, uint32_t* tlist) {
     h.stats.rounds = round + 1;
     // a round without proposals applies nothing (cc_forest.cpp:91)
     if (!proposed) break;
-    h.timer.begin(h.stream, "cc.apply_compress");
+    h.timer.begin(h.stream, "cc.apply_compress", 16.0 * n);  // slot + rep read/write
     resolve_round(h, rep, n, kSrcApply, io);
     h.timer.end(h.stream);
     mode ^= 1;

@@ -1,4 +1,6 @@
 // engine.cu -- Handle, workspace, phase timer, shared small kernels.
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 
 #include "engine.hpp"
@@ -25,26 +27,31 @@ cudaEvent_t PhaseTimer::get() {
   }
   return pool_[used_++];
 }
-void PhaseTimer::begin(cudaStream_t s, const char* name) {
+// Every phase is also an NVTX push/pop range (a no-op unless a tool is
+// attached), so ncu --nvtx --print-nvtx-rename kernel attributes each
+// launch to its phase (scripts/gpu_round.sh).
+void PhaseTimer::begin(cudaStream_t s, const char* name, double bytes) {
+  nvtxRangePushA(name);
   if (!enabled) return;
-  Rec r{name, get(), nullptr};
+  Rec r{name, bytes, get(), nullptr};
   CK(cudaEventRecord(r.a, s));
   recs_.push_back(r);
 }
 void PhaseTimer::end(cudaStream_t s) {
+  nvtxRangePop();
   if (!enabled || recs_.empty()) return;
   Rec& r = recs_.back();
   r.b = get();
   CK(cudaEventRecord(r.b, s));
 }
-std::vector<std::pair<std::string, double>> PhaseTimer::collect() {
-  std::vector<std::pair<std::string, double>> out;
+std::vector<PhaseRec> PhaseTimer::collect() {
+  std::vector<PhaseRec> out;
   for (auto& r : recs_) {
     if (!r.b) continue;
     CK(cudaEventSynchronize(r.b));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, r.a, r.b));
-    out.emplace_back(r.name, (double)ms);
+    out.push_back(PhaseRec{r.name, (double)ms, r.bytes});
   }
   recs_.clear();
   used_ = 0;

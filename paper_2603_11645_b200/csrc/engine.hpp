@@ -37,17 +37,25 @@ struct Stats {
 
 // Named phase timer on the handle's stream (CUDA events; no host sync
 // until collect()).
+// Each phase carries its algorithmic bytes (every element the
+// phase must touch, once), so the bench's roofline needs no model of its own.
+struct PhaseRec {
+  std::string name;
+  double ms;
+  double bytes;
+};
 class PhaseTimer {
  public:
-  void begin(cudaStream_t s, const char* name);
+  void begin(cudaStream_t s, const char* name, double bytes = 0);
   void end(cudaStream_t s);
-  // Synchronizes and returns (name, ms) per phase in order; clears.
-  std::vector<std::pair<std::string, double>> collect();
+  // Synchronizes and returns the phases in order; clears.
+  std::vector<PhaseRec> collect();
   bool enabled = false;
 
  private:
   struct Rec {
     std::string name;
+    double bytes;
     cudaEvent_t a, b;
   };
   std::vector<Rec> recs_;
@@ -94,7 +102,7 @@ class Handle {
   // Small pinned host mailbox for flag/count readbacks.
   int64_t* host_box = nullptr;
   // Device counters block (256 x int64) zeroed per use by the caller; fixed
-  // regions: [0,2) cc, [4] euler, [8] lr, [16] pr, [30] bfs, [40] validate,
+  // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,12] lr, [16] pr, [30] bfs, [40] validate,
   // [48] normalize, [50,53) capi/lr verify, [128,160) jump-round flags.
   int64_t* dev_box = nullptr;
 
@@ -134,7 +142,6 @@ enum WsSlot : int {
   WS_SCAN,        // u32 scan partials
   WS_SCAN2,
   WS_ROOTS,       // int32 n       roots list
-  WS_TLIST,       // u32 n         tree-edge list
   WS_ELIST0,      // u32 m         active (still crossing) edges, ping
   WS_ELIST1,      // u32 m         pong
   // PR-RST
@@ -155,27 +162,89 @@ enum WsSlot : int {
   WS_VAL_A,
   WS_VAL_B,
   WS_VAL_C,
+  // Euler tour (euler.cu): rotation lists
+  WS_VHEAD,       // u32 n         first arc of each vertex's local rotation list
+  WS_VTAIL,       // u32 n         its last arc
+  WS_RHEAD,       // u32 n         remote list (atomic prepends): first arc
+  WS_RTAIL,       // u32 n         its last arc (the first one inserted)
+  WS_ETO,         // u32 2N        arc heads, pairs (2i: a->b, 2i+1: b->a)
+  WS_XBITS,       // u32 n/32      exit-set membership bitmap (cc.cu)
+  // list-ranking levels >= 1 (listrank.cu), one arena per level
+  WS_LR_L1,
+  WS_LR_LAST = WS_LR_L1 + 12,
   WS_COUNT
 };
+
+// ---- Euler tour as rotation lists (euler.cu) ----------------------------
+// Tree edge slot i (of N) with endpoints (a, b), a < b, owns arcs i = (a -> b)
+// and N + i = (b -> a): rev(p) = p +- N. The two directions live in
+// separate halves so that a tour running along a chain of consecutive slots
+// reads 8 successors per 32-byte sector, not 4. Each vertex keeps a singly linked
+// list of the arcs leaving it (any rotation order gives the same parent
+// array), built by atomicExch prepends the moment a
+// tree edge is created (the CC apply step). succ(p) = next(rev p), the arc
+// after rev(p) in the list of the vertex p enters (euler_rooting.cpp:83-86);
+// it is stored directly: S[rev p] = next(p). The wrap from a list's last
+// arc to its first is filled in after the CC, and left open (NONE) for a
+// root, which is exactly break_cycles (euler_rooting.cpp:96-101).
+//
+// Two lists per vertex, concatenated by the vertex pass after the CC: the
+// "local" one written by round 0's shared-memory tiles with plain stores
+// (vhead/vtail, every vertex covered, so no initialisation), and the
+// "remote" one that every other link prepends to with atomicExch
+// (rhead/rtail, NONE-initialised).
+struct EulerIO {
+  uint32_t nslots;  // N
+  uint32_t* eto;    // N pairs (to(i), to(N + i)) = (b, a)
+  uint32_t* S;      // 2N  successors
+  uint32_t* vhead;  // n   local list: first arc
+  uint32_t* vtail;  // n   local list: last arc
+  uint32_t* rhead;  // n   remote list: first arc (NONE-initialised)
+  uint32_t* rtail;  // n   remote list: last arc (the first inserted)
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void link_tree_edge(const EulerIO& io, uint32_t slot, uint32_t a,
+                                               uint32_t b) {
+  const uint32_t p = slot, q = io.nslots + slot;  // p: a -> b, q: b -> a
+  reinterpret_cast<uint2*>(io.eto)[slot] = make_uint2(b, a);
+  const uint32_t na = atomicExch(&io.rhead[a], p);  // next(p) = na
+  const uint32_t nb = atomicExch(&io.rhead[b], q);  // next(q) = nb
+  io.S[p] = nb;  // S[p] = next(rev p) = next(q)
+  io.S[q] = na;
+  if (na == kNone32) io.rtail[a] = p;
+  if (nb == kNone32) io.rtail[b] = q;
+}
+__device__ __forceinline__ uint32_t arc_rev(uint32_t p, uint32_t nslots) {
+  return p < nslots ? p + nslots : p - nslots;
+}
+#endif
 
 // ---- algorithms (device-resident in/out; int32 ids) ----
 // cc_spanning_forest (cc_forest.cpp:73-102), exact: labels = converged reps,
 // tflag[e] = 1 for tree edges. Returns the number of tree edges.
 // tlist (nullable, n entries): tlist[v] = global id of the tree edge that
 // hooked root v, or kNone32 (every tree edge appears exactly once).
-int64_t cc_exact(Handle& h, int32_t* labels, uint8_t* tflag, uint32_t* tlist = nullptr);
+// euler (nullable): every tree edge is linked into the rotation lists as it
+// is created, slot = the vertex it hooked (EulerIO; N = n slots).
+int64_t cc_exact(Handle& h, int32_t* labels, uint8_t* tflag, const EulerIO* euler = nullptr);
 // cc labels only, validity-level (any correct partition; used by BFS
 // seeding and the validator). Returns the number of hook rounds.
 void cc_labels_fast(Handle& h, int32_t* labels);
-// euler_root_forest (euler_rooting.cpp:180-215) over the graph's CSR and a
-// tree-edge flag set; parent[n] out (int32 device).
-// verify: also prove the tree-edge set is a forest (list ranking reaches
-// every arc and every ruler chain ends), else "list ranking failed to
-// converge: not a forest" (euler_rooting.cpp:131-133).
-// Tree edges: tsrc[i] for i in [0, N) (kNone32 entries skipped), or, with
-// tsrc == null, graph edges 0..T-1 (explicit forests). Needs no CSR.
-void euler_root(Handle& h, const int32_t* labels, const uint32_t* tsrc, int64_t N, int64_t T,
-                int32_t designated_root, int32_t* parent, bool verify = false);
+// euler_root_forest (euler_rooting.cpp:180-215) on rotation lists already
+// linked (EulerIO over N slots): roots, successor wrap, ruler registration,
+// list ranking, orientation; parent[n] out (int32 device).
+//   cc_slots: slot v holds the edge that hooked v (valid iff labels[v] != v,
+//             N = n); otherwise slots [0, T) are all valid.
+//   verify:   also prove the structure is a forest (edge count, every arc
+//             reached, ruler lists acyclic), else the reference's errors.
+void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, int64_t T,
+                bool cc_slots, int32_t designated_root, int32_t* parent, bool verify = false);
+// EulerIO buffers of the handle for N slots; the remote lists reset to
+// NONE, the local ones too unless round 0 will write them (local_written).
+EulerIO euler_buffers(Handle& h, int64_t N, bool local_written);
+// Links graph edges [0, T) as tree edges (explicit forests).
+void euler_link_edges(Handle& h, const EulerIO& io, int64_t T);
 // pr_rst (pr_rst.cpp:267-314)
 void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent);
 // bfs_rst (bfs_rst.cpp:10-77): parent, levels; roots in discovery order

@@ -1,5 +1,5 @@
-// euler.cu -- Euler-tour rooting of the CC spanning forest
-// (euler_root_forest, euler_rooting.cpp:180-215), sort-free and CSR-free.
+// euler.cu -- Euler-tour rooting of a spanning forest (euler_root_forest,
+// euler_rooting.cpp:180-215), sort-free, scan-free and CSR-free.
 //
 // The reference lays out arcs i=(u->v), i+T=(v->u), host-std::sorts them by
 // (from, to) to chain each vertex's arcs (euler_rooting.cpp:49-72), and
@@ -7,33 +7,39 @@
 // rotation system (any circular order of each vertex's arcs) yields an
 // Euler tour of the same tree, and a tree with a fixed root has exactly one
 // parent array, so the order is free. Here:
-//   * the apply step of the CC appends tree-edge ids to a list (no scan of
-//     the m edges or the 2m CSR arcs);
-//   * each tree edge claims a slot in both endpoints' arc segments with a
-//     warp-aggregated atomicAdd (segment offsets = scan of tree degrees);
-//     the thread that placed both arcs writes to/rev/succ for both, so
-//     compute_successor and break_cycles (:89-102: the wrap into a root's
-//     first arc is cut) cost no search;
+//   * the CC apply step links every new tree edge into the rotation lists
+//     of its endpoints (link_tree_edge, engine.hpp): arcs i and N + i per
+//     slot, so rev(p) = p +- N and successors are written at link time;
+//   * one vertex pass (k_euler_fix) picks the roots -- the designated root
+//     for its label, the smallest vertex of every other label (:190-203) --,
+//     closes each non-root list into a cycle (the wrap of compute_successor)
+//     and leaves the roots' lists open (break_cycles, :96-101), and
+//     registers the list-ranking rulers (hash-selected arcs, the tours'
+//     first arcs) with warp-aggregated id claims;
 //   * ranks come from sparse ruling-set list ranking (listrank.cu);
 //   * derive_parents (:155-178): in each arc pair the higher-ranked arc is
 //     the return arc, parent[from] = to.
-// Roots: the designated root for its label, the smallest vertex of every
-// other label (:190-203).
+#include <algorithm>
+
 #include "engine.hpp"
-#include "scan.cuh"
+#include "listrank.cuh"
 
 namespace rstg {
 
-const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ, int stride,
-                                 const uint32_t* heads, int64_t H, uint32_t* sl,
-                                 int64_t* R_out, bool verify);
-
-// min_vertex per label (euler_rooting.cpp:190-195); labels are vertex ids.
-__global__ void k_min_vertex(int64_t n, const int32_t* __restrict__ lab, uint32_t* minv) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t l = lab[v];
-    if ((uint32_t)v < minv[l]) atomicMin(&minv[l], (uint32_t)v);
+// min_vertex per label (euler_rooting.cpp:190-195). Labels are vertex ids;
+// a warp whose lanes share a label (the common case: one giant component)
+// issues one atomic instead of 32.
+__global__ void __launch_bounds__(kBlock)
+    k_min_vertex(int64_t n, const int32_t* __restrict__ lab, uint32_t* minv) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += stride) {
+    const int64_t v = b + threadIdx.x;
+    const int32_t l = v < n ? lab[v] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    // lanes are in ascending v order: the lowest lane of a label group
+    // holds its smallest vertex
+    const int lane = threadIdx.x & 31;
+    if (v < n && lane == __ffs(peers) - 1 && (uint32_t)v < minv[l]) atomicMin(&minv[l], (uint32_t)v);
   }
 }
 void launch_min_vertex(Handle& h, const int32_t* lab, uint32_t* minv) {
@@ -44,157 +50,187 @@ void launch_min_vertex(Handle& h, const int32_t* lab, uint32_t* minv) {
 __global__ void k_override_root(const int32_t* lab, uint32_t* minv, int32_t root) {
   if (threadIdx.x == 0 && blockIdx.x == 0 && root >= 0) minv[lab[root]] = (uint32_t)root;
 }
-__global__ void k_mark_roots(int64_t n, const int32_t* __restrict__ lab,
-                             const uint32_t* __restrict__ minv, uint8_t* isroot,
-                             int32_t* parent, uint32_t* tdeg, unsigned long long* count) {
-  uint32_t c = 0;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const bool r = minv[lab[v]] == (uint32_t)v;
-    isroot[v] = r;
-    parent[v] = (int32_t)v;  // derive_parents :167
-    tdeg[v] = 0;
-    c += r;
+
+// Vertex pass: roots (parent[r] = r, derive_parents :167 for roots), the
+// successor wrap of every non-root list, the heads of the roots' tours, and
+// the rulers. cc_slots: slot v (arcs 2v, 2v+1) is valid iff lab[v] != v.
+// Tiles of kFixItems x kBlock vertices, one ruler-id claim per tile.
+constexpr int kFixItems = 8;
+__global__ void __launch_bounds__(kBlock)
+    k_euler_fix(int64_t n, const int32_t* __restrict__ lab, const uint32_t* __restrict__ minv,
+                EulerIO io, bool cc_slots, int32_t* __restrict__ parent, uint32_t* rpos,
+                uint32_t* sl, unsigned long long* ctr, unsigned long long* comps,
+                unsigned long long* tiles, int logk, int ob, uint32_t cap) {
+  constexpr int64_t kTile = (int64_t)kFixItems * kBlock;
+  __shared__ unsigned long long s_tile;
+  uint32_t nroots = 0;
+  // tiles claimed in order from a counter: ruler ids then follow positions
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(tiles, 1ull);
+    __syncthreads();
+    const int64_t base = (int64_t)s_tile * kTile;
+    if (base >= n) break;
+    uint32_t flags = 0;  // 3 bits per item: head, arc 2v, arc 2v+1
+    uint32_t hdv[kFixItems];
+#pragma unroll
+    for (int k = 0; k < kFixItems; ++k) {
+      const int64_t v = base + k * kBlock + threadIdx.x;
+      hdv[k] = kNone32;
+      if (v >= n) continue;
+      const int32_t l = lab[v];
+      const bool root = minv[l] == (uint32_t)v;
+      // local list, then the remote list: one rotation
+      const uint32_t h1 = io.vhead[v], h2 = io.rhead[v];
+      uint32_t hd = h1, tl = kNone32;
+      if (h1 != kNone32) {
+        tl = io.vtail[v];
+        if (h2 != kNone32) {
+          io.S[arc_rev(tl, io.nslots)] = h2;  // next(local tail) = remote head
+          tl = io.rtail[v];
+        }
+      } else if (h2 != kNone32) {
+        hd = h2;
+        tl = io.rtail[v];
+      }
+      hdv[k] = hd;
+      if (root) {
+        parent[v] = (int32_t)v;
+        ++nroots;
+        if (hd != kNone32 && !lr_hash_ruler(hd, logk)) flags |= 1u << (3 * k);
+      } else if (hd != kNone32) {
+        io.S[arc_rev(tl, io.nslots)] = hd;  // last arc wraps to the first
+      }
+      if (cc_slots && l != (int32_t)v) {
+        if (lr_hash_ruler((uint32_t)v, logk)) flags |= 2u << (3 * k);
+        if (lr_hash_ruler(io.nslots + (uint32_t)v, logk)) flags |= 4u << (3 * k);
+      }
+    }
+    uint32_t id = lr_block_claim(__popc(flags), ctr);
+#pragma unroll
+    for (int k = 0; k < kFixItems; ++k) {
+      const uint32_t v = (uint32_t)(base + k * kBlock + threadIdx.x);
+      const uint32_t f = (flags >> (3 * k)) & 7u;
+      if (f & 1u) lr_put(id++, hdv[k], rpos, sl, ob, cap);
+      if (f & 2u) lr_put(id++, v, rpos, sl, ob, cap);
+      if (f & 4u) lr_put(id++, io.nslots + v, rpos, sl, ob, cap);
+    }
   }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+  for (int o = 16; o > 0; o >>= 1) nroots += __shfl_xor_sync(0xffffffffu, nroots, o);
+  if ((threadIdx.x & 31) == 0 && nroots) atomicAdd(comps, (unsigned long long)nroots);
 }
 
-// Tree degrees + each arc's slot inside its tail's segment. Tree edge i is
-// tsrc[i] (kNone32 = no edge), or graph edge i when tsrc is null.
+// Rulers of explicit slots [0, T): hash-selected arcs, one claim per tile.
 __global__ void __launch_bounds__(kBlock)
-    k_tree_slots(int64_t N, const uint32_t* __restrict__ tsrc, const int2* __restrict__ edges,
-                 uint32_t e_base, uint32_t* tdeg, uint2* __restrict__ lpos) {
+    k_register_slots(int64_t T, uint32_t* rpos, uint32_t* sl, unsigned long long* ctr, int logk,
+                     int ob, uint32_t cap) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < T; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = b + threadIdx.x;
+    const bool a0 = i < T && lr_hash_ruler((uint32_t)i, logk);
+    const bool a1 = i < T && lr_hash_ruler((uint32_t)(T + i), logk);
+    uint32_t id = lr_block_claim((uint32_t)a0 + (uint32_t)a1, ctr);
+    if (a0) lr_put(id++, (uint32_t)i, rpos, sl, ob, cap);
+    if (a1) lr_put(id++, (uint32_t)(T + i), rpos, sl, ob, cap);
+  }
+}
+
+__global__ void k_link_edges(int64_t T, const int2* __restrict__ edges, EulerIO io) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int2 e = edges[i];
+    link_tree_edge(io, (uint32_t)i, (uint32_t)e.x, (uint32_t)e.y);
+  }
+}
+
+// derive_parents (:172-176) on (ruler, offset) ranks, one thread per slot.
+__global__ void __launch_bounds__(kBlock)
+    k_orient(int64_t N, const int32_t* __restrict__ lab, bool cc_slots,
+             const uint2* __restrict__ eto, const uint32_t* __restrict__ sl,
+             const uint32_t* __restrict__ rstart, int ob, int32_t* __restrict__ parent) {
+  const uint32_t mask = (1u << ob) - 1u;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t e = tsrc ? tsrc[i] : (uint32_t)i;
-    if (e == kNone32) continue;
-    const int2 uv = edges[e - e_base];
-    const uint32_t pu = atomicAdd(&tdeg[uv.x], 1u);
-    const uint32_t pv = atomicAdd(&tdeg[uv.y], 1u);
-    lpos[i] = make_uint2(pu, pv);
-  }
-}
-
-// Both arcs of tree edge i: {to, rev} records plus the separate succ array
-// the list-ranking walk chases (4-byte entries keep 8 successors per
-// sector). compute_successor :83-86 and the break_cycles cut :96-101.
-__global__ void __launch_bounds__(kBlock)
-    k_tree_arcs(int64_t N, const uint32_t* __restrict__ tsrc, const int2* __restrict__ edges,
-                uint32_t e_base, const uint2* __restrict__ lpos, const uint32_t* __restrict__ tf,
-                const uint8_t* __restrict__ isroot, uint2* __restrict__ arc,
-                uint32_t* __restrict__ succ) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t e = tsrc ? tsrc[i] : (uint32_t)i;
-    if (e == kNone32) continue;
-    const int2 uv = edges[e - e_base];
-    const uint2 lp = lpos[i];
-    const uint32_t u = (uint32_t)uv.x, v = (uint32_t)uv.y;
-    const uint32_t fu = tf[u], eu = tf[u + 1], fv = tf[v], ev = tf[v + 1];
-    const uint32_t p1 = fu + lp.x;  // u -> v
-    const uint32_t p2 = fv + lp.y;  // v -> u
-    arc[p1] = make_uint2(v, p2);
-    succ[p1] = (p2 + 1 < ev) ? p2 + 1 : (isroot[v] ? kNone32 : fv);
-    arc[p2] = make_uint2(u, p1);
-    succ[p2] = (p1 + 1 < eu) ? p1 + 1 : (isroot[u] ? kNone32 : fu);
-  }
-}
-
-namespace {
-struct ArrF {
-  const uint32_t* a;
-  __device__ uint32_t operator()(int64_t i) const { return a[i]; }
-};
-struct HeadFlag {  // roots with at least one tree arc: their first arc heads a list
-  const uint8_t* isroot;
-  const uint32_t* tf;
-  __device__ uint32_t operator()(int64_t x) const {
-    return (isroot[x] && tf[x] < tf[x + 1]) ? 1u : 0u;
-  }
-};
-struct EmitHeadArc {
-  const uint32_t* tf;
-  uint32_t* heads;
-  __device__ void operator()(int64_t x, uint32_t p, uint32_t v) const {
-    if (v) heads[p] = tf[x];
-  }
-};
-}  // namespace
-
-// derive_parents (:172-176) on (ruler, offset) ranks; from(p) = to(rev p).
-__global__ void __launch_bounds__(kBlock)
-    k_orient(int64_t E, const uint2* __restrict__ arc, const uint32_t* __restrict__ sl,
-             const uint32_t* __restrict__ rstart, int32_t* __restrict__ parent) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < E;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 ap = arc[p];
-    const uint32_t q = ap.y;
-    if ((uint32_t)p > q) continue;
-    const uint32_t to_q = arc[q].x;  // = from(p)
-    const uint32_t a = sl[p], b = sl[q];  // (ruler << 7) | offset
-    const uint32_t rp = rstart[a >> 7] + (a & 127u);
-    const uint32_t rq = rstart[b >> 7] + (b & 127u);
+    if (cc_slots && lab[i] == (int32_t)i) continue;  // no tree edge in this slot
+    const uint2 t = eto[i];  // (b, a): arc i = a -> b, arc N + i = b -> a
+    const uint32_t wp = sl[i], wq = sl[N + i];
+    const uint32_t rp = rstart[wp >> ob] + (wp & mask);
+    const uint32_t rq = rstart[wq >> ob] + (wq & mask);
     // the higher-ranked arc returns from the child: parent[from] = to
     if (rp > rq)
-      parent[to_q] = (int32_t)ap.x;
+      parent[t.y] = (int32_t)t.x;  // a -> b returns: parent[a] = b
     else
-      parent[ap.x] = (int32_t)to_q;
+      parent[t.x] = (int32_t)t.y;  // b -> a returns: parent[b] = a
   }
 }
 
-void euler_root(Handle& h, const int32_t* labels, const uint32_t* tsrc, int64_t N, int64_t T,
-                int32_t designated_root, int32_t* parent, bool verify) {
+EulerIO euler_buffers(Handle& h, int64_t N, bool local_written) {
+  EulerIO io;
+  io.nslots = (uint32_t)N;
+  io.eto = h.ws<uint32_t>(WS_ETO, 2 * N);
+  io.S = h.ws<uint32_t>(WS_SUCC, 2 * N);
+  io.vhead = h.ws<uint32_t>(WS_VHEAD, h.g.n);
+  io.vtail = h.ws<uint32_t>(WS_VTAIL, h.g.n);
+  io.rhead = h.ws<uint32_t>(WS_RHEAD, h.g.n);
+  io.rtail = h.ws<uint32_t>(WS_RTAIL, h.g.n);
+  if (!local_written) CK(cudaMemsetAsync(io.vhead, 0xFF, (size_t)h.g.n * sizeof(uint32_t), h.stream));
+  CK(cudaMemsetAsync(io.rhead, 0xFF, (size_t)h.g.n * sizeof(uint32_t), h.stream));
+  return io;
+}
+
+void euler_link_edges(Handle& h, const EulerIO& io, int64_t T) {
+  if (T <= 0) return;
+  k_link_edges<<<grid_for(T), kBlock, 0, h.stream>>>(T, h.g.edges, io);
+  CK_LAUNCH();
+  h.stats.step(T);
+}
+
+void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, int64_t T,
+                bool cc_slots, int32_t designated_root, int32_t* parent, bool verify) {
   const int64_t n = h.g.n;
+  const int64_t E = 2 * N;  // arc position space (holes where a slot is empty)
+  // lists = tours of components with an edge: at most min(T, n - T) heads
+  // (the explicit, unverified input may have more: bound by n there)
+  const LrParams P = lr_params(E, verify ? n : std::min<int64_t>(T, n - T) + 1);
   uint32_t* minv = h.ws<uint32_t>(WS_MINV, n);
-  uint8_t* isroot = h.ws<uint8_t>(WS_ISROOT, n);
-  uint32_t* tdeg = h.ws<uint32_t>(WS_POS, n + 1);
-  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box) + 4;
-
-  h.timer.begin(h.stream, "euler.roots");
-  CK(cudaMemsetAsync(minv, 0xFF, n * sizeof(uint32_t), h.stream));
-  CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), h.stream));
-  k_min_vertex<<<grid_for(n), kBlock, 0, h.stream>>>(n, labels, minv);
-  k_override_root<<<1, 32, 0, h.stream>>>(labels, minv, designated_root);
-  k_mark_roots<<<grid_for(n), kBlock, 0, h.stream>>>(n, labels, minv, isroot, parent, tdeg, ctr);
-  CK_LAUNCH();
-  h.stats.step(n, 3);
-  h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
-  const int64_t comps = h.host_box[0];
-  h.stats.components = comps;
-  h.timer.end(h.stream);
-  if (T != n - comps)  // euler_rooting.cpp:205-208
-    throw AlgoError("edge count does not match a spanning forest of the labeling");
-  const int64_t E = 2 * T;
-  if (E == 0) return;
-
-  h.timer.begin(h.stream, "euler.arcs");
-  if (!tsrc) N = T;
-  uint2* lpos = h.ws<uint2>(WS_VAL_B, N);
-  k_tree_slots<<<grid_for(N), kBlock, 0, h.stream>>>(N, tsrc, h.g.edges, (uint32_t)h.g.e_base,
-                                                    tdeg, lpos);
-  CK_LAUNCH();
-  h.stats.step(N);
-  uint32_t* tf = h.ws<uint32_t>(WS_TF, n + 1);
-  scan_emit(h, n, ArrF{tdeg}, EmitExcl{tf, n}, false);
-  uint2* arc = h.ws<uint2>(WS_ATO, E);
-  uint32_t* succ = h.ws<uint32_t>(WS_SUCC, E);
-  k_tree_arcs<<<grid_for(N), kBlock, 0, h.stream>>>(N, tsrc, h.g.edges, (uint32_t)h.g.e_base,
-                                                   lpos, tf, isroot, arc, succ);
-  CK_LAUNCH();
-  h.stats.step(N);
-  uint32_t* heads = h.ws<uint32_t>(WS_HEADS, n + 1);
-  const int64_t H = scan_emit(h, n, HeadFlag{isroot, tf}, EmitHeadArc{tf, heads}, true);
-  h.timer.end(h.stream);
-
+  uint32_t* rpos = h.ws<uint32_t>(WS_RPOS, P.cap);
   uint32_t* sl = h.ws<uint32_t>(WS_SL, E);
-  int64_t R = 0;
-  const uint32_t* rstart = list_rank_rulers(h, E, succ, 1, heads, H, sl, &R, verify);
-  h.timer.begin(h.stream, "euler.orient");
-  k_orient<<<grid_for(E), kBlock, 0, h.stream>>>(E, arc, sl, rstart, parent);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box) + 8;
+  unsigned long long* comps = reinterpret_cast<unsigned long long*>(h.dev_box) + 4;
+  unsigned long long* tiles = reinterpret_cast<unsigned long long*>(h.dev_box) + 13;
+  const cudaStream_t s = h.stream;
+
+  h.timer.begin(s, "euler.roots", 4.0 * n + 4.0 * n + 16.0 * n);
+  CK(cudaMemsetAsync(minv, 0xFF, n * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(h.dev_box + 4, 0, sizeof(int64_t), s));
+  CK(cudaMemsetAsync(h.dev_box + 8, 0, sizeof(int64_t), s));
+  CK(cudaMemsetAsync(h.dev_box + 13, 0, sizeof(int64_t), s));
+  if (verify && E > 0) CK(cudaMemsetAsync(sl, 0xFF, E * sizeof(uint32_t), s));
+  k_min_vertex<<<grid_for(n), kBlock, 0, s>>>(n, labels, minv);
+  k_override_root<<<1, 32, 0, s>>>(labels, minv, designated_root);
+  k_euler_fix<<<grid_for((n + kFixItems - 1) / kFixItems), kBlock, 0, s>>>(n, labels, minv, io, cc_slots, parent, rpos, sl, ctr,
+                                             comps, tiles, P.logk0, P.ob, (uint32_t)P.cap);
+  if (!cc_slots && T > 0)
+    k_register_slots<<<grid_for(T), kBlock, 0, s>>>(T, rpos, sl, ctr, P.logk0, P.ob, (uint32_t)P.cap);
   CK_LAUNCH();
-  h.stats.step(E);
-  h.timer.end(h.stream);
+  h.stats.step(n, cc_slots ? 3 : 4);
+  h.timer.end(s);
+  if (verify) {
+    h.read_box(reinterpret_cast<int64_t*>(comps), 1);
+    const int64_t nc = h.host_box[0];
+    h.stats.components = nc;
+    if (T != n - nc)  // euler_rooting.cpp:205-208
+      throw AlgoError("edge count does not match a spanning forest of the labeling");
+  }
+  if (T == 0) return;
+
+  const uint32_t* rstart = lr_rank(h, P, E, io.S, sl, rpos, ctr, verify, nullptr);
+
+  h.timer.begin(s, "euler.orient", 8.0 * N + 16.0 * T + 4.0 * T);
+  k_orient<<<grid_for(N), kBlock, 0, s>>>(N, labels, cc_slots, reinterpret_cast<const uint2*>(io.eto),
+                                          sl, rstart, P.ob, parent);
+  CK_LAUNCH();
+  h.stats.step(N);
+  h.timer.end(s);
 }
 
 }  // namespace rstg

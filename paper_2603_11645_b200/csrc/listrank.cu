@@ -2,254 +2,521 @@
 // list_rank, euler_rooting.cpp:104-153, which costs ceil(log2 E) full
 // passes over all E arcs).
 //
-//   1. rulers = every arc whose multiplicative hash falls in a 1/K bucket
-//      (found by one index-only pass, ids handed out by warp-aggregated
-//      atomics), plus every list head (heads have no predecessor, so no
-//      walk would ever reach them);
-//   2. one thread per ruler walks its sublist (succ chain) until the next
-//      ruler or the list tail, writing a 32-bit (ruler id, offset) word per
-//      arc; a walk longer than kWalkCap turns the next arc into a fresh
-//      ruler and stops, so a launch is bounded by kWalkCap dependent loads
-//      and the geometric tail is handled by a few short follow-up launches;
-//   3. the ruler list (about E/K nodes) is prefix-summed by Jacobi pointer
-//      jumping on packed (prefix, jump) words;
-//   4. rank(arc) = rstart[ruler] + offset, evaluated by the consumer.
-// Ranks equal the reference's list_rank output (distance from the head):
+// Level 0 (the tour):
+//   1. rulers = positions whose multiplicative hash falls in a 1/2^logk0
+//      bucket, plus every list head (no walk would reach a head); the
+//      producer registers them inside its own pass (lr_register_warp);
+//   2. a persistent walk kernel: each CTA owns a slice of the ruler ids and
+//      each thread keeps kChains sublist walks in flight at once (memory-
+//      level parallelism on the dependent succ loads), claiming the next
+//      ruler of its CTA's slice from shared memory when a walk ends. A walk
+//      writes one 32-bit (ruler id, offset) word per arc and stops at the
+//      next ruler or the list tail; a walk longer than 2^ob - 1 hops turns
+//      its next arc into a fresh ruler (rare, walked by a follow-up launch).
+// Levels >= 1 (the ruler lists, weighted by sublist length): the same
+//   scheme recursively -- pred marks, ruler registration, persistent
+//   weighted walk, recurse, expand -- until a level fits one CTA, which runs
+//   Wyllie doubling in shared memory. Single-node lists drop out of the
+//   recursion (their prefix is 0), so every level shrinks.
+// rank(arc) = rstart[ruler] + offset is evaluated by the consumer. Ranks
+// equal the reference's list_rank output (distance from the list head):
 // checked arc for arc against the reference's own ranks
 // (tests/golden/euler_ranks.npz) and the oracle's Wyllie restatement.
+#include <cstdlib>
+
 #include "engine.hpp"
+#include "listrank.cuh"
 #include "scan.cuh"
 
 namespace rstg {
 
-constexpr int kLogK = 5;  // ruler density 1/32
-constexpr uint32_t kWalkCap = 64;
-constexpr int kOffBits = 7;  // sl word = (ruler id << 7) | offset, offset <= kWalkCap
-constexpr uint32_t kOffMask = (1u << kOffBits) - 1u;
-constexpr uint32_t kMaxRulers = (1u << (32 - kOffBits)) - 2u;  // all-ones = unvisited
-static_assert(kWalkCap <= kOffMask, "offset field too narrow");
+// sublist walks kept in flight per thread (runtime choice: RSTG_LR_CHAINS)
+constexpr int kMaxChains = 4;
+constexpr int kBaseMax = 8192;  // one-CTA Wyllie (64 KB of shared memory)
+constexpr uint32_t kChunk = 64;  // ruler ids per round-robin chunk of the walks
 
-__device__ __forceinline__ bool is_hash_ruler(uint32_t p) {
-  return ((p * 0x9E3779B1u) >> (32 - kLogK)) == 0u;
-}
-
-// Hash rulers: an index-only pass; each 4096-position tile counts its
-// rulers with a block scan and claims its id range with one atomicAdd.
-// sl[ruler] = (id, 0).
-constexpr int kRulerItems = 16;
-__global__ void __launch_bounds__(kBlock)
-    k_find_rulers(int64_t E, uint32_t* __restrict__ rpos, uint32_t* __restrict__ sl,
-                  unsigned long long* counter) {
-  __shared__ uint32_t s_total;
-  __shared__ unsigned long long s_base;
-  const int64_t tile_len = (int64_t)kBlock * kRulerItems;
-  for (int64_t tile = blockIdx.x; tile * tile_len < E; tile += gridDim.x) {
-    const int64_t p0 = tile * tile_len + (int64_t)threadIdx.x * kRulerItems;
-    uint32_t mine = 0;
-#pragma unroll
-    for (int k = 0; k < kRulerItems; ++k) {
-      const int64_t p = p0 + k;
-      mine |= (p < E && is_hash_ruler((uint32_t)p)) ? (1u << k) : 0u;
-    }
-    const uint32_t off = block_excl_scan(__popc(mine), &s_total);
-    if (threadIdx.x == 0) s_base = s_total ? atomicAdd(counter, (unsigned long long)s_total) : 0;
-    __syncthreads();
-    uint32_t id = (uint32_t)s_base + off;
-    while (mine) {
-      const int k = __ffs(mine) - 1;
-      mine &= mine - 1;
-      rpos[id] = (uint32_t)(p0 + k);
-      sl[p0 + k] = id << kOffBits;
-      ++id;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void k_append_heads(const uint32_t* heads, int64_t H, uint32_t* rpos, uint32_t* sl,
-                               unsigned long long* counter) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < H;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t hd = heads[i];
-    if (is_hash_ruler(hd)) continue;
-    const uint32_t id = (uint32_t)atomicAdd(counter, 1ull);
-    rpos[id] = hd;
-    sl[hd] = id << kOffBits;
-  }
-}
-
-// One thread per ruler in [lo, hi). Dynamic rulers are appended at
-// *rcount (device counter) and walked by the next launch.
-__global__ void __launch_bounds__(kBlock)
-    k_walk(const uint32_t* __restrict__ succ, int stride, uint32_t* rpos, uint32_t* __restrict__ rlen,
-           uint32_t* __restrict__ rnext, uint32_t* sl, uint32_t lo, uint32_t hi,
-           unsigned long long* rcount) {
-  const int64_t t = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= hi) return;
-  const uint32_t i = (uint32_t)t;
-  const uint32_t tag = i << kOffBits;
-  uint32_t cur = succ[(size_t)rpos[i] * stride];
-  uint32_t off = 1;
-  uint32_t nxt = kNone32;
-  for (;;) {
-    if (cur == kNone32) break;
-    if (is_hash_ruler(cur)) {
-      nxt = ld_cg(&sl[cur]) >> kOffBits;
-      break;
-    }
-    if (off > kWalkCap) {  // split: cur becomes a new ruler
-      const uint32_t nid = (uint32_t)atomicAdd(rcount, 1ull);
-      rpos[nid] = cur;
-      sl[cur] = nid << kOffBits;
-      nxt = nid;
-      break;
-    }
-    sl[cur] = tag | off;
-    ++off;
-    cur = succ[(size_t)cur * stride];
-  }
-  rlen[i] = off;
-  rnext[i] = nxt;
-}
-
-// pred over the ruler list, packed Wyllie word (prefix << 32 | jump).
-__global__ void k_ruler_pred(int64_t R, const uint32_t* rnext, uint32_t* pred) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t nx = rnext[i];
-    if (nx != kNone32) pred[nx] = (uint32_t)i;
-  }
-}
-__global__ void k_ruler_wyllie_init(int64_t R, const uint32_t* pred, const uint32_t* rlen,
-                                    unsigned long long* w) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t p = pred[i];
-    w[i] = (p == kNone32) ? (unsigned long long)kNone32 : (((unsigned long long)rlen[p] << 32) | p);
-  }
-}
-__global__ void k_ruler_wyllie(int64_t R, const unsigned long long* __restrict__ w,
-                               unsigned long long* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long x = w[i];
-    const uint32_t j = (uint32_t)x;
-    if (j == kNone32) {
-      out[i] = x;
-      continue;
-    }
-    const unsigned long long y = w[j];
-    out[i] = (((x >> 32) + (y >> 32)) << 32) | (y & 0xffffffffull);
-  }
-}
-// Verification (only for caller-supplied structures that may not be
-// forests): every ruler chain must have ended and every arc been visited.
-__global__ void k_lr_verify(int64_t R, const unsigned long long* w, int64_t E, const uint32_t* sl,
-                            int* bad) {
-  const int64_t total = R > E ? R : E;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < R && (uint32_t)w[i] != kNone32) *bad = 1;
-    if (i < E && sl[i] == kNone32) *bad = 1;
-  }
-}
-__global__ void k_ruler_extract(int64_t R, const unsigned long long* w, uint32_t* rstart) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
-       i += (int64_t)gridDim.x * blockDim.x)
-    rstart[i] = (uint32_t)(w[i] >> 32);
-}
-
-static int ceil_log2_i(int64_t x) {
+static int ceil_log2_ll(int64_t x) {
   int k = 0;
-  int64_t p = 1;
-  while (p < x) {
-    p <<= 1;
-    ++k;
-  }
+  while ((int64_t{1} << k) < x) ++k;
   return k;
 }
 
-// Returns rstart (device, R entries); sl filled for every arc:
-// rank(p) = rstart[sl[p] >> 7] + (sl[p] & 127).
-const uint32_t* list_rank_rulers(Handle& h, int64_t E, const uint32_t* succ, int stride,
-                                 const uint32_t* heads, int64_t H, uint32_t* sl, int64_t* R_out,
-                                 bool verify) {
-  const int64_t cap = E / (1 << kLogK) * 2 + H + E / kWalkCap + 64;
-  uint32_t* rpos = h.ws<uint32_t>(WS_RPOS, cap);
-  uint32_t* rlen = h.ws<uint32_t>(WS_RLEN, cap);
-  uint32_t* rnext = h.ws<uint32_t>(WS_RNEXT, cap);
-  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box) + 8;
+static int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = getenv(name);
+  if (!e) return dflt;
+  const int v = atoi(e);
+  return (v < lo || v > hi) ? dflt : v;
+}
 
-  h.timer.begin(h.stream, "lr.rulers");
-  if (verify) CK(cudaMemsetAsync(sl, 0xFF, E * sizeof(uint32_t), h.stream));
-  CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), h.stream));
-  k_find_rulers<<<grid_for(E), kBlock, 0, h.stream>>>(E, rpos, sl, ctr);
-  if (H > 0) k_append_heads<<<grid_for(H), kBlock, 0, h.stream>>>(heads, H, rpos, sl, ctr);
-  CK_LAUNCH();
-  h.stats.step(E, H > 0 ? 2 : 1);
-  h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
-  uint32_t R = (uint32_t)h.host_box[0];
-  if ((int64_t)R > cap) throw std::runtime_error("ruler capacity exceeded");
-  h.timer.end(h.stream);
+LrParams lr_params(int64_t E, int64_t heads_bound) {
+  LrParams P;
+  P.logk0 = env_int("RSTG_LR_LOGK0", 4, 1, 10);
+  P.logk1 = env_int("RSTG_LR_LOGK1", 3, 1, 10);
+  P.chains = env_int("RSTG_LR_CHAINS", 1, 1, 4);
+  if (P.chains == 3) P.chains = 2;
+  // static rulers: hash hits (~E/2^logk, the Weyl sequence is
+  // equidistributed; 2x slack) + heads; dynamic splits add <= E/walk_cap
+  const int64_t stat = 2 * (E >> P.logk0) + heads_bound + 1024;
+  int idb = ceil_log2_ll(stat + (E >> 6) + 64);
+  if (idb < 1) idb = 1;
+  if (idb > 31) throw std::runtime_error("list ranking: too many arcs");
+  P.ob = 32 - idb;
+  if (P.ob > 16) P.ob = 16;
+  P.walk_cap = (1u << P.ob) - 1u;
+  P.cap = stat + E / P.walk_cap + 64;
+  if (P.cap >= (int64_t{1} << (32 - P.ob))) throw std::runtime_error("list ranking: capacity");
+  return P;
+}
 
-  // Walks; dynamic rulers are counted from R upwards.
-  h.timer.begin(h.stream, "lr.walk");
-  uint32_t lo = 0, hi = R;
-  while (lo < hi) {
-    if ((int64_t)hi + (int64_t)(hi - lo) > std::min<int64_t>(cap, kMaxRulers))
-      throw std::runtime_error("list ranking: ruler capacity exceeded");
-    const unsigned grid = (unsigned)((hi - lo + kBlock - 1) / kBlock);
-    k_walk<<<grid, kBlock, 0, h.stream>>>(succ, stride, rpos, rlen, rnext, sl, lo, hi, ctr);
-    CK_LAUNCH();
-    h.stats.launches++;
-    h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
-    lo = hi;
-    hi = (uint32_t)h.host_box[0];
+static unsigned persistent_grid() { return (unsigned)num_sms() * (2048 / kBlock); }
+
+// ------------------------------------------------------------- level 0
+template <int kChains>
+__global__ void __launch_bounds__(kBlock)
+    k_walk0(const uint32_t* __restrict__ succ, uint32_t* rpos, uint32_t* __restrict__ rlen,
+            uint32_t* __restrict__ rnext, uint32_t* sl, const unsigned long long* range,
+            unsigned long long* ctr, int logk, int ob, uint32_t walk_cap, uint32_t cap) {
+  // Rulers in chunks of kChunk ids dealt round-robin to the CTAs: CTA b
+  // walks chunks b, b + G, b + 2G, ... in order, so the rulers in flight
+  // over the whole grid form a sliding window of ids -- and ids follow
+  // positions (tile-ordered registration) -- which keeps the touched part
+  // of succ and sl L2-resident instead of spreading over the whole tour.
+  __shared__ uint32_t s_claim;
+  const uint32_t lo = (uint32_t)range[0], hi = (uint32_t)range[1];
+  if (threadIdx.x == 0) s_claim = 0;
+  __syncthreads();
+  // Each walk is a small state machine that issues exactly ONE load per
+  // loop iteration, whatever its state (claim -> rpos, start/hop -> succ,
+  // at the next ruler -> its word): the lanes of a warp, all in different
+  // states, then wait for one memory latency per iteration instead of one
+  // per branch taken.
+  enum : uint32_t { kClaim = 0, kStart, kHop, kRuler, kDone };
+  uint32_t st[kChains], id[kChains], cur[kChains], off[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) st[c] = kClaim;
+  for (;;) {
+    const uint32_t* ptr[kChains];
+    bool live = false;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      if (st[c] == kClaim) {
+        const uint32_t j = atomicAdd(&s_claim, 1u);
+        const uint64_t t = lo + ((uint64_t)(j / kChunk) * gridDim.x + blockIdx.x) * kChunk + j % kChunk;
+        if (t < hi) {
+          id[c] = (uint32_t)t;
+          ptr[c] = &rpos[t];
+        } else {
+          st[c] = kDone;
+        }
+      } else if (st[c] == kStart) {
+        ptr[c] = &succ[cur[c]];
+        off[c] = 1;
+      } else if (st[c] == kHop) {
+        sl[cur[c]] = (id[c] << ob) | off[c];
+        ++off[c];
+        ptr[c] = &succ[cur[c]];
+      } else if (st[c] == kRuler) {
+        ptr[c] = &sl[cur[c]];
+      }
+      live |= st[c] != kDone;
+    }
+    if (!live) break;
+    uint32_t val[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) val[c] = st[c] != kDone ? __ldg(ptr[c]) : 0u;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      const uint32_t x = val[c];
+      if (st[c] == kClaim) {
+        cur[c] = x;
+        st[c] = kStart;
+      } else if (st[c] == kRuler) {
+        rlen[id[c]] = off[c];
+        rnext[id[c]] = x >> ob;
+        st[c] = kClaim;
+      } else if (st[c] == kStart || st[c] == kHop) {
+        if (x == kNone32) {
+          rlen[id[c]] = off[c];
+          rnext[id[c]] = kNone32;
+          st[c] = kClaim;
+        } else if (lr_hash_ruler(x, logk)) {
+          cur[c] = x;
+          st[c] = kRuler;
+        } else if (off[c] > walk_cap) {  // split: x becomes a dynamic ruler
+          const uint32_t nid = (uint32_t)atomicAdd(ctr, 1ull);
+          if (nid < cap) {  // else counted only: the host throws on the count
+            rpos[nid] = x;
+            sl[x] = nid << ob;
+          }
+          rlen[id[c]] = off[c];
+          rnext[id[c]] = nid;
+          st[c] = kClaim;
+        } else {
+          cur[c] = x;
+          st[c] = kHop;
+        }
+      }
+    }
   }
-  // Counters stay deterministic although the number of follow-up walks
-  // (dynamic rulers) depends on the tour layout: one logical barrier, E arcs.
-  h.stats.steps++;
-  h.stats.work += E;
-  const int64_t R_static = R;
-  R = hi;
-  h.timer.end(h.stream);
+}
 
-  // Prefix over the ruler lists.
-  h.timer.begin(h.stream, "lr.rulers_rank");
-  // sized by the deterministic capacity, not R (R varies with the tour
-  // layout; a grow-only buffer must not reallocate inside the timed loop)
-  uint32_t* pred = h.ws<uint32_t>(WS_RA, cap);
-  unsigned long long* wa = h.ws<unsigned long long>(WS_RB, cap);
-  unsigned long long* wb = h.ws<unsigned long long>(WS_RC, cap);
-  uint32_t* rstart = h.ws<uint32_t>(WS_RD, cap);
-  CK(cudaMemsetAsync(pred, 0xFF, R * sizeof(uint32_t), h.stream));
-  const unsigned g = grid_for(R);
-  k_ruler_pred<<<g, kBlock, 0, h.stream>>>(R, rnext, pred);
-  k_ruler_wyllie_init<<<g, kBlock, 0, h.stream>>>(R, pred, rlen, wa);
+// Overflowed registration: remember the true count in spill[0] and clamp.
+__global__ void k_clamp_count(unsigned long long* ctr, unsigned long long cap,
+                              unsigned long long* spill) {
+  spill[0] = *ctr;
+  if (*ctr > cap) *ctr = cap;
+}
+
+static void launch_walk0(Handle& h, const LrParams& P, const uint32_t* succ, uint32_t* rpos,
+                         uint32_t* rlen, uint32_t* rnext, uint32_t* sl,
+                         const unsigned long long* range, unsigned long long* ctr) {
+  const unsigned g = persistent_grid();
+  if (P.chains == 1)
+    k_walk0<1><<<g, kBlock, 0, h.stream>>>(succ, rpos, rlen, rnext, sl, range, ctr, P.logk0, P.ob,
+                                           P.walk_cap, (uint32_t)P.cap);
+  else if (P.chains == 2)
+    k_walk0<2><<<g, kBlock, 0, h.stream>>>(succ, rpos, rlen, rnext, sl, range, ctr, P.logk0, P.ob,
+                                           P.walk_cap, (uint32_t)P.cap);
+  else
+    k_walk0<4><<<g, kBlock, 0, h.stream>>>(succ, rpos, rlen, rnext, sl, range, ctr, P.logk0, P.ob,
+                                           P.walk_cap, (uint32_t)P.cap);
   CK_LAUNCH();
-  h.stats.step(R_static, 2);
-  // round count from the deterministic capacity (>= ceil(log2 R) + 1)
-  const int rounds = ceil_log2_i(cap < 2 ? 2 : cap) + 1;
+}
+
+// range[0..1] = [lo, hi) of the next walk launch from the ruler counter.
+__global__ void k_lr_range(unsigned long long* range, const unsigned long long* ctr) {
+  range[0] = range[1];
+  range[1] = *ctr;
+}
+
+// -------------------------------------------------------- levels >= 1
+__global__ void k_mark_pred(int64_t N, const uint32_t* __restrict__ next, uint8_t* haspred) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t nx = next[x];
+    if (nx != kNone32) haspred[nx] = 1;
+  }
+}
+
+// Rulers of a weighted level: hash hits with a predecessor, and heads of
+// lists with more than one node. Singletons get sub = NONE (prefix 0).
+__global__ void __launch_bounds__(kBlock)
+    k_register1(int64_t N, const uint32_t* __restrict__ next, const uint8_t* __restrict__ haspred,
+                uint32_t* rpos, uint32_t* sub, uint32_t* off, unsigned long long* ctr, int logk) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < N; b += stride) {
+    const int64_t x = b + threadIdx.x;
+    bool want = false;
+    if (x < N) {
+      const bool hp = haspred[x] != 0;
+      const bool single = !hp && next[x] == kNone32;
+      want = hp ? lr_hash_ruler((uint32_t)x, logk) : !single;
+      if (single) {
+        sub[x] = kNone32;
+        off[x] = 0;
+      }
+    }
+    const uint32_t id = lr_block_claim(want ? 1u : 0u, ctr);
+    if (want) {
+      rpos[id] = (uint32_t)x;
+      sub[x] = id;
+      off[x] = 0;
+    }
+  }
+}
+
+template <int kChains>
+__global__ void __launch_bounds__(kBlock)
+    k_walk1(const uint32_t* __restrict__ next, const uint32_t* __restrict__ w,
+            const uint32_t* __restrict__ rpos, const unsigned long long* ctr, uint32_t* sub,
+            uint32_t* __restrict__ off, uint32_t* __restrict__ rw, uint32_t* __restrict__ rn,
+            int logk) {
+  __shared__ uint32_t s_claim;
+  const uint32_t R = (uint32_t)*ctr;
+  if (threadIdx.x == 0) s_claim = 0;
+  __syncthreads();
+  // the same one-load-per-iteration state machine as k_walk0 (two
+  // independent loads in the hop state: next and weight of a node)
+  enum : uint32_t { kClaim = 0, kStart, kHop, kRuler, kDone };
+  uint32_t st[kChains], id[kChains], cur[kChains], acc[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) st[c] = kClaim;
+  for (;;) {
+    const uint32_t* pa[kChains];
+    const uint32_t* pb[kChains];
+    bool live = false;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      pb[c] = nullptr;
+      if (st[c] == kClaim) {
+        const uint32_t j = atomicAdd(&s_claim, 1u);
+        const uint64_t t = ((uint64_t)(j / kChunk) * gridDim.x + blockIdx.x) * kChunk + j % kChunk;
+        if (t < R) {
+          id[c] = (uint32_t)t;
+          pa[c] = &rpos[t];
+        } else {
+          st[c] = kDone;
+        }
+      } else if (st[c] == kStart) {
+        pa[c] = &next[cur[c]];
+        pb[c] = &w[cur[c]];
+      } else if (st[c] == kHop) {
+        sub[cur[c]] = id[c];
+        off[cur[c]] = acc[c];
+        pa[c] = &next[cur[c]];
+        pb[c] = &w[cur[c]];
+      } else if (st[c] == kRuler) {
+        pa[c] = &sub[cur[c]];
+      }
+      live |= st[c] != kDone;
+    }
+    if (!live) break;
+    uint32_t va[kChains], vb[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      va[c] = st[c] != kDone ? ld_cg(pa[c]) : 0u;
+      vb[c] = pb[c] ? __ldg(pb[c]) : 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      const uint32_t x = va[c];
+      if (st[c] == kClaim) {
+        cur[c] = x;
+        st[c] = kStart;
+      } else if (st[c] == kRuler) {
+        rw[id[c]] = acc[c];
+        rn[id[c]] = x;
+        st[c] = kClaim;
+      } else if (st[c] == kStart || st[c] == kHop) {
+        acc[c] = (st[c] == kStart ? 0u : acc[c]) + vb[c];
+        if (x == kNone32) {
+          rw[id[c]] = acc[c];
+          rn[id[c]] = kNone32;
+          st[c] = kClaim;
+        } else if (lr_hash_ruler(x, logk)) {  // every reachable hash hit is a ruler
+          cur[c] = x;
+          st[c] = kRuler;
+        } else {
+          cur[c] = x;
+          st[c] = kHop;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_expand(int64_t N, const uint32_t* __restrict__ sub, const uint32_t* __restrict__ off,
+                         const uint32_t* __restrict__ pre1, uint32_t* __restrict__ pre) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = sub[x];
+    pre[x] = (s == kNone32) ? 0u : pre1[s] + off[x];
+  }
+}
+
+// Verification: every node of the level was visited (sub set).
+__global__ void k_check_visited(int64_t N, const uint32_t* sub, const uint32_t* next,
+                                const uint8_t* haspred, int* bad) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
+       x += (int64_t)gridDim.x * blockDim.x)
+    if (sub[x] == kNone32 && (haspred[x] || next[x] != kNone32)) *bad = 1;
+}
+
+// Base case: one CTA, Wyllie over predecessor pointers in shared memory:
+// pre[x] = sum of w over the predecessors of x. A pointer still live after
+// ceil(log2 N) + 1 rounds means a cycle.
+__global__ void __launch_bounds__(1024)
+    k_lr_base(int N, const uint32_t* __restrict__ next, const uint32_t* __restrict__ w,
+              uint32_t* __restrict__ pre, int rounds, int* bad) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* p = sm;        // predecessor pointer
+  uint32_t* v = sm + N;    // accumulated prefix
+  for (int x = threadIdx.x; x < N; x += blockDim.x) p[x] = kNone32;
+  __syncthreads();
+  for (int x = threadIdx.x; x < N; x += blockDim.x) {
+    const uint32_t nx = next[x];
+    if (nx != kNone32) p[nx] = (uint32_t)x;
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < N; x += blockDim.x) v[x] = (p[x] == kNone32) ? 0u : w[p[x]];
+  __syncthreads();
+  constexpr int kPer = kBaseMax / 1024;
   for (int r = 0; r < rounds; ++r) {
-    k_ruler_wyllie<<<g, kBlock, 0, h.stream>>>(R, wa, wb);
-    CK_LAUNCH();
-    h.stats.step(R_static);
-    std::swap(wa, wb);
+    uint32_t np[kPer], nv[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int x = threadIdx.x + k * 1024;
+      if (x < N) {
+        const uint32_t q = p[x];
+        np[k] = (q == kNone32) ? kNone32 : p[q];
+        nv[k] = (q == kNone32) ? v[x] : v[x] + v[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int x = threadIdx.x + k * 1024;
+      if (x < N) {
+        p[x] = np[k];
+        v[x] = nv[k];
+      }
+    }
+    __syncthreads();
   }
-  k_ruler_extract<<<g, kBlock, 0, h.stream>>>(R, wa, rstart);
-  CK_LAUNCH();
-  h.stats.step(R_static);
-  if (verify) {
-    int* bad = reinterpret_cast<int*>(h.dev_box + 52);
-    CK(cudaMemsetAsync(bad, 0, sizeof(int), h.stream));
-    k_lr_verify<<<grid_for(std::max<int64_t>(R, E)), kBlock, 0, h.stream>>>(R, wa, E, sl, bad);
+  for (int x = threadIdx.x; x < N; x += blockDim.x) {
+    if (p[x] != kNone32) *bad = 1;
+    pre[x] = v[x];
+  }
+}
+
+// pre[x] = sum of w over the nodes before x in its list.
+static void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t* next,
+                        const uint32_t* w, uint32_t* pre, int depth, bool verify, int* bad) {
+  if (N <= 0) return;
+  const cudaStream_t s = h.stream;
+  if (N <= kBaseMax) {
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_lr_base, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(2 * kBaseMax * sizeof(uint32_t))));
+      attr = true;
+    }
+    k_lr_base<<<1, 1024, 2 * N * sizeof(uint32_t), s>>>((int)N, next, w, pre,
+                                                         ceil_log2_ll(N < 2 ? 2 : N) + 1, bad);
     CK_LAUNCH();
+    h.stats.step(N);
+    return;
+  }
+  if (depth >= 12) throw std::runtime_error("list ranking: recursion too deep");
+  // level arena: haspred N, sub N, off N, rpos N, rw N, rn N, pre1 N
+  uint8_t* arena = h.ws<uint8_t>(WS_LR_L1 + depth, (size_t)N * (1 + 6 * 4) + 64);
+  uint8_t* haspred = arena;
+  uint32_t* sub = reinterpret_cast<uint32_t*>(arena + ((N + 15) & ~int64_t{15}));
+  uint32_t* off = sub + N;
+  uint32_t* rpos = off + N;
+  uint32_t* rw = rpos + N;
+  uint32_t* rn = rw + N;
+  uint32_t* pre1 = rn + N;
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box) + 9;
+  CK(cudaMemsetAsync(haspred, 0, (size_t)N, s));
+  CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
+  if (verify) CK(cudaMemsetAsync(sub, 0xFF, (size_t)N * 4, s));
+  const unsigned g = grid_for(N);
+  k_mark_pred<<<g, kBlock, 0, s>>>(N, next, haspred);
+  k_register1<<<g, kBlock, 0, s>>>(N, next, haspred, rpos, sub, off, ctr, P.logk1);
+  if (P.chains == 1)
+    k_walk1<1><<<persistent_grid(), kBlock, 0, s>>>(next, w, rpos, ctr, sub, off, rw, rn, P.logk1);
+  else if (P.chains == 2)
+    k_walk1<2><<<persistent_grid(), kBlock, 0, s>>>(next, w, rpos, ctr, sub, off, rw, rn, P.logk1);
+  else
+    k_walk1<4><<<persistent_grid(), kBlock, 0, s>>>(next, w, rpos, ctr, sub, off, rw, rn, P.logk1);
+  CK_LAUNCH();
+  h.stats.step(N, 3);
+  if (verify) {
+    k_check_visited<<<g, kBlock, 0, s>>>(N, sub, next, haspred, bad);
+    CK_LAUNCH();
+  }
+  h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
+  const int64_t R1 = h.host_box[0];
+  list_prefix(h, P, R1, rn, rw, pre1, depth + 1, verify, bad);
+  k_expand<<<g, kBlock, 0, s>>>(N, sub, off, pre1, pre);
+  CK_LAUNCH();
+  h.stats.step(N);
+}
+
+__global__ void k_check_words(int64_t E, const uint32_t* sl, int* bad) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < E;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if (sl[p] == kNone32) *bad = 1;
+}
+
+const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t* succ, uint32_t* sl,
+                        uint32_t* rpos, unsigned long long* ctr, bool verify, int64_t* R_out) {
+  const cudaStream_t s = h.stream;
+  if (ctr != reinterpret_cast<unsigned long long*>(h.dev_box) + 8)
+    throw std::logic_error("lr_rank: ruler counter must be dev_box[8]");
+  uint32_t* rlen = h.ws<uint32_t>(WS_RLEN, P.cap);
+  uint32_t* rnext = h.ws<uint32_t>(WS_RNEXT, P.cap);
+  unsigned long long* range = reinterpret_cast<unsigned long long*>(h.dev_box) + 10;  // [10], [11]
+  int* bad = reinterpret_cast<int*>(h.dev_box + 52);
+  if (verify) CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+
+  h.timer.begin(s, "lr.walk", 8.0 * E);
+  // registration overflow (more rulers than P.cap) is caught from the count
+  // read after the walk; the walk only ever touches ids below the count,
+  // so bound it first on the device
+  k_clamp_count<<<1, 1, 0, s>>>(ctr, (unsigned long long)P.cap, range + 2);
+  CK(cudaMemsetAsync(range, 0, 2 * sizeof(unsigned long long), s));
+  k_lr_range<<<1, 1, 0, s>>>(range, ctr);
+  launch_walk0(h, P, succ, rpos, rlen, rnext, sl, range, ctr);
+  CK_LAUNCH();
+  h.stats.step(E, 2);
+  // one readback: ctr (dev_box[8]), the [lo, hi) just walked (dev_box[10..11])
+  // and the registered count before clamping (dev_box[12])
+  h.read_box(reinterpret_cast<int64_t*>(ctr), 5);
+  if (h.host_box[4] > P.cap) throw std::runtime_error("list ranking: ruler capacity exceeded");
+  int64_t hi = h.host_box[3];
+  int64_t R = h.host_box[0];
+  while (R > hi) {  // walks that split: their new rulers (rare)
+    if (R > P.cap) throw std::runtime_error("list ranking: ruler capacity exceeded");
+    k_lr_range<<<1, 1, 0, s>>>(range, ctr);
+    launch_walk0(h, P, succ, rpos, rlen, rnext, sl, range, ctr);
+    CK_LAUNCH();
+    h.stats.launches += 2;
+    hi = R;
+    h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
+    R = h.host_box[0];
+  }
+  if (R > P.cap) throw std::runtime_error("list ranking: ruler capacity exceeded");
+  if (verify) {  // every position reached by a walk (a cycle without a ruler is not)
+    k_check_words<<<grid_for(E), kBlock, 0, s>>>(E, sl, bad);
+    CK_LAUNCH();
+  }
+  h.timer.end(s);
+
+  h.timer.begin(s, "lr.rulers_rank", 16.0 * R);
+  uint32_t* rstart = h.ws<uint32_t>(WS_RD, P.cap);
+  list_prefix(h, P, R, rnext, rlen, rstart, 0, verify, bad);
+  if (verify) {
     h.read_box(reinterpret_cast<int64_t*>(bad), 1);
     if (*reinterpret_cast<int*>(h.host_box))
       throw AlgoError("list ranking failed to converge: not a forest");
   }
-  h.timer.end(h.stream);
+  h.timer.end(s);
   if (R_out) *R_out = R;
+  return rstart;
+}
+
+// ------------------------------------------------------- generic lists
+__global__ void __launch_bounds__(kBlock)
+    k_register0(int64_t E, const uint32_t* __restrict__ succ, const uint8_t* __restrict__ haspred,
+                uint32_t* rpos, uint32_t* sl, unsigned long long* ctr, int logk, int ob,
+                uint32_t cap) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < E; b += stride) {
+    const int64_t p = b + threadIdx.x;
+    const bool want = p < E && (lr_hash_ruler((uint32_t)p, logk) || !haspred[p]);
+    const uint32_t id = lr_block_claim(want ? 1u : 0u, ctr);
+    if (want) lr_put(id, (uint32_t)p, rpos, sl, ob, cap);
+  }
+}
+
+const uint32_t* lr_rank_lists(Handle& h, int64_t E, const uint32_t* succ, uint32_t* sl, bool verify,
+                              LrParams* P_out) {
+  const LrParams P = lr_params(E, E);
+  uint32_t* rpos = h.ws<uint32_t>(WS_RPOS, P.cap);
+  uint8_t* haspred = h.ws<uint8_t>(WS_ISROOT, E);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box) + 8;
+  CK(cudaMemsetAsync(haspred, 0, (size_t)E, h.stream));
+  CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), h.stream));
+  if (verify) CK(cudaMemsetAsync(sl, 0xFF, (size_t)E * 4, h.stream));
+  k_mark_pred<<<grid_for(E), kBlock, 0, h.stream>>>(E, succ, haspred);
+  k_register0<<<grid_for(E), kBlock, 0, h.stream>>>(E, succ, haspred, rpos, sl, ctr, P.logk0, P.ob,
+                                                    (uint32_t)P.cap);
+  CK_LAUNCH();
+  h.stats.step(E, 2);
+  const uint32_t* rstart = lr_rank(h, P, E, succ, sl, rpos, ctr, verify, nullptr);
+  if (P_out) *P_out = P;
   return rstart;
 }
 

@@ -250,12 +250,19 @@ __global__ void __launch_bounds__(kTileThreads)
   }
   if (kLocal && io.link) {
     // the tile's lists become the vertices' local lists (plain stores;
-    // links from other tiles went to the remote lists)
+    // links from other tiles went to the remote lists), each closed into
+    // its rotation cycle right away: next(tail) = head (the Euler pass
+    // re-splices the few vertices that also have a remote list, and opens
+    // the roots' cycles)
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
       const uint32_t hd = s_head[i];
       io.eu.vhead[base + i] = hd;
-      if (hd != kNone32) io.eu.vtail[base + i] = s_tail[i];
+      if (hd != kNone32) {
+        const uint32_t tl = s_tail[i];
+        io.eu.vtail[base + i] = tl;
+        io.eu.S[arc_rev(tl, io.eu.nslots)] = hd;
+      }
     }
   }
   if (SRC != kSrcRep) {

@@ -169,6 +169,7 @@ enum WsSlot : int {
   WS_RTAIL,       // u32 n         its last arc (the first one inserted)
   WS_ETO,         // u32 2N        arc heads, pairs (2i: a->b, 2i+1: b->a)
   WS_XBITS,       // u32 n/32      exit-set membership bitmap (cc.cu)
+  WS_LABELS,      // u32 n         one label per component (euler.cu)
   // list-ranking levels >= 1 (listrank.cu), one arena per level
   WS_LR_L1,
   WS_LR_LAST = WS_LR_L1 + 12,

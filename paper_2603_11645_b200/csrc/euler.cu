@@ -26,9 +26,8 @@
 
 namespace rstg {
 
-// min_vertex per label (euler_rooting.cpp:190-195). Labels are vertex ids;
-// a warp whose lanes share a label (the common case: one giant component)
-// issues one atomic instead of 32.
+// min_vertex per label (euler_rooting.cpp:190-195) on its own (the BFS
+// seeds use it); labels are vertex ids, lanes sharing one issue one atomic.
 __global__ void __launch_bounds__(kBlock)
     k_min_vertex(int64_t n, const int32_t* __restrict__ lab, uint32_t* minv) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -36,10 +35,8 @@ __global__ void __launch_bounds__(kBlock)
     const int64_t v = b + threadIdx.x;
     const int32_t l = v < n ? lab[v] : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, l);
-    // lanes are in ascending v order: the lowest lane of a label group
-    // holds its smallest vertex
-    const int lane = threadIdx.x & 31;
-    if (v < n && lane == __ffs(peers) - 1 && (uint32_t)v < minv[l]) atomicMin(&minv[l], (uint32_t)v);
+    if (v < n && (threadIdx.x & 31) == __ffs(peers) - 1 && (uint32_t)v < minv[l])
+      atomicMin(&minv[l], (uint32_t)v);
   }
 }
 void launch_min_vertex(Handle& h, const int32_t* lab, uint32_t* minv) {
@@ -47,90 +44,128 @@ void launch_min_vertex(Handle& h, const int32_t* lab, uint32_t* minv) {
   CK_LAUNCH();
   h.stats.step(h.g.n);
 }
+
 __global__ void k_override_root(const int32_t* lab, uint32_t* minv, int32_t root) {
   if (threadIdx.x == 0 && blockIdx.x == 0 && root >= 0) minv[lab[root]] = (uint32_t)root;
 }
 
-// Vertex pass: roots (parent[r] = r, derive_parents :167 for roots), the
-// successor wrap of every non-root list, the heads of the roots' tours, and
-// the rulers. cc_slots: slot v (arcs 2v, 2v+1) is valid iff lab[v] != v.
-// Tiles of kFixItems x kBlock vertices, one ruler-id claim per tile.
+// Labels present (explicit forests: caller labels need not be rep roots).
+__global__ void k_mark_labels(int64_t n, const int32_t* __restrict__ lab, uint8_t* present) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    present[lab[v]] = 1;
+}
+
+// Vertex pass, in tiles of kFixItems x kBlock vertices claimed in order:
+//   * min_vertex per label (euler_rooting.cpp:190-195): lanes sharing a
+//     label (one giant component: all of them) issue one atomicMin;
+//   * the label list (one entry per component) for the root pass;
+//   * rotation cycles: round 0 closed every local list already; a vertex
+//     with a remote list gets local + remote spliced into one cycle;
+//   * the list-ranking rulers among its slot's arcs (cc_slots: slot v holds
+//     a tree edge iff lab[v] != v), one id claim per tile, so ruler ids
+//     follow positions.
+// Most vertices touch two coalesced words here (label, remote head).
 constexpr int kFixItems = 8;
 __global__ void __launch_bounds__(kBlock)
-    k_euler_fix(int64_t n, const int32_t* __restrict__ lab, const uint32_t* __restrict__ minv,
-                EulerIO io, bool cc_slots, int32_t* __restrict__ parent, uint32_t* rpos,
-                uint32_t* sl, unsigned long long* ctr, unsigned long long* comps,
+    k_euler_fix(int64_t n, const int32_t* __restrict__ lab, const uint8_t* __restrict__ present,
+                uint32_t* minv, EulerIO io, bool cc_slots, uint32_t* labels_out,
+                unsigned long long* nlabels, uint32_t* rpos, uint32_t* sl, unsigned long long* ctr,
                 unsigned long long* tiles, int logk, int ob, uint32_t cap) {
   constexpr int64_t kTile = (int64_t)kFixItems * kBlock;
   __shared__ unsigned long long s_tile;
-  uint32_t nroots = 0;
-  // tiles claimed in order from a counter: ruler ids then follow positions
+  __shared__ uint32_t s_nl;
+  __shared__ unsigned long long s_lb;
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_tile = atomicAdd(tiles, 1ull);
+    if (threadIdx.x == 0) {
+      s_tile = atomicAdd(tiles, 1ull);
+      s_nl = 0;
+    }
     __syncthreads();
     const int64_t base = (int64_t)s_tile * kTile;
     if (base >= n) break;
-    uint32_t flags = 0;  // 3 bits per item: head, arc 2v, arc 2v+1
-    uint32_t hdv[kFixItems];
+    uint32_t flags = 0;  // 2 bits per item: arc v, arc N + v; bit 16+k: label
 #pragma unroll
     for (int k = 0; k < kFixItems; ++k) {
       const int64_t v = base + k * kBlock + threadIdx.x;
-      hdv[k] = kNone32;
+      const int32_t l = v < n ? lab[v] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, l);
       if (v >= n) continue;
-      const int32_t l = lab[v];
-      const bool root = minv[l] == (uint32_t)v;
-      // local list, then the remote list: one rotation
-      const uint32_t h1 = io.vhead[v], h2 = io.rhead[v];
-      uint32_t hd = h1, tl = kNone32;
-      if (h1 != kNone32) {
-        tl = io.vtail[v];
-        if (h2 != kNone32) {
-          io.S[arc_rev(tl, io.nslots)] = h2;  // next(local tail) = remote head
-          tl = io.rtail[v];
+      if ((threadIdx.x & 31) == __ffs(peers) - 1 && (uint32_t)v < minv[l])
+        atomicMin(&minv[l], (uint32_t)v);  // the group's lowest lane has its smallest vertex
+      if (present ? present[v] != 0 : l == (int32_t)v) flags |= 1u << (16 + k);
+      const uint32_t h2 = io.rhead[v];
+      if (h2 != kNone32) {
+        const uint32_t h1 = io.vhead[v], t2 = io.rtail[v];
+        if (h1 != kNone32) {
+          io.S[arc_rev(io.vtail[v], io.nslots)] = h2;  // next(local tail) = remote head
+          io.S[arc_rev(t2, io.nslots)] = h1;           // next(remote tail) = local head
+        } else {
+          io.S[arc_rev(t2, io.nslots)] = h2;
         }
-      } else if (h2 != kNone32) {
-        hd = h2;
-        tl = io.rtail[v];
-      }
-      hdv[k] = hd;
-      if (root) {
-        parent[v] = (int32_t)v;
-        ++nroots;
-        if (hd != kNone32 && !lr_hash_ruler(hd, logk)) flags |= 1u << (3 * k);
-      } else if (hd != kNone32) {
-        io.S[arc_rev(tl, io.nslots)] = hd;  // last arc wraps to the first
       }
       if (cc_slots && l != (int32_t)v) {
-        if (lr_hash_ruler((uint32_t)v, logk)) flags |= 2u << (3 * k);
-        if (lr_hash_ruler(io.nslots + (uint32_t)v, logk)) flags |= 4u << (3 * k);
+        if (lr_hash_ruler((uint32_t)v, logk)) flags |= 1u << (2 * k);
+        if (lr_hash_ruler(io.nslots + (uint32_t)v, logk)) flags |= 2u << (2 * k);
       }
     }
-    uint32_t id = lr_block_claim(__popc(flags), ctr);
+    uint32_t id = lr_block_claim(__popc(flags & 0xFFFFu), ctr);
+    const uint32_t nl = __popc(flags >> 16);
+    uint32_t li = nl ? atomicAdd(&s_nl, nl) : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0 && s_nl) s_lb = atomicAdd(nlabels, (unsigned long long)s_nl);
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < kFixItems; ++k) {
       const uint32_t v = (uint32_t)(base + k * kBlock + threadIdx.x);
-      const uint32_t f = (flags >> (3 * k)) & 7u;
-      if (f & 1u) lr_put(id++, hdv[k], rpos, sl, ob, cap);
-      if (f & 2u) lr_put(id++, v, rpos, sl, ob, cap);
-      if (f & 4u) lr_put(id++, io.nslots + v, rpos, sl, ob, cap);
+      if (flags & (1u << (2 * k))) lr_put(id++, v, rpos, sl, ob, cap);
+      if (flags & (2u << (2 * k))) lr_put(id++, io.nslots + v, rpos, sl, ob, cap);
+      if (flags & (1u << (16 + k))) labels_out[s_lb + li++] = v;
     }
   }
-  for (int o = 16; o > 0; o >>= 1) nroots += __shfl_xor_sync(0xffffffffu, nroots, o);
-  if ((threadIdx.x & 31) == 0 && nroots) atomicAdd(comps, (unsigned long long)nroots);
 }
 
-// Rulers of explicit slots [0, T): hash-selected arcs, one claim per tile.
+// Root pass over the labels: the root of label x is minv[x] (the designated
+// root already stored for its label): parent[r] = r (derive_parents :167),
+// its rotation cycle opened just before its first arc (break_cycles
+// :96-101) and that first arc registered as the head ruler of its tour.
 __global__ void __launch_bounds__(kBlock)
-    k_register_slots(int64_t T, uint32_t* rpos, uint32_t* sl, unsigned long long* ctr, int logk,
-                     int ob, uint32_t cap) {
+    k_euler_roots(const uint32_t* __restrict__ labels, const unsigned long long* nlabels,
+                  const uint32_t* __restrict__ minv, EulerIO io, int32_t* parent, uint32_t* rpos,
+                  uint32_t* sl, unsigned long long* ctr, int logk, int ob, uint32_t cap) {
+  const int64_t L = (int64_t)*nlabels;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < L; b += stride) {
+    const int64_t i = b + threadIdx.x;
+    uint32_t hd = kNone32;
+    if (i < L) {
+      const uint32_t r = minv[labels[i]];
+      parent[r] = (int32_t)r;
+      const uint32_t h1 = io.vhead[r], h2 = io.rhead[r];
+      hd = h1 != kNone32 ? h1 : h2;
+      if (hd != kNone32) {
+        const uint32_t tl = h2 != kNone32 ? io.rtail[r] : io.vtail[r];
+        io.S[arc_rev(tl, io.nslots)] = kNone32;  // the tour ends back at the root
+      }
+    }
+    const bool head = hd != kNone32 && !lr_hash_ruler(hd, logk);
+    const uint32_t id = lr_block_claim(head ? 1u : 0u, ctr);
+    if (head) lr_put(id, hd, rpos, sl, ob, cap);
+  }
+}
+
+// Hash-selected rulers of explicit slots [0, T) (all occupied).
+__global__ void __launch_bounds__(kBlock)
+    k_register_slots(int64_t T, uint32_t nslots, uint32_t* rpos, uint32_t* sl,
+                     unsigned long long* ctr, int logk, int ob, uint32_t cap) {
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < T; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = b + threadIdx.x;
     const bool a0 = i < T && lr_hash_ruler((uint32_t)i, logk);
-    const bool a1 = i < T && lr_hash_ruler((uint32_t)(T + i), logk);
+    const bool a1 = i < T && lr_hash_ruler(nslots + (uint32_t)i, logk);
     uint32_t id = lr_block_claim((uint32_t)a0 + (uint32_t)a1, ctr);
     if (a0) lr_put(id++, (uint32_t)i, rpos, sl, ob, cap);
-    if (a1) lr_put(id++, (uint32_t)(T + i), rpos, sl, ob, cap);
+    if (a1) lr_put(id++, nslots + (uint32_t)i, rpos, sl, ob, cap);
   }
 }
 
@@ -145,7 +180,7 @@ __global__ void k_link_edges(int64_t T, const int2* __restrict__ edges, EulerIO 
 // derive_parents (:172-176) on (ruler, offset) ranks, one thread per slot.
 __global__ void __launch_bounds__(kBlock)
     k_orient(int64_t N, const int32_t* __restrict__ lab, bool cc_slots,
-             const uint2* __restrict__ eto, const uint32_t* __restrict__ sl,
+             const uint2* __restrict__ eto, const uint32_t* __restrict__ sl,  // the rank words
              const uint32_t* __restrict__ rstart, int ob, int32_t* __restrict__ parent) {
   const uint32_t mask = (1u << ob) - 1u;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
@@ -199,20 +234,30 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   unsigned long long* tiles = reinterpret_cast<unsigned long long*>(h.dev_box) + 13;
   const cudaStream_t s = h.stream;
 
-  h.timer.begin(s, "euler.roots", 4.0 * n + 4.0 * n + 16.0 * n);
+  uint32_t* lablist = h.ws<uint32_t>(WS_LABELS, n + 1);
+  // labels + remote heads read, min table written, one label entry per component
+  h.timer.begin(s, "euler.roots", 4.0 * n + 4.0 * n + 4.0 * n);
   CK(cudaMemsetAsync(minv, 0xFF, n * sizeof(uint32_t), s));
   CK(cudaMemsetAsync(h.dev_box + 4, 0, sizeof(int64_t), s));
   CK(cudaMemsetAsync(h.dev_box + 8, 0, sizeof(int64_t), s));
   CK(cudaMemsetAsync(h.dev_box + 13, 0, sizeof(int64_t), s));
-  if (verify && E > 0) CK(cudaMemsetAsync(sl, 0xFF, E * sizeof(uint32_t), s));
-  k_min_vertex<<<grid_for(n), kBlock, 0, s>>>(n, labels, minv);
+  uint8_t* present = nullptr;
+  if (!cc_slots) {
+    present = h.ws<uint8_t>(WS_ISROOT, n);
+    CK(cudaMemsetAsync(present, 0, (size_t)n, s));
+    k_mark_labels<<<grid_for(n), kBlock, 0, s>>>(n, labels, present);
+  }
+  k_euler_fix<<<grid_for((n + kFixItems - 1) / kFixItems), kBlock, 0, s>>>(
+      n, labels, present, minv, io, cc_slots, lablist, comps, rpos, sl, ctr, tiles, P.logk0, P.ob,
+      (uint32_t)P.cap);
   k_override_root<<<1, 32, 0, s>>>(labels, minv, designated_root);
-  k_euler_fix<<<grid_for((n + kFixItems - 1) / kFixItems), kBlock, 0, s>>>(n, labels, minv, io, cc_slots, parent, rpos, sl, ctr,
-                                             comps, tiles, P.logk0, P.ob, (uint32_t)P.cap);
+  k_euler_roots<<<grid_for(n), kBlock, 0, s>>>(lablist, comps, minv, io, parent, rpos, sl, ctr,
+                                               P.logk0, P.ob, (uint32_t)P.cap);
   if (!cc_slots && T > 0)
-    k_register_slots<<<grid_for(T), kBlock, 0, s>>>(T, rpos, sl, ctr, P.logk0, P.ob, (uint32_t)P.cap);
+    k_register_slots<<<grid_for(T), kBlock, 0, s>>>(T, io.nslots, rpos, sl, ctr, P.logk0, P.ob,
+                                                    (uint32_t)P.cap);
   CK_LAUNCH();
-  h.stats.step(n, cc_slots ? 3 : 4);
+  h.stats.step(n, cc_slots ? 3 : 5);
   h.timer.end(s);
   if (verify) {
     h.read_box(reinterpret_cast<int64_t*>(comps), 1);
@@ -223,7 +268,7 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   }
   if (T == 0) return;
 
-  const uint32_t* rstart = lr_rank(h, P, E, io.S, sl, rpos, ctr, verify, nullptr);
+  const uint32_t* rstart = lr_rank(h, P, E, io.S, sl, rpos, ctr, verify, 2 * T, nullptr);
 
   h.timer.begin(s, "euler.orient", 8.0 * N + 16.0 * T + 4.0 * T);
   k_orient<<<grid_for(N), kBlock, 0, s>>>(N, labels, cc_slots, reinterpret_cast<const uint2*>(io.eto),

@@ -75,23 +75,30 @@ template <int kChains>
 __global__ void __launch_bounds__(kBlock)
     k_walk0(const uint32_t* __restrict__ succ, uint32_t* rpos, uint32_t* __restrict__ rlen,
             uint32_t* __restrict__ rnext, uint32_t* sl, const unsigned long long* range,
-            unsigned long long* ctr, int logk, int ob, uint32_t walk_cap, uint32_t cap) {
+            unsigned long long* ctr, unsigned long long* walked, int logk, int ob, uint32_t walk_cap,
+            uint32_t cap) {
   // Rulers in chunks of kChunk ids dealt round-robin to the CTAs: CTA b
   // walks chunks b, b + G, b + 2G, ... in order, so the rulers in flight
   // over the whole grid form a sliding window of ids -- and ids follow
   // positions (tile-ordered registration) -- which keeps the touched part
   // of succ and sl L2-resident instead of spreading over the whole tour.
   __shared__ uint32_t s_claim;
+  __shared__ unsigned long long s_walked;
   const uint32_t lo = (uint32_t)range[0], hi = (uint32_t)range[1];
-  if (threadIdx.x == 0) s_claim = 0;
+  if (threadIdx.x == 0) {
+    s_claim = 0;
+    s_walked = 0;
+  }
   __syncthreads();
-  // Each walk is a small state machine that issues exactly ONE load per
-  // loop iteration, whatever its state (claim -> rpos, start/hop -> succ,
-  // at the next ruler -> its word): the lanes of a warp, all in different
-  // states, then wait for one memory latency per iteration instead of one
-  // per branch taken.
+  // Each walk is a small state machine issuing exactly ONE load per loop
+  // iteration whatever its state (claim -> rpos, start/hop -> succ, at the
+  // next ruler -> its word), so the lanes of a warp, all in different
+  // states, wait for one memory latency per iteration. (Writing the words
+  // over succ in place halves the traffic but serialises each hop's load
+  // behind the previous hop's store to the same sector: 4x slower.)
   enum : uint32_t { kClaim = 0, kStart, kHop, kRuler, kDone };
   uint32_t st[kChains], id[kChains], cur[kChains], off[kChains];
+  uint64_t mine = 0;
 #pragma unroll
   for (int c = 0; c < kChains; ++c) st[c] = kClaim;
   for (;;) {
@@ -133,11 +140,13 @@ __global__ void __launch_bounds__(kBlock)
       } else if (st[c] == kRuler) {
         rlen[id[c]] = off[c];
         rnext[id[c]] = x >> ob;
+        mine += off[c];
         st[c] = kClaim;
       } else if (st[c] == kStart || st[c] == kHop) {
         if (x == kNone32) {
           rlen[id[c]] = off[c];
           rnext[id[c]] = kNone32;
+          mine += off[c];
           st[c] = kClaim;
         } else if (lr_hash_ruler(x, logk)) {
           cur[c] = x;
@@ -150,6 +159,7 @@ __global__ void __launch_bounds__(kBlock)
           }
           rlen[id[c]] = off[c];
           rnext[id[c]] = nid;
+          mine += off[c];
           st[c] = kClaim;
         } else {
           cur[c] = x;
@@ -158,6 +168,10 @@ __global__ void __launch_bounds__(kBlock)
       }
     }
   }
+  // arcs covered (ruler itself included), for the forest check
+  if (mine) atomicAdd(&s_walked, (unsigned long long)mine);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_walked) atomicAdd(walked, s_walked);
 }
 
 // Overflowed registration: remember the true count in spill[0] and clamp.
@@ -167,18 +181,19 @@ __global__ void k_clamp_count(unsigned long long* ctr, unsigned long long cap,
   if (*ctr > cap) *ctr = cap;
 }
 
-static void launch_walk0(Handle& h, const LrParams& P, const uint32_t* succ, uint32_t* rpos,
+static void launch_walk0(Handle& h, const LrParams& P, const uint32_t* S, uint32_t* rsucc,
                          uint32_t* rlen, uint32_t* rnext, uint32_t* sl,
-                         const unsigned long long* range, unsigned long long* ctr) {
+                         const unsigned long long* range, unsigned long long* ctr,
+                         unsigned long long* walked) {
   const unsigned g = persistent_grid();
   if (P.chains == 1)
-    k_walk0<1><<<g, kBlock, 0, h.stream>>>(succ, rpos, rlen, rnext, sl, range, ctr, P.logk0, P.ob,
+    k_walk0<1><<<g, kBlock, 0, h.stream>>>(S, rsucc, rlen, rnext, sl, range, ctr, walked, P.logk0, P.ob,
                                            P.walk_cap, (uint32_t)P.cap);
   else if (P.chains == 2)
-    k_walk0<2><<<g, kBlock, 0, h.stream>>>(succ, rpos, rlen, rnext, sl, range, ctr, P.logk0, P.ob,
+    k_walk0<2><<<g, kBlock, 0, h.stream>>>(S, rsucc, rlen, rnext, sl, range, ctr, walked, P.logk0, P.ob,
                                            P.walk_cap, (uint32_t)P.cap);
   else
-    k_walk0<4><<<g, kBlock, 0, h.stream>>>(succ, rpos, rlen, rnext, sl, range, ctr, P.logk0, P.ob,
+    k_walk0<4><<<g, kBlock, 0, h.stream>>>(S, rsucc, rlen, rnext, sl, range, ctr, walked, P.logk0, P.ob,
                                            P.walk_cap, (uint32_t)P.cap);
   CK_LAUNCH();
 }
@@ -424,20 +439,16 @@ static void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t*
   h.stats.step(N);
 }
 
-__global__ void k_check_words(int64_t E, const uint32_t* sl, int* bad) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < E;
-       p += (int64_t)gridDim.x * blockDim.x)
-    if (sl[p] == kNone32) *bad = 1;
-}
-
-const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t* succ, uint32_t* sl,
-                        uint32_t* rpos, unsigned long long* ctr, bool verify, int64_t* R_out) {
+const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t* S, uint32_t* sl,
+                        uint32_t* rsucc, unsigned long long* ctr, bool verify, int64_t expect,
+                        int64_t* R_out) {
   const cudaStream_t s = h.stream;
   if (ctr != reinterpret_cast<unsigned long long*>(h.dev_box) + 8)
     throw std::logic_error("lr_rank: ruler counter must be dev_box[8]");
   uint32_t* rlen = h.ws<uint32_t>(WS_RLEN, P.cap);
   uint32_t* rnext = h.ws<uint32_t>(WS_RNEXT, P.cap);
   unsigned long long* range = reinterpret_cast<unsigned long long*>(h.dev_box) + 10;  // [10], [11]
+  unsigned long long* walked = reinterpret_cast<unsigned long long*>(h.dev_box) + 14;
   int* bad = reinterpret_cast<int*>(h.dev_box + 52);
   if (verify) CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
 
@@ -447,31 +458,28 @@ const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t*
   // so bound it first on the device
   k_clamp_count<<<1, 1, 0, s>>>(ctr, (unsigned long long)P.cap, range + 2);
   CK(cudaMemsetAsync(range, 0, 2 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(walked, 0, sizeof(unsigned long long), s));
   k_lr_range<<<1, 1, 0, s>>>(range, ctr);
-  launch_walk0(h, P, succ, rpos, rlen, rnext, sl, range, ctr);
-  CK_LAUNCH();
+  launch_walk0(h, P, S, rsucc, rlen, rnext, sl, range, ctr, walked);
   h.stats.step(E, 2);
-  // one readback: ctr (dev_box[8]), the [lo, hi) just walked (dev_box[10..11])
-  // and the registered count before clamping (dev_box[12])
-  h.read_box(reinterpret_cast<int64_t*>(ctr), 5);
+  // one readback: ctr [8], the [lo, hi) just walked [10..11], the count
+  // registered before clamping [12], arcs walked [14]
+  h.read_box(reinterpret_cast<int64_t*>(ctr), 7);
   if (h.host_box[4] > P.cap) throw std::runtime_error("list ranking: ruler capacity exceeded");
   int64_t hi = h.host_box[3];
   int64_t R = h.host_box[0];
   while (R > hi) {  // walks that split: their new rulers (rare)
     if (R > P.cap) throw std::runtime_error("list ranking: ruler capacity exceeded");
     k_lr_range<<<1, 1, 0, s>>>(range, ctr);
-    launch_walk0(h, P, succ, rpos, rlen, rnext, sl, range, ctr);
-    CK_LAUNCH();
+    launch_walk0(h, P, S, rsucc, rlen, rnext, sl, range, ctr, walked);
     h.stats.launches += 2;
     hi = R;
-    h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
+    h.read_box(reinterpret_cast<int64_t*>(ctr), 7);
     R = h.host_box[0];
   }
   if (R > P.cap) throw std::runtime_error("list ranking: ruler capacity exceeded");
-  if (verify) {  // every position reached by a walk (a cycle without a ruler is not)
-    k_check_words<<<grid_for(E), kBlock, 0, s>>>(E, sl, bad);
-    CK_LAUNCH();
-  }
+  if (verify && h.host_box[6] != expect)  // some position unreachable from every ruler
+    throw AlgoError("list ranking failed to converge: not a forest");
   h.timer.end(s);
 
   h.timer.begin(s, "lr.rulers_rank", 16.0 * R);
@@ -489,9 +497,8 @@ const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t*
 
 // ------------------------------------------------------- generic lists
 __global__ void __launch_bounds__(kBlock)
-    k_register0(int64_t E, const uint32_t* __restrict__ succ, const uint8_t* __restrict__ haspred,
-                uint32_t* rpos, uint32_t* sl, unsigned long long* ctr, int logk, int ob,
-                uint32_t cap) {
+    k_register0(int64_t E, const uint8_t* __restrict__ haspred, uint32_t* rpos, uint32_t* sl,
+                unsigned long long* ctr, int logk, int ob, uint32_t cap) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < E; b += stride) {
     const int64_t p = b + threadIdx.x;
@@ -509,13 +516,12 @@ const uint32_t* lr_rank_lists(Handle& h, int64_t E, const uint32_t* succ, uint32
   unsigned long long* ctr = reinterpret_cast<unsigned long long*>(h.dev_box) + 8;
   CK(cudaMemsetAsync(haspred, 0, (size_t)E, h.stream));
   CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), h.stream));
-  if (verify) CK(cudaMemsetAsync(sl, 0xFF, (size_t)E * 4, h.stream));
   k_mark_pred<<<grid_for(E), kBlock, 0, h.stream>>>(E, succ, haspred);
-  k_register0<<<grid_for(E), kBlock, 0, h.stream>>>(E, succ, haspred, rpos, sl, ctr, P.logk0, P.ob,
+  k_register0<<<grid_for(E), kBlock, 0, h.stream>>>(E, haspred, rpos, sl, ctr, P.logk0, P.ob,
                                                     (uint32_t)P.cap);
   CK_LAUNCH();
   h.stats.step(E, 2);
-  const uint32_t* rstart = lr_rank(h, P, E, succ, sl, rpos, ctr, verify, nullptr);
+  const uint32_t* rstart = lr_rank(h, P, E, succ, sl, rpos, ctr, verify, E, nullptr);
   if (P_out) *P_out = P;
   return rstart;
 }

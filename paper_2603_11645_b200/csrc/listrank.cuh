@@ -64,6 +64,7 @@ __device__ __forceinline__ uint32_t lr_block_claim(uint32_t c, unsigned long lon
   __syncthreads();
   return b;
 }
+// Registers position p as ruler `id`: rpos[id] = p, sl[p] = id << ob.
 __device__ __forceinline__ void lr_put(uint32_t id, uint32_t p, uint32_t* rpos, uint32_t* sl, int ob,
                                        uint32_t cap) {
   if (id < cap) {
@@ -77,13 +78,15 @@ class Handle;
 LrParams lr_params(int64_t E, int64_t heads_bound);
 
 // Walks every registered ruler (ids [0, *ctr) on the device, positions in
-// rpos) over succ, fills sl for every reachable position, then ranks the
-// ruler lists. Returns rstart (device, indexed by ruler id). When verify,
-// sl must have been set to all-ones beforehand for the `valid` positions
-// and an unreached position or a ruler cycle throws the reference's
-// "list ranking failed to converge: not a forest".
+// rpos) over succ and fills sl, for every position a walk reached, with
+// its word (ruler id << ob) | offset; then ranks the ruler lists. Returns
+// rstart (device, by ruler id): rank(p) = rstart[sl[p] >> ob] + (sl[p] & mask).
+// When verify, the walks must cover exactly `expect` positions (else a
+// cycle without a ruler exists) and the ruler lists must be acyclic, or
+// the reference's "list ranking failed to converge: not a forest" is thrown.
 const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t* succ, uint32_t* sl,
-                        uint32_t* rpos, unsigned long long* ctr, bool verify, int64_t* R_out);
+                        uint32_t* rpos, unsigned long long* ctr, bool verify, int64_t expect,
+                        int64_t* R_out);
 
 // Generic entry (rstg_k_list_rank, explicit lists): registers hash rulers
 // and every list head (positions without a predecessor), then lr_rank.

@@ -49,12 +49,18 @@ __global__ void k_cc_init(int64_t n, int32_t* rep, unsigned long long* slot) {
 constexpr int kHookItems = 8;
 constexpr int kHookTile = kHookItems * kBlock;
 
+// Hook rounds after round 0 skip the full compression pass (lazy mode): a
+// vertex's rep may then point at an old root that has since hooked, so the
+// root is found by walking up (find_root, engine.hpp). Roots are frozen for
+// the whole hook kernel (apply runs later), so the root found equals the
+// fully compressed label -- the proposals are exactly those of hook_step on
+// compressed labels.
 template <int MODE, bool WRITE>
 __global__ void __launch_bounds__(kBlock)
     k_hook(const int2* __restrict__ edges, int64_t count, uint32_t e_base,
-           const uint32_t* __restrict__ in_list, const int32_t* __restrict__ rep,
+           const uint32_t* __restrict__ in_list, int32_t* rep,
            unsigned long long* __restrict__ slot, int* any_proposal, uint32_t* __restrict__ out_list,
-           unsigned long long* out_count) {
+           unsigned long long* out_count, bool lazy) {
   __shared__ unsigned long long s_base;
   __shared__ uint32_t s_total;
   bool proposed = false;
@@ -70,16 +76,36 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
     for (int k = 0; k < kHookItems; ++k)
       e[k] = (idx[k] != kNone32) ? edges[idx[k]] : make_int2(0, 0);
+    // reps of both endpoints of all items first (independent loads), then
+    // in lazy mode their reps (independent again), then the rare deeper walks
+    int32_t ru[kHookItems], rv[kHookItems];
+#pragma unroll
+    for (int k = 0; k < kHookItems; ++k) {
+      ru[k] = rep[e[k].x];
+      rv[k] = rep[e[k].y];
+    }
+    if (lazy) {
+      int32_t gu[kHookItems], gv[kHookItems];
+#pragma unroll
+      for (int k = 0; k < kHookItems; ++k) {
+        gu[k] = rep[ru[k]];
+        gv[k] = rep[rv[k]];
+      }
+#pragma unroll
+      for (int k = 0; k < kHookItems; ++k) {
+        if (gu[k] != ru[k]) ru[k] = find_root(rep, e[k].x);
+        if (gv[k] != rv[k]) rv[k] = find_root(rep, e[k].y);
+      }
+    }
     uint32_t ncross = 0;
 #pragma unroll
     for (int k = 0; k < kHookItems; ++k) {
-      const int32_t ru = rep[e[k].x], rv = rep[e[k].y];
-      if (idx[k] == kNone32 || ru == rv) {
+      const int32_t lo = min(ru[k], rv[k]), hi = max(ru[k], rv[k]);
+      if (idx[k] == kNone32 || lo == hi) {
         idx[k] = kNone32;
         continue;
       }
       ++ncross;
-      const int32_t lo = min(ru, rv), hi = max(ru, rv);
       const int32_t winner = MODE == 0 ? lo : hi;
       const int32_t loser = MODE == 0 ? hi : lo;
       const unsigned long long key = pack_key((uint32_t)winner, e_base + idx[k]);
@@ -172,6 +198,8 @@ struct RoundIO {
   const int2* edges;
   bool link;                    // link new tree edges into the Euler rotation lists
   EulerIO eu;
+  uint32_t* roots;              // round 0: vertices left as roots (nullable)
+  unsigned long long* nroots;
 };
 
 template <int SRC>
@@ -195,6 +223,7 @@ __global__ void __launch_bounds__(kTileThreads)
     __syncthreads();
   }
   uint32_t hooked = 0;
+  uint32_t rootmask = 0;  // round 0: items of this thread that stay roots
   for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
     const int64_t v = base + i;
     int32_t r;
@@ -217,9 +246,11 @@ __global__ void __launch_bounds__(kTileThreads)
     } else {
       const uint32_t o = io.offsets[v];
       r = (int32_t)v;
+      rootmask |= 1u << (i / kTileThreads);  // cleared below if v hooks
       if (o < io.offsets[v + 1]) {
         const int32_t u = io.nbrs[o];
         if (u < r) {  // hooked onto its smallest neighbour by edge (u, v)
+          rootmask &= ~(1u << (i / kTileThreads));
           r = u;
           ++hooked;
           if (io.tflag) {
@@ -247,6 +278,18 @@ __global__ void __launch_bounds__(kTileThreads)
       }
     }
     s[i] = r;
+  }
+  if (kLocal && io.roots) {  // the round-0 roots, appended with one atomic per tile
+    __shared__ uint32_t s_rc;
+    __shared__ unsigned long long s_rb;
+    if (threadIdx.x == 0) s_rc = 0;
+    __syncthreads();
+    uint32_t pos = rootmask ? atomicAdd(&s_rc, (uint32_t)__popc(rootmask)) : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) s_rb = s_rc ? atomicAdd(io.nroots, (unsigned long long)s_rc) : 0ull;
+    __syncthreads();
+    for (uint32_t mk = rootmask; mk; mk &= mk - 1)
+      io.roots[s_rb + pos++] = (uint32_t)(base + threadIdx.x + (__ffs(mk) - 1) * kTileThreads);
   }
   if (kLocal && io.link) {
     // the tile's lists become the vertices' local lists (plain stores;
@@ -420,21 +463,23 @@ void launch_compress2(Handle& h, int32_t* rep, int64_t n) {
 }
 
 static void launch_hook_k(Handle& h, int mode, const int2* edges, int64_t count, uint32_t e_base,
-                          const uint32_t* in_list, const int32_t* rep, unsigned long long* slot,
+                          const uint32_t* in_list, const int32_t* rep_c, unsigned long long* slot,
                           int* any_prop, uint32_t* out_list, unsigned long long* out_count) {
   const unsigned grid = grid_for((count + kHookItems - 1) / kHookItems);
+  int32_t* rep = const_cast<int32_t*>(rep_c);  // lazy mode path-compresses
+  const bool lazy = h.cc_lazy;
   if (mode == 0 && out_list)
     k_hook<0, true><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
-                                                   any_prop, out_list, out_count);
+                                                   any_prop, out_list, out_count, lazy);
   else if (mode == 0)
     k_hook<0, false><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
-                                                    any_prop, out_list, out_count);
+                                                    any_prop, out_list, out_count, lazy);
   else if (out_list)
     k_hook<1, true><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
-                                                   any_prop, out_list, out_count);
+                                                   any_prop, out_list, out_count, lazy);
   else
     k_hook<1, false><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
-                                                    any_prop, out_list, out_count);
+                                                    any_prop, out_list, out_count, lazy);
   CK_LAUNCH();
   h.stats.step(count);
 }
@@ -473,6 +518,7 @@ void cc_round_done(Handle& h, int64_t out_count) {
   ++h.cc_round;
 }
 void cc_reset_rounds(Handle& h) {
+  h.cc_lazy = false;
   h.cc_round = 0;
   h.cc_active = -1;
   h.cc_list = 0;
@@ -485,6 +531,60 @@ void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tf
                                                      counter, tlist);
   CK_LAUNCH();
   h.stats.step(h.g.n);
+}
+
+// Lazy-mode apply (cc_forest.cpp:39-46) over the current roots only: a
+// root with a proposal takes its winner (rep[r] = winner, slot reset, tree
+// edge recorded / linked); the others stay roots for the next round.
+// list == nullptr: the roots are all vertices [0, n).
+__global__ void __launch_bounds__(kBlock)
+    k_apply_roots(const uint32_t* __restrict__ list, const unsigned long long* count, int64_t n,
+                  int32_t* rep, RoundIO io, uint32_t* out_list, unsigned long long* out_count) {
+  const int64_t R = list ? (int64_t)*count : n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  __shared__ uint32_t s_n, s_h;
+  __shared__ unsigned long long s_b;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < R; b += stride) {
+    if (threadIdx.x == 0) s_n = s_h = 0;
+    __syncthreads();
+    const int64_t i = b + threadIdx.x;
+    bool keep = false;
+    uint32_t r = 0;
+    if (i < R) {
+      r = list ? list[i] : (uint32_t)i;
+      const unsigned long long key = io.slot[r];
+      if (key == kKeyInf) {
+        keep = true;
+      } else {
+        rep[r] = (int32_t)(key >> 32);
+        io.slot[r] = kKeyInf;
+        const uint32_t e = (uint32_t)key - io.e_base;
+        if (io.tflag && e < io.m_local) io.tflag[e] = 1;
+        if (io.link) {
+          const int2 ab = io.edges[e];
+          link_tree_edge(io.eu, r, (uint32_t)ab.x, (uint32_t)ab.y);
+        }
+        atomicAdd(&s_h, 1u);
+      }
+    }
+    const uint32_t pos = keep ? atomicAdd(&s_n, 1u) : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_b = s_n ? atomicAdd(out_count, (unsigned long long)s_n) : 0ull;
+      if (s_h) atomicAdd(io.counter, (unsigned long long)s_h);
+    }
+    __syncthreads();
+    if (keep) out_list[s_b + pos] = r;
+    __syncthreads();
+  }
+}
+
+// Final labels of lazy mode: every vertex onto its root (one pass; the
+// roots are few and hot, so the walk is mostly cache hits).
+__global__ void __launch_bounds__(kBlock) k_find_all(int64_t n, int32_t* rep) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    find_root(rep, (int32_t)v);
 }
 
 void launch_cc_init(Handle& h, int32_t* rep, unsigned long long* slot) {
@@ -504,8 +604,12 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   h.timer.end(h.stream);
   int mode = 0;  // HookMode::kMin first (cc_forest.cpp:87)
   int* any = reinterpret_cast<int*>(h.dev_box + 2);
+  uint32_t* rlist = h.ws<uint32_t>(WS_CCROOTS, 2 * n + 2);
+  uint32_t* rl[2] = {rlist, rlist + n + 1};
+  unsigned long long* rcount = reinterpret_cast<unsigned long long*>(h.dev_box) + 20;  // [20], [21]: in / out
+  CK(cudaMemsetAsync(rcount, 0, sizeof(unsigned long long), h.stream));
   RoundIO io{slot, tflag, (uint32_t)h.g.e_base, (uint32_t)m, counter, h.g.offsets, h.g.nbrs,
-             h.g.arc_edge, h.g.edges, euler != nullptr, euler ? *euler : EulerIO{}};
+             h.g.arc_edge, h.g.edges, euler != nullptr, euler ? *euler : EulerIO{}, rl[0], rcount};
   cc_reset_rounds(h);
   int64_t round = 0;
   if (h.g.has_csr() && m > 0) {
@@ -519,9 +623,17 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
     round = 1;
     mode = 1;
   }
+  // Rounds >= 1 run lazy: no compression pass per round (hooks find roots,
+  // apply touches the current roots only), one find pass at the end.
+  int cur = 0;
+  bool have_list = round == 1;  // round 0 collected the roots
+  h.cc_lazy = true;
   int64_t total = 0;
   for (;; ++round) {
-    if (round > n + 1) throw AlgoError("hooking failed to converge");
+    if (round > n + 1) {
+      h.cc_lazy = false;
+      throw AlgoError("hooking failed to converge");
+    }
     CK(cudaMemsetAsync(counter + 1, 0, 2 * sizeof(unsigned long long), h.stream));
     // edge 8 B + two rep gathers per visited edge (+ 4 B list entry when filtered)
     const double visited = (h.cc_round >= 2 && h.cc_active >= 0) ? (double)h.cc_active : (double)m;
@@ -536,10 +648,26 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
     h.stats.rounds = round + 1;
     // a round without proposals applies nothing (cc_forest.cpp:91)
     if (!proposed) break;
-    h.timer.begin(h.stream, "cc.apply_compress", 16.0 * n);  // slot + rep read/write
-    resolve_round(h, rep, n, kSrcApply, io);
+    h.timer.begin(h.stream, "cc.apply", 16.0 * n);  // (upper bound: every vertex a root)
+    CK(cudaMemsetAsync(rcount + 1, 0, sizeof(unsigned long long), h.stream));
+    k_apply_roots<<<grid_for(n), kBlock, 0, h.stream>>>(have_list ? rl[cur] : nullptr, rcount, n,
+                                                        rep, io, rl[cur ^ 1], rcount + 1);
+    CK(cudaMemcpyAsync(rcount, rcount + 1, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                       h.stream));
+    CK_LAUNCH();
+    h.stats.step(n);
+    cur ^= 1;
+    have_list = true;
     h.timer.end(h.stream);
     mode ^= 1;
+  }
+  h.cc_lazy = false;
+  if (!euler) {  // (the Euler vertex pass finds the labels itself)
+    h.timer.begin(h.stream, "cc.final", 8.0 * n);  // rep read + write
+    k_find_all<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
+    CK_LAUNCH();
+    h.stats.step(n);
+    h.timer.end(h.stream);
   }
   h.stats.tree_edges = total;
   return total;

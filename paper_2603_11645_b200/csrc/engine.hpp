@@ -87,6 +87,7 @@ class Handle {
   int cc_round = 0;
   int64_t cc_active = -1;  // edges in the current active list, -1 = all
   int cc_list = 0;
+  bool cc_lazy = false;    // hook rounds find roots (no per-round compression)
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   DeviceGraph g;
@@ -102,7 +103,8 @@ class Handle {
   // Small pinned host mailbox for flag/count readbacks.
   int64_t* host_box = nullptr;
   // Device counters block (256 x int64) zeroed per use by the caller; fixed
-  // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,12] lr, [16] pr, [30] bfs, [40] validate,
+  // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,14] lr, [16] pr, [20,21] cc
+  // roots, [30] bfs, [40] validate,
   // [48] normalize, [50,53) capi/lr verify, [128,160) jump-round flags.
   int64_t* dev_box = nullptr;
 
@@ -170,6 +172,7 @@ enum WsSlot : int {
   WS_ETO,         // u32 2N        arc heads, pairs (2i: a->b, 2i+1: b->a)
   WS_XBITS,       // u32 n/32      exit-set membership bitmap (cc.cu)
   WS_LABELS,      // u32 n         one label per component (euler.cu)
+  WS_CCROOTS,     // u32 2(n+1)    current CC roots, ping-pong (cc.cu lazy rounds)
   // list-ranking levels >= 1 (listrank.cu), one arena per level
   WS_LR_L1,
   WS_LR_LAST = WS_LR_L1 + 12,
@@ -205,6 +208,22 @@ struct EulerIO {
 };
 
 #ifdef __CUDACC__
+// Root of x in a rep forest whose roots are frozen, path-compressing x
+// (every value a racing compression stores is a valid ancestor).
+__device__ __forceinline__ int32_t find_root(int32_t* rep, int32_t x) {
+  const int32_t p = rep[x];
+  if (p == x) return x;
+  int32_t r = rep[p];
+  if (r == p) return p;
+  for (;;) {
+    const int32_t q = rep[r];
+    if (q == r) break;
+    r = q;
+  }
+  rep[x] = r;
+  return r;
+}
+
 __device__ __forceinline__ void link_tree_edge(const EulerIO& io, uint32_t slot, uint32_t a,
                                                uint32_t b) {
   const uint32_t p = slot, q = io.nslots + slot;  // p: a -> b, q: b -> a
@@ -227,7 +246,8 @@ __device__ __forceinline__ uint32_t arc_rev(uint32_t p, uint32_t nslots) {
 // tlist (nullable, n entries): tlist[v] = global id of the tree edge that
 // hooked root v, or kNone32 (every tree edge appears exactly once).
 // euler (nullable): every tree edge is linked into the rotation lists as it
-// is created, slot = the vertex it hooked (EulerIO; N = n slots).
+// is created, slot = the vertex it hooked (EulerIO; N = n slots); the labels
+// are then left lazy (reps pointing at ancestors), euler_root resolves them.
 int64_t cc_exact(Handle& h, int32_t* labels, uint8_t* tflag, const EulerIO* euler = nullptr);
 // cc labels only, validity-level (any correct partition; used by BFS
 // seeding and the validator). Returns the number of hook rounds.

@@ -68,7 +68,7 @@ __global__ void k_mark_labels(int64_t n, const int32_t* __restrict__ lab, uint8_
 // Most vertices touch two coalesced words here (label, remote head).
 constexpr int kFixItems = 8;
 __global__ void __launch_bounds__(kBlock)
-    k_euler_fix(int64_t n, const int32_t* __restrict__ lab, const uint8_t* __restrict__ present,
+    k_euler_fix(int64_t n, const int32_t* lab, const uint8_t* __restrict__ present,
                 uint32_t* minv, EulerIO io, bool cc_slots, uint32_t* labels_out,
                 unsigned long long* nlabels, uint32_t* rpos, uint32_t* sl, unsigned long long* ctr,
                 unsigned long long* tiles, int logk, int ob, uint32_t cap) {
@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
     for (int k = 0; k < kFixItems; ++k) {
       const int64_t v = base + k * kBlock + threadIdx.x;
-      const int32_t l = v < n ? lab[v] : -1;
+      // CC labels may be lazy (cc_exact with Euler): resolve and compress
+      const int32_t l = v < n ? (cc_slots ? find_root(const_cast<int32_t*>(lab), (int32_t)v) : lab[v])
+                              : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, l);
       if (v >= n) continue;
       if ((threadIdx.x & 31) == __ffs(peers) - 1 && (uint32_t)v < minv[l])

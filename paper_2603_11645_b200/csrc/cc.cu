@@ -303,7 +303,6 @@ __global__ void __launch_bounds__(kTileThreads)
       io.eu.vhead[base + i] = hd;
       if (hd != kNone32) {
         const uint32_t tl = s_tail[i];
-        io.eu.vtail[base + i] = tl;
         io.eu.S[arc_rev(tl, io.eu.nslots)] = hd;
       }
     }
@@ -627,7 +626,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   // apply touches the current roots only), one find pass at the end.
   int cur = 0;
   bool have_list = round == 1;  // round 0 collected the roots
-  h.cc_lazy = true;
+  h.cc_lazy = false;  // the first hook sees compressed reps (round 0 compressed, or singletons)
   int64_t total = 0;
   for (;; ++round) {
     if (round > n + 1) {
@@ -660,6 +659,18 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
     have_list = true;
     h.timer.end(h.stream);
     mode ^= 1;
+    // Lazy finds cost extra gathers per active edge endpoint; while many
+    // edges are still active one compression pass over n is cheaper.
+    if (h.cc_active > n / 4) {
+      h.timer.begin(h.stream, "cc.compress", 8.0 * n);
+      k_find_all<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
+      CK_LAUNCH();
+      h.stats.step(n);
+      h.timer.end(h.stream);
+      h.cc_lazy = false;
+    } else {
+      h.cc_lazy = true;
+    }
   }
   h.cc_lazy = false;
   if (!euler) {  // (the Euler vertex pass finds the labels itself)

@@ -100,10 +100,12 @@ __global__ void __launch_bounds__(kBlock)
       const uint32_t h2 = io.rhead[v];
       if (h2 != kNone32) {
         const uint32_t h1 = io.vhead[v], t2 = io.rtail[v];
-        if (h1 != kNone32) {
-          io.S[arc_rev(io.vtail[v], io.nslots)] = h2;  // next(local tail) = remote head
-          io.S[arc_rev(t2, io.nslots)] = h1;           // next(remote tail) = local head
-        } else {
+        if (h1 != kNone32) {  // splice the remote list in right after the local head
+          const uint32_t ra = arc_rev(h1, io.nslots);
+          const uint32_t after = io.S[ra];  // next(h1) in the closed local cycle
+          io.S[ra] = h2;
+          io.S[arc_rev(t2, io.nslots)] = after;
+        } else {  // close the remote list into a cycle
           io.S[arc_rev(t2, io.nslots)] = h2;
         }
       }
@@ -130,8 +132,8 @@ __global__ void __launch_bounds__(kBlock)
 
 // Root pass over the labels: the root of label x is minv[x] (the designated
 // root already stored for its label): parent[r] = r (derive_parents :167),
-// its rotation cycle opened just before its first arc (break_cycles
-// :96-101) and that first arc registered as the head ruler of its tour.
+// its rotation cycle opened (break_cycles :96-101; any arc of the root may
+// start the tour) and the first arc registered as the head ruler.
 __global__ void __launch_bounds__(kBlock)
     k_euler_roots(const uint32_t* __restrict__ labels, const unsigned long long* nlabels,
                   const uint32_t* __restrict__ minv, EulerIO io, int32_t* parent, uint32_t* rpos,
@@ -144,11 +146,12 @@ __global__ void __launch_bounds__(kBlock)
     if (i < L) {
       const uint32_t r = minv[labels[i]];
       parent[r] = (int32_t)r;
-      const uint32_t h1 = io.vhead[r], h2 = io.rhead[r];
-      hd = h1 != kNone32 ? h1 : h2;
-      if (hd != kNone32) {
-        const uint32_t tl = h2 != kNone32 ? io.rtail[r] : io.vtail[r];
-        io.S[arc_rev(tl, io.nslots)] = kNone32;  // the tour ends back at the root
+      const uint32_t h1 = io.vhead[r];
+      const uint32_t a = h1 != kNone32 ? h1 : io.rhead[r];
+      if (a != kNone32) {  // open the cycle after arc a: the tour runs next(a) ... a
+        const uint32_t ra = arc_rev(a, io.nslots);
+        hd = io.S[ra];
+        io.S[ra] = kNone32;  // the tour ends entering the root along rev(a)
       }
     }
     const bool head = hd != kNone32 && !lr_hash_ruler(hd, logk);
@@ -206,7 +209,6 @@ EulerIO euler_buffers(Handle& h, int64_t N, bool local_written) {
   io.eto = h.ws<uint32_t>(WS_ETO, 2 * N);
   io.S = h.ws<uint32_t>(WS_SUCC, 2 * N);
   io.vhead = h.ws<uint32_t>(WS_VHEAD, h.g.n);
-  io.vtail = h.ws<uint32_t>(WS_VTAIL, h.g.n);
   io.rhead = h.ws<uint32_t>(WS_RHEAD, h.g.n);
   io.rtail = h.ws<uint32_t>(WS_RTAIL, h.g.n);
   if (!local_written) CK(cudaMemsetAsync(io.vhead, 0xFF, (size_t)h.g.n * sizeof(uint32_t), h.stream));

@@ -53,6 +53,8 @@ LrParams lr_params(int64_t E, int64_t heads_bound) {
   P.logk0 = env_int("RSTG_LR_LOGK0", 4, 1, 10);
   P.logk1 = env_int("RSTG_LR_LOGK1", 3, 1, 10);
   P.chains = env_int("RSTG_LR_CHAINS", 1, 1, 4);
+  P.walk_blocks = env_int("RSTG_LR_BLOCKS", 8, 1, 8);  // CTAs per SM of the level-0 walk
+  P.chunk = (uint32_t)env_int("RSTG_LR_CHUNK", 64, 1, 4096);
   if (P.chains == 3) P.chains = 2;
   // static rulers: hash hits (~E/2^logk, the Weyl sequence is
   // equidistributed; 2x slack) + heads; dynamic splits add <= E/walk_cap
@@ -76,7 +78,7 @@ __global__ void __launch_bounds__(kBlock)
     k_walk0(const uint32_t* __restrict__ succ, uint32_t* rpos, uint32_t* __restrict__ rlen,
             uint32_t* __restrict__ rnext, uint32_t* sl, const unsigned long long* range,
             unsigned long long* ctr, unsigned long long* walked, int logk, int ob, uint32_t walk_cap,
-            uint32_t cap) {
+            uint32_t cap, uint32_t chunk) {
   // Rulers in chunks of kChunk ids dealt round-robin to the CTAs: CTA b
   // walks chunks b, b + G, b + 2G, ... in order, so the rulers in flight
   // over the whole grid form a sliding window of ids -- and ids follow
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(kBlock)
     for (int c = 0; c < kChains; ++c) {
       if (st[c] == kClaim) {
         const uint32_t j = atomicAdd(&s_claim, 1u);
-        const uint64_t t = lo + ((uint64_t)(j / kChunk) * gridDim.x + blockIdx.x) * kChunk + j % kChunk;
+        const uint64_t t = lo + ((uint64_t)(j / chunk) * gridDim.x + blockIdx.x) * chunk + j % chunk;
         if (t < hi) {
           id[c] = (uint32_t)t;
           ptr[c] = &rpos[t];
@@ -185,16 +187,16 @@ static void launch_walk0(Handle& h, const LrParams& P, const uint32_t* S, uint32
                          uint32_t* rlen, uint32_t* rnext, uint32_t* sl,
                          const unsigned long long* range, unsigned long long* ctr,
                          unsigned long long* walked) {
-  const unsigned g = persistent_grid();
+  const unsigned g = (unsigned)num_sms() * P.walk_blocks;
   if (P.chains == 1)
     k_walk0<1><<<g, kBlock, 0, h.stream>>>(S, rsucc, rlen, rnext, sl, range, ctr, walked, P.logk0, P.ob,
-                                           P.walk_cap, (uint32_t)P.cap);
+                                           P.walk_cap, (uint32_t)P.cap, P.chunk);
   else if (P.chains == 2)
     k_walk0<2><<<g, kBlock, 0, h.stream>>>(S, rsucc, rlen, rnext, sl, range, ctr, walked, P.logk0, P.ob,
-                                           P.walk_cap, (uint32_t)P.cap);
+                                           P.walk_cap, (uint32_t)P.cap, P.chunk);
   else
     k_walk0<4><<<g, kBlock, 0, h.stream>>>(S, rsucc, rlen, rnext, sl, range, ctr, walked, P.logk0, P.ob,
-                                           P.walk_cap, (uint32_t)P.cap);
+                                           P.walk_cap, (uint32_t)P.cap, P.chunk);
   CK_LAUNCH();
 }
 
@@ -433,6 +435,8 @@ static void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t*
   }
   h.read_box(reinterpret_cast<int64_t*>(ctr), 1);
   const int64_t R1 = h.host_box[0];
+  static const bool dbg = getenv("RSTG_LR_DEBUG") != nullptr;
+  if (dbg) fprintf(stderr, "[lr] level %d: %lld nodes -> %lld rulers\n", depth + 1, (long long)N, (long long)R1);
   list_prefix(h, P, R1, rn, rw, pre1, depth + 1, verify, bad);
   k_expand<<<g, kBlock, 0, s>>>(N, sub, off, pre1, pre);
   CK_LAUNCH();

@@ -17,6 +17,8 @@ struct LrParams {
   int logk0 = 4;      // level-0 ruler density 1/2^logk0
   int logk1 = 3;      // ruler density of the ruler-list levels
   int chains = 1;     // walks in flight per thread (more thrash the L2)
+  int walk_blocks = 8;  // CTAs per SM of the level-0 walk
+  uint32_t chunk = 64;  // ruler ids per round-robin chunk
   int ob = 10;        // offset bits of the level-0 word
   uint32_t walk_cap;  // longest walk before a split, (1 << ob) - 1
   int64_t cap;        // ruler-id capacity

@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(kTileThreads)
       io.eu.vhead[base + i] = hd;
       if (hd != kNone32) {
         const uint32_t tl = s_tail[i];
+        io.eu.vtail[base + i] = tl;
         io.eu.S[arc_rev(tl, io.eu.nslots)] = hd;
       }
     }
@@ -457,6 +458,31 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
   h.stats.step(n);
 }
 
+// Compression after lazy rounds: every pointer chain runs through former
+// roots only (a vertex's first hop lands on a root of some earlier round),
+// so pointer-jumping the round-0 roots list in place (one cooperative
+// launch) and one gather rep[v] = rep[rep[v]] compress the whole forest.
+void compress_via_roots(Handle& h, int32_t* rep, int64_t n, const uint32_t* roots,
+                        const unsigned long long* nroots) {
+  int* flags = reinterpret_cast<int*>(h.dev_box + 6);  // 3 ints in dev_box[6..7]
+  CK(cudaMemsetAsync(h.dev_box + 6, 0, 2 * sizeof(int64_t), h.stream));
+  static int coop_blocks = 0;
+  if (!coop_blocks) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jump_x, kBlock, 0));
+    coop_blocks = std::max(1, per_sm) * num_sms();
+  }
+  int rounds = 2;
+  while ((int64_t{1} << (rounds - 2)) < n) ++rounds;
+  void* args[] = {(void*)&roots, (void*)&nroots, (void*)&rep, (void*)&flags, (void*)&rounds};
+  CK(cudaLaunchCooperativeKernel((void*)k_jump_x, dim3(coop_blocks), dim3(kBlock), args, 0,
+                                 h.stream));
+  h.stats.step(n);
+  k_final_gather<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
+  CK_LAUNCH();
+  h.stats.step(n);
+}
+
 void launch_compress2(Handle& h, int32_t* rep, int64_t n) {
   resolve_round(h, rep, n, kSrcRep, RoundIO{});
 }
@@ -578,14 +604,6 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-// Final labels of lazy mode: every vertex onto its root (one pass; the
-// roots are few and hot, so the walk is mostly cache hits).
-__global__ void __launch_bounds__(kBlock) k_find_all(int64_t n, int32_t* rep) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x)
-    find_root(rep, (int32_t)v);
-}
-
 void launch_cc_init(Handle& h, int32_t* rep, unsigned long long* slot) {
   k_cc_init<<<grid_for(h.g.n), kBlock, 0, h.stream>>>(h.g.n, rep, slot);
   CK_LAUNCH();
@@ -603,9 +621,12 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   h.timer.end(h.stream);
   int mode = 0;  // HookMode::kMin first (cc_forest.cpp:87)
   int* any = reinterpret_cast<int*>(h.dev_box + 2);
-  uint32_t* rlist = h.ws<uint32_t>(WS_CCROOTS, 2 * n + 2);
-  uint32_t* rl[2] = {rlist, rlist + n + 1};
-  unsigned long long* rcount = reinterpret_cast<unsigned long long*>(h.dev_box) + 20;  // [20], [21]: in / out
+  // roots lists: [0] the round-0 roots (kept: every former root), [1] and
+  // [2] the current roots, ping-pong
+  uint32_t* rlist = h.ws<uint32_t>(WS_CCROOTS, 3 * n + 3);
+  uint32_t* rl[3] = {rlist, rlist + n + 1, rlist + 2 * n + 2};
+  // dev_box [20] round-0 roots, [21] current roots in, [22] out
+  unsigned long long* rcount = reinterpret_cast<unsigned long long*>(h.dev_box) + 20;
   CK(cudaMemsetAsync(rcount, 0, sizeof(unsigned long long), h.stream));
   RoundIO io{slot, tflag, (uint32_t)h.g.e_base, (uint32_t)m, counter, h.g.offsets, h.g.nbrs,
              h.g.arc_edge, h.g.edges, euler != nullptr, euler ? *euler : EulerIO{}, rl[0], rcount};
@@ -624,10 +645,20 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   }
   // Rounds >= 1 run lazy: no compression pass per round (hooks find roots,
   // apply touches the current roots only), one find pass at the end.
-  int cur = 0;
-  bool have_list = round == 1;  // round 0 collected the roots
+  const bool have_r0 = round == 1;  // round 0 collected the roots
+  if (have_r0)
+    CK(cudaMemcpyAsync(rcount + 1, rcount, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                       h.stream));
+  const uint32_t* in_list = have_r0 ? rl[0] : nullptr;  // nullptr: all vertices
+  int out = 1;
+  auto compress = [&]() {
+    if (have_r0)
+      compress_via_roots(h, rep, n, rl[0], rcount);
+    else
+      resolve_round(h, rep, n, kSrcRep, RoundIO{});
+  };
   h.cc_lazy = false;  // the first hook sees compressed reps (round 0 compressed, or singletons)
-  int64_t total = 0;
+  int64_t total = 0, last_hooks = 0;
   for (;; ++round) {
     if (round > n + 1) {
       h.cc_lazy = false;
@@ -648,38 +679,40 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
     // a round without proposals applies nothing (cc_forest.cpp:91)
     if (!proposed) break;
     h.timer.begin(h.stream, "cc.apply", 16.0 * n);  // (upper bound: every vertex a root)
-    CK(cudaMemsetAsync(rcount + 1, 0, sizeof(unsigned long long), h.stream));
-    k_apply_roots<<<grid_for(n), kBlock, 0, h.stream>>>(have_list ? rl[cur] : nullptr, rcount, n,
-                                                        rep, io, rl[cur ^ 1], rcount + 1);
-    CK(cudaMemcpyAsync(rcount, rcount + 1, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+    CK(cudaMemsetAsync(rcount + 2, 0, sizeof(unsigned long long), h.stream));
+    k_apply_roots<<<grid_for(n), kBlock, 0, h.stream>>>(in_list, rcount + 1, n, rep, io, rl[out],
+                                                        rcount + 2);
+    CK(cudaMemcpyAsync(rcount + 1, rcount + 2, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
                        h.stream));
     CK_LAUNCH();
     h.stats.step(n);
-    cur ^= 1;
-    have_list = true;
+    in_list = rl[out];
+    out = out == 1 ? 2 : 1;
     h.timer.end(h.stream);
     mode ^= 1;
     // Lazy finds cost extra gathers per active edge endpoint; while many
-    // edges are still active one compression pass over n is cheaper.
+    // edges are still active one compression pass over n is cheaper (the
+    // two-level resolve: hook chains of one round may be long).
     if (h.cc_active > n / 4) {
       h.timer.begin(h.stream, "cc.compress", 8.0 * n);
-      k_find_all<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
-      CK_LAUNCH();
-      h.stats.step(n);
+      compress();
       h.timer.end(h.stream);
       h.cc_lazy = false;
     } else {
       h.cc_lazy = true;
     }
+    last_hooks = -total;  // completed when the next round reads the hook total
   }
-  h.cc_lazy = false;
-  if (!euler) {  // (the Euler vertex pass finds the labels itself)
-    h.timer.begin(h.stream, "cc.final", 8.0 * n);  // rep read + write
-    k_find_all<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
-    CK_LAUNCH();
-    h.stats.step(n);
+  last_hooks += total;
+  // Labels left lazy by the last productive round: the Euler vertex pass
+  // resolves them itself with find_root when that round hooked few roots
+  // (short chains); otherwise, and for every other caller, compress here.
+  if (h.cc_lazy && (!euler || last_hooks > n / 64)) {
+    h.timer.begin(h.stream, "cc.final", 8.0 * n);
+    compress();
     h.timer.end(h.stream);
   }
+  h.cc_lazy = false;
   h.stats.tree_edges = total;
   return total;
 }

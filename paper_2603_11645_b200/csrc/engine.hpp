@@ -103,7 +103,7 @@ class Handle {
   // Small pinned host mailbox for flag/count readbacks.
   int64_t* host_box = nullptr;
   // Device counters block (256 x int64) zeroed per use by the caller; fixed
-  // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,14] lr, [16] pr, [20,21] cc
+  // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,14] lr, [16] pr, [20,22] cc
   // roots, [30] bfs, [40] validate,
   // [48] normalize, [50,53) capi/lr verify, [128,160) jump-round flags.
   int64_t* dev_box = nullptr;
@@ -166,12 +166,13 @@ enum WsSlot : int {
   WS_VAL_C,
   // Euler tour (euler.cu): rotation lists
   WS_VHEAD,       // u32 n         first arc of each vertex's local rotation list
+  WS_VTAIL,       // u32 n         its last arc
   WS_RHEAD,       // u32 n         remote list (atomic prepends): first arc
   WS_RTAIL,       // u32 n         its last arc (the first one inserted)
   WS_ETO,         // u32 2N        arc heads, pairs (2i: a->b, 2i+1: b->a)
   WS_XBITS,       // u32 n/32      exit-set membership bitmap (cc.cu)
   WS_LABELS,      // u32 n         one label per component (euler.cu)
-  WS_CCROOTS,     // u32 2(n+1)    current CC roots, ping-pong (cc.cu lazy rounds)
+  WS_CCROOTS,     // u32 3(n+1)    round-0 roots + current CC roots, ping-pong (cc.cu)
   // list-ranking levels >= 1 (listrank.cu), one arena per level
   WS_LR_L1,
   WS_LR_LAST = WS_LR_L1 + 12,
@@ -193,8 +194,8 @@ enum WsSlot : int {
 //
 // Two lists per vertex, concatenated by the vertex pass after the CC: the
 // "local" one written by round 0's shared-memory tiles with plain stores
-// (vhead, every vertex covered, so no initialisation; closed into its
-// cycle at once), and the
+// (vhead/vtail, every vertex covered, so no initialisation; closed into
+// its cycle at once), and the
 // "remote" one that every other link prepends to with atomicExch
 // (rhead/rtail, NONE-initialised).
 struct EulerIO {
@@ -202,6 +203,7 @@ struct EulerIO {
   uint32_t* eto;    // N pairs (to(i), to(N + i)) = (b, a)
   uint32_t* S;      // 2N  successors
   uint32_t* vhead;  // n   local list: first arc
+  uint32_t* vtail;  // n   local list: last arc
   uint32_t* rhead;  // n   remote list: first arc (NONE-initialised)
   uint32_t* rtail;  // n   remote list: last arc (the first inserted)
 };

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kBlock)
     const int64_t base = (int64_t)s_tile * kTile;
     if (base >= n) break;
     uint32_t flags = 0;  // 2 bits per item: arc v, arc N + v; bit 16+k: label
+    uint32_t h2[kFixItems];
 #pragma unroll
     for (int k = 0; k < kFixItems; ++k) {
       const int64_t v = base + k * kBlock + threadIdx.x;
@@ -93,25 +94,30 @@ __global__ void __launch_bounds__(kBlock)
       const int32_t l = v < n ? (cc_slots ? find_root(const_cast<int32_t*>(lab), (int32_t)v) : lab[v])
                               : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, l);
+      h2[k] = kNone32;
       if (v >= n) continue;
       if ((threadIdx.x & 31) == __ffs(peers) - 1 && (uint32_t)v < minv[l])
         atomicMin(&minv[l], (uint32_t)v);  // the group's lowest lane has its smallest vertex
       if (present ? present[v] != 0 : l == (int32_t)v) flags |= 1u << (16 + k);
-      const uint32_t h2 = io.rhead[v];
-      if (h2 != kNone32) {
-        const uint32_t h1 = io.vhead[v], t2 = io.rtail[v];
-        if (h1 != kNone32) {  // splice the remote list in right after the local head
-          const uint32_t ra = arc_rev(h1, io.nslots);
-          const uint32_t after = io.S[ra];  // next(h1) in the closed local cycle
-          io.S[ra] = h2;
-          io.S[arc_rev(t2, io.nslots)] = after;
-        } else {  // close the remote list into a cycle
-          io.S[arc_rev(t2, io.nslots)] = h2;
-        }
-      }
+      h2[k] = io.rhead[v];
       if (cc_slots && l != (int32_t)v) {
         if (lr_hash_ruler((uint32_t)v, logk)) flags |= 1u << (2 * k);
         if (lr_hash_ruler(io.nslots + (uint32_t)v, logk)) flags |= 2u << (2 * k);
+      }
+    }
+    // Splices, their loads batched across the items (independent lists):
+    // local tail -> remote head and remote tail -> local head, or the remote
+    // list closed into a cycle of its own when there is no local list.
+#pragma unroll
+    for (int k = 0; k < kFixItems; ++k) {
+      if (h2[k] == kNone32) continue;
+      const int64_t v = base + k * kBlock + threadIdx.x;
+      const uint32_t h1 = io.vhead[v], t2 = io.rtail[v];
+      if (h1 != kNone32) {
+        io.S[arc_rev(io.vtail[v], io.nslots)] = h2[k];
+        io.S[arc_rev(t2, io.nslots)] = h1;
+      } else {
+        io.S[arc_rev(t2, io.nslots)] = h2[k];
       }
     }
     uint32_t id = lr_block_claim(__popc(flags & 0xFFFFu), ctr);
@@ -132,8 +138,8 @@ __global__ void __launch_bounds__(kBlock)
 
 // Root pass over the labels: the root of label x is minv[x] (the designated
 // root already stored for its label): parent[r] = r (derive_parents :167),
-// its rotation cycle opened (break_cycles :96-101; any arc of the root may
-// start the tour) and the first arc registered as the head ruler.
+// its rotation cycle opened just before its first arc (break_cycles
+// :96-101) and that first arc registered as the head ruler of its tour.
 __global__ void __launch_bounds__(kBlock)
     k_euler_roots(const uint32_t* __restrict__ labels, const unsigned long long* nlabels,
                   const uint32_t* __restrict__ minv, EulerIO io, int32_t* parent, uint32_t* rpos,
@@ -146,12 +152,11 @@ __global__ void __launch_bounds__(kBlock)
     if (i < L) {
       const uint32_t r = minv[labels[i]];
       parent[r] = (int32_t)r;
-      const uint32_t h1 = io.vhead[r];
-      const uint32_t a = h1 != kNone32 ? h1 : io.rhead[r];
-      if (a != kNone32) {  // open the cycle after arc a: the tour runs next(a) ... a
-        const uint32_t ra = arc_rev(a, io.nslots);
-        hd = io.S[ra];
-        io.S[ra] = kNone32;  // the tour ends entering the root along rev(a)
+      const uint32_t h1 = io.vhead[r], h2 = io.rhead[r];
+      hd = h1 != kNone32 ? h1 : h2;  // the combined list: local, then remote
+      if (hd != kNone32) {
+        const uint32_t tl = h2 != kNone32 ? io.rtail[r] : io.vtail[r];
+        io.S[arc_rev(tl, io.nslots)] = kNone32;  // the tour ends back at the root
       }
     }
     const bool head = hd != kNone32 && !lr_hash_ruler(hd, logk);
@@ -209,6 +214,7 @@ EulerIO euler_buffers(Handle& h, int64_t N, bool local_written) {
   io.eto = h.ws<uint32_t>(WS_ETO, 2 * N);
   io.S = h.ws<uint32_t>(WS_SUCC, 2 * N);
   io.vhead = h.ws<uint32_t>(WS_VHEAD, h.g.n);
+  io.vtail = h.ws<uint32_t>(WS_VTAIL, h.g.n);
   io.rhead = h.ws<uint32_t>(WS_RHEAD, h.g.n);
   io.rtail = h.ws<uint32_t>(WS_RTAIL, h.g.n);
   if (!local_written) CK(cudaMemsetAsync(io.vhead, 0xFF, (size_t)h.g.n * sizeof(uint32_t), h.stream));

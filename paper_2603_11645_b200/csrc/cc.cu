@@ -32,8 +32,8 @@ namespace rstg {
 __global__ void k_cc_init(int64_t n, int32_t* rep, unsigned long long* slot) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    rep[v] = (int32_t)v;
-    slot[v] = kKeyInf;
+    if (rep) rep[v] = (int32_t)v;
+    if (slot) slot[v] = kKeyInf;
   }
 }
 
@@ -71,11 +71,13 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
     for (int k = 0; k < kHookItems; ++k) {
       const int64_t i = base + k * kBlock + threadIdx.x;
-      idx[k] = (i < count) ? (in_list ? in_list[i] : (uint32_t)i) : kNone32;
+      idx[k] = (i < count) ? (in_list ? __ldcs(&in_list[i]) : (uint32_t)i) : kNone32;
     }
+    // the edge stream is read once: evict-first loads keep the L2 for the
+    // rep gathers and slot atomics
 #pragma unroll
     for (int k = 0; k < kHookItems; ++k)
-      e[k] = (idx[k] != kNone32) ? edges[idx[k]] : make_int2(0, 0);
+      e[k] = (idx[k] != kNone32) ? __ldcs(&edges[idx[k]]) : make_int2(0, 0);
     // reps of both endpoints of all items first (independent loads), then
     // in lazy mode their reps (independent again), then the rare deeper walks
     int32_t ru[kHookItems], rv[kHookItems];
@@ -614,8 +616,16 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   const int64_t n = h.g.n, m = h.g.m;
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(h.dev_box);
-  h.timer.begin(h.stream, "cc.init", 12.0 * n);  // rep + slot
-  launch_cc_init(h, rep, slot);
+  const bool round0 = h.g.has_csr() && m > 0;  // writes every rep itself
+  const bool slots_ok = h.slots_clean == slot;
+  h.slots_clean = nullptr;  // until this build completes
+  h.timer.begin(h.stream, "cc.init", (round0 ? 0.0 : 4.0 * n) + (slots_ok ? 0.0 : 8.0 * n));
+  if (!round0 || !slots_ok) {
+    k_cc_init<<<grid_for(n), kBlock, 0, h.stream>>>(n, round0 ? nullptr : rep,
+                                                     slots_ok ? nullptr : slot);
+    CK_LAUNCH();
+    h.stats.step(n);
+  }
   if (tflag && m > 0) CK(cudaMemsetAsync(tflag, 0, (size_t)m, h.stream));
   CK(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), h.stream));
   h.timer.end(h.stream);
@@ -714,6 +724,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   }
   h.cc_lazy = false;
   h.stats.tree_edges = total;
+  h.slots_clean = slot;
   return total;
 }
 

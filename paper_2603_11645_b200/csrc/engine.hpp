@@ -88,6 +88,10 @@ class Handle {
   int64_t cc_active = -1;  // edges in the current active list, -1 = all
   int cc_list = 0;
   bool cc_lazy = false;    // hook rounds find roots (no per-round compression)
+  // WS_SLOT holds all-empty keys from a completed cc_exact (apply resets
+  // every slot it consumes), so the next build skips re-initialising it;
+  // any other user of the slot buffer clears this.
+  const void* slots_clean = nullptr;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   DeviceGraph g;

@@ -235,7 +235,7 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   const int64_t E = 2 * N;  // arc position space (holes where a slot is empty)
   // lists = tours of components with an edge: at most min(T, n - T) heads
   // (the explicit, unverified input may have more: bound by n there)
-  const LrParams P = lr_params(E, verify ? n : std::min<int64_t>(T, n - T) + 1);
+  const LrParams P = lr_params(E, verify ? n : std::min<int64_t>(T, n - T) + 1, 2 * T);
   uint32_t* minv = h.ws<uint32_t>(WS_MINV, n);
   uint32_t* rpos = h.ws<uint32_t>(WS_RPOS, P.cap);
   uint32_t* sl = h.ws<uint32_t>(WS_SL, E);

@@ -22,11 +22,16 @@
 // equal the reference's list_rank output (distance from the list head):
 // checked arc for arc against the reference's own ranks
 // (tests/golden/euler_ranks.npz) and the oracle's Wyllie restatement.
+#include <cooperative_groups.h>
+
+#include <algorithm>
 #include <cstdlib>
 
 #include "engine.hpp"
 #include "listrank.cuh"
 #include "scan.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rstg {
 
@@ -48,12 +53,24 @@ static int env_int(const char* name, int dflt, int lo, int hi) {
   return (v < lo || v > hi) ? dflt : v;
 }
 
-LrParams lr_params(int64_t E, int64_t heads_bound) {
+LrParams lr_params(int64_t E, int64_t heads_bound, int64_t arcs) {
+  if (arcs < 0) arcs = E;  // positions actually on a list (the rest are holes)
   LrParams P;
-  P.logk0 = env_int("RSTG_LR_LOGK0", 4, 1, 10);
+  // Ruler density: sparse rulers cut the ruler levels' work but lengthen
+  // the longest sublist (the walk's critical path, ~2^k ln R hops), which
+  // dominates when the tour is short. 1/32 from 24M arcs, 1/8 below
+  // 4M (measured: grid 1M, road 24M, path 16M, RMAT-24).
+  const int lk = arcs >= (int64_t{24} << 20) ? 5 : arcs >= (int64_t{4} << 20) ? 4 : 3;
+  P.logk0 = env_int("RSTG_LR_LOGK0", lk, 1, 10);
   P.logk1 = env_int("RSTG_LR_LOGK1", 3, 1, 10);
   P.chains = env_int("RSTG_LR_CHAINS", 1, 1, 4);
-  P.walk_blocks = env_int("RSTG_LR_BLOCKS", 8, 1, 8);  // CTAs per SM of the level-0 walk
+  // one cooperative launch for the ruler levels measured slower than the
+  // host-driven recursion (grid barriers cost more than the syncs saved)
+  P.coop_levels = env_int("RSTG_LR_COOP", 0, 0, 1) != 0;
+  // CTAs per SM of the level-0 walk: 4 (1024 walks per SM) measured best on
+  // the road mesh -- more walks in flight thrash the L2 (profiles/)
+  // (a tour whose succ + word arrays fit in half the L2 keeps all 8)
+  P.walk_blocks = env_int("RSTG_LR_BLOCKS", arcs * 8 < (int64_t{48} << 20) ? 8 : 4, 1, 8);
   P.chunk = (uint32_t)env_int("RSTG_LR_CHUNK", 64, 1, 4096);
   if (P.chains == 3) P.chains = 2;
   // static rulers: hash hits (~E/2^logk, the Weyl sequence is
@@ -386,6 +403,264 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// ---------------------------------------- levels >= 1 in one launch
+// The whole ruler-list recursion as ONE cooperative kernel: per level a
+// pred-mark, a registration (tile-ordered claims), a weighted persistent
+// walk, each phase behind a grid barrier; the level that fits kBaseCoop
+// nodes is solved by CTA 0 in shared memory; then the expansions run back
+// down. No host round trip between levels (their sizes stay on the
+// device). Arenas are carved per level with halving capacities; a level
+// that outgrows its capacity sets *fallback and the host reruns the
+// host-driven recursion (list_prefix).
+constexpr int kMaxCoopLevels = 12;
+constexpr int kBaseCoop = 4096;
+struct LrLevel {
+  const uint32_t* next;  // this level's list
+  const uint32_t* w;
+  uint32_t* pre;         // this level's output
+  unsigned long long* N; // node count (device)
+  int64_t cap;           // capacity of this level's arrays
+  uint8_t* haspred;
+  uint32_t* sub;
+  uint32_t* off;
+  uint32_t* rpos;        // next level's nodes = this level's rulers
+};
+
+__global__ void __launch_bounds__(kBlock)
+    k_lr_levels(LrLevel* L, int maxl, int logk, bool verify, int* bad, int* fallback) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint32_t s_claim;
+  __shared__ uint32_t s_p[kBaseCoop], s_v[kBaseCoop];
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+  int k = 0;
+  for (; k < maxl; ++k) {
+    const int64_t N = (int64_t)*((volatile unsigned long long*)L[k].N);
+    if (N <= kBaseCoop) break;
+    if (k + 1 >= maxl || N > L[k].cap) {  // (uniform across the grid)
+      if (gtid == 0) *fallback = 1;
+      return;
+    }
+    const LrLevel& c = L[k];
+    const LrLevel& nx = L[k + 1];
+    if (gtid == 0) *nx.N = 0;
+    for (int64_t x = gtid; x < N; x += gsize) {
+      c.haspred[x] = 0;
+      if (verify) c.sub[x] = kNone32;
+    }
+    grid.sync();
+    for (int64_t x = gtid; x < N; x += gsize) {
+      const uint32_t n1 = c.next[x];
+      if (n1 != kNone32) c.haspred[n1] = 1;
+    }
+    grid.sync();
+    // registration: next level's nodes, one claim per CTA tile
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < N; b += gsize) {
+      const int64_t x = b + threadIdx.x;
+      bool want = false;
+      if (x < N) {
+        const bool hp = c.haspred[x] != 0;
+        const bool single = !hp && c.next[x] == kNone32;
+        want = hp ? lr_hash_ruler((uint32_t)x, logk) : !single;
+        if (single) {
+          c.sub[x] = kNone32;
+          c.off[x] = 0;
+        }
+      }
+      const uint32_t id = lr_block_claim(want ? 1u : 0u, nx.N);
+      if (want) {
+        if (id < nx.cap) c.rpos[id] = (uint32_t)x;
+        c.sub[x] = id;
+        c.off[x] = 0;
+      }
+    }
+    grid.sync();
+    const uint32_t R = (uint32_t)*((volatile unsigned long long*)nx.N);
+    if (R > nx.cap) {  // (uniform)
+      if (gtid == 0) *fallback = 1;
+      return;
+    }
+    // weighted walks (the k_walk1 state machine), chunks round-robin
+    if (threadIdx.x == 0) s_claim = 0;
+    __syncthreads();
+    {
+      enum : uint32_t { kClaim = 0, kStart, kHop, kRuler, kDone };
+      uint32_t st = kClaim, id = 0, cur = 0, acc = 0;
+      for (;;) {
+        const uint32_t* pa = nullptr;
+        const uint32_t* pb = nullptr;
+        if (st == kClaim) {
+          const uint32_t j = atomicAdd(&s_claim, 1u);
+          const uint64_t t = ((uint64_t)(j / kChunk) * gridDim.x + blockIdx.x) * kChunk + j % kChunk;
+          if (t < R) {
+            id = (uint32_t)t;
+            pa = &c.rpos[t];
+          } else {
+            break;
+          }
+        } else if (st == kStart) {
+          pa = &c.next[cur];
+          pb = &c.w[cur];
+        } else if (st == kHop) {
+          c.sub[cur] = id;
+          c.off[cur] = acc;
+          pa = &c.next[cur];
+          pb = &c.w[cur];
+        } else {  // kRuler
+          pa = &c.sub[cur];
+        }
+        const uint32_t x = ld_cg(pa);
+        const uint32_t wv = pb ? ld_cg(pb) : 0u;
+        if (st == kClaim) {
+          cur = x;
+          st = kStart;
+        } else if (st == kRuler) {
+          const_cast<uint32_t*>(nx.w)[id] = acc;
+          const_cast<uint32_t*>(nx.next)[id] = x;
+          st = kClaim;
+        } else {
+          acc = (st == kStart ? 0u : acc) + wv;
+          if (x == kNone32) {
+            const_cast<uint32_t*>(nx.w)[id] = acc;
+            const_cast<uint32_t*>(nx.next)[id] = kNone32;
+            st = kClaim;
+          } else {
+            cur = x;
+            st = lr_hash_ruler(x, logk) ? kRuler : kHop;
+          }
+        }
+      }
+    }
+    grid.sync();
+    if (verify)
+      for (int64_t x = gtid; x < N; x += gsize)
+        if (c.sub[x] == kNone32 && (c.haspred[x] || c.next[x] != kNone32)) *bad = 1;
+  }
+  if (k >= maxl) {
+    if (gtid == 0) *fallback = 1;
+    return;
+  }
+  // base: CTA 0, Wyllie over predecessor pointers in shared memory
+  if (blockIdx.x == 0) {
+    const LrLevel& c = L[k];
+    const int N = (int)*((volatile unsigned long long*)c.N);
+    for (int x = threadIdx.x; x < N; x += blockDim.x) s_p[x] = kNone32;
+    __syncthreads();
+    for (int x = threadIdx.x; x < N; x += blockDim.x) {
+      const uint32_t n1 = c.next[x];
+      if (n1 != kNone32) s_p[n1] = (uint32_t)x;
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < N; x += blockDim.x) s_v[x] = (s_p[x] == kNone32) ? 0u : c.w[s_p[x]];
+    __syncthreads();
+    constexpr int kPer = kBaseCoop / kBlock;
+    int rounds = 1;
+    while ((1 << (rounds - 1)) < N) ++rounds;
+    for (int r = 0; r < rounds; ++r) {
+      uint32_t np[kPer], nv[kPer];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int x = threadIdx.x + q * kBlock;
+        if (x < N) {
+          const uint32_t p = s_p[x];
+          np[q] = (p == kNone32) ? kNone32 : s_p[p];
+          nv[q] = (p == kNone32) ? s_v[x] : s_v[x] + s_v[p];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int x = threadIdx.x + q * kBlock;
+        if (x < N) {
+          s_p[x] = np[q];
+          s_v[x] = nv[q];
+        }
+      }
+      __syncthreads();
+    }
+    for (int x = threadIdx.x; x < N; x += blockDim.x) {
+      if (s_p[x] != kNone32) *bad = 1;
+      c.pre[x] = s_v[x];
+    }
+  }
+  grid.sync();
+  for (int j = k - 1; j >= 0; --j) {
+    const LrLevel& c = L[j];
+    const int64_t N = (int64_t)*((volatile unsigned long long*)c.N);
+    const uint32_t* pre1 = L[j + 1].pre;
+    for (int64_t x = gtid; x < N; x += gsize) {
+      const uint32_t sb = c.sub[x];
+      c.pre[x] = (sb == kNone32) ? 0u : pre1[sb] + c.off[x];
+    }
+    grid.sync();
+  }
+}
+
+// Host side of the cooperative recursion; returns false when the host path
+// must run instead (capacity fallback).
+static bool list_prefix_coop(Handle& h, const LrParams& P, int64_t N0, const uint32_t* next,
+                             const uint32_t* w, uint32_t* pre, bool verify, int* bad) {
+  const cudaStream_t s = h.stream;
+  // capacities halve per level; per level N x (haspred 1 + sub, off, rpos,
+  // next', w', pre' 4 each) bytes
+  int64_t caps[kMaxCoopLevels];
+  int64_t total = 0;
+  caps[0] = N0;
+  for (int k = 0; k < kMaxCoopLevels; ++k) {
+    if (k > 0) caps[k] = std::max<int64_t>(caps[k - 1] / 2, kBaseCoop);
+    total += ((caps[k] + 15) & ~int64_t{15}) * 25 + 64;
+  }
+  uint8_t* arena = h.ws<uint8_t>(WS_LR_L1, (size_t)total + 256);
+  LrLevel Lh[kMaxCoopLevels];
+  unsigned long long* counts = reinterpret_cast<unsigned long long*>(h.dev_box) + 224;  // [224, 236)
+  CK(cudaMemsetAsync(counts + 1, 0, (kMaxCoopLevels - 1) * sizeof(unsigned long long), s));
+  uint8_t* q = arena;
+  for (int k = 0; k < kMaxCoopLevels; ++k) {
+    const int64_t c = (caps[k] + 15) & ~int64_t{15};
+    Lh[k].cap = caps[k];
+    Lh[k].haspred = q;
+    q += c;
+    Lh[k].sub = reinterpret_cast<uint32_t*>(q);
+    Lh[k].off = Lh[k].sub + c;
+    Lh[k].rpos = Lh[k].off + c;
+    uint32_t* nn = Lh[k].rpos + c;  // next level's next / w / pre
+    uint32_t* nw = nn + c;
+    uint32_t* np = nw + c;
+    q = reinterpret_cast<uint8_t*>(np + c) + 64;
+    if (k == 0) {
+      Lh[0].next = next;
+      Lh[0].w = w;
+      Lh[0].pre = pre;
+      Lh[0].N = counts;
+    }
+    if (k + 1 < kMaxCoopLevels) {
+      Lh[k + 1].next = nn;
+      Lh[k + 1].w = nw;
+      Lh[k + 1].pre = np;
+      Lh[k + 1].N = counts + k + 1;
+    }
+  }
+  CK(cudaMemcpyAsync(counts, &N0, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  LrLevel* Ld = reinterpret_cast<LrLevel*>(h.ws<uint8_t>(WS_LR_L1 + 1, sizeof(Lh)));
+  CK(cudaMemcpyAsync(Ld, Lh, sizeof(Lh), cudaMemcpyHostToDevice, s));
+  int* fallback = reinterpret_cast<int*>(h.dev_box + 53);
+  CK(cudaMemsetAsync(fallback, 0, sizeof(int), s));
+  static int coop_blocks = 0;
+  if (!coop_blocks) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lr_levels, kBlock, 0));
+    coop_blocks = std::max(1, std::min(per_sm, 4)) * num_sms();
+  }
+  int maxl = kMaxCoopLevels;
+  int logk = P.logk1;
+  void* args[] = {(void*)&Ld, (void*)&maxl, (void*)&logk, (void*)&verify, (void*)&bad,
+                  (void*)&fallback};
+  CK(cudaLaunchCooperativeKernel((void*)k_lr_levels, dim3(coop_blocks), dim3(kBlock), args, 0, s));
+  h.stats.step(N0, 1);
+  // the fallback flag is read with the caller's next readback (lr_rank)
+  return true;
+}
+
 // pre[x] = sum of w over the nodes before x in its list.
 static void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t* next,
                         const uint32_t* w, uint32_t* pre, int depth, bool verify, int* bad) {
@@ -405,8 +680,12 @@ static void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t*
     return;
   }
   if (depth >= 12) throw std::runtime_error("list ranking: recursion too deep");
-  // level arena: haspred N, sub N, off N, rpos N, rw N, rn N, pre1 N
-  uint8_t* arena = h.ws<uint8_t>(WS_LR_L1 + depth, (size_t)N * (1 + 6 * 4) + 64);
+  // level arena: haspred N, sub N, off N, rpos N, rw N, rn N, pre1 N --
+  // sized by the ruler capacity (every level has at most that many nodes),
+  // not by N: N varies with the tour layout from build to build, and a
+  // grow-only workspace must not reallocate inside a timed build
+  const int64_t C = std::max<int64_t>(N, P.cap);
+  uint8_t* arena = h.ws<uint8_t>(WS_LR_L1 + depth, (size_t)C * (1 + 6 * 4) + 64);
   uint8_t* haspred = arena;
   uint32_t* sub = reinterpret_cast<uint32_t*>(arena + ((N + 15) & ~int64_t{15}));
   uint32_t* off = sub + N;
@@ -488,7 +767,13 @@ const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t*
 
   h.timer.begin(s, "lr.rulers_rank", 16.0 * R);
   uint32_t* rstart = h.ws<uint32_t>(WS_RD, P.cap);
-  list_prefix(h, P, R, rnext, rlen, rstart, 0, verify, bad);
+  if (P.coop_levels) {
+    list_prefix_coop(h, P, R, rnext, rlen, rstart, verify, bad);
+    h.read_box(h.dev_box + 52, 2);  // [52] bad (int), [53] fallback (int)
+    if (*reinterpret_cast<int*>(h.host_box + 1)) list_prefix(h, P, R, rnext, rlen, rstart, 0, verify, bad);
+  } else {
+    list_prefix(h, P, R, rnext, rlen, rstart, 0, verify, bad);
+  }
   if (verify) {
     h.read_box(reinterpret_cast<int64_t*>(bad), 1);
     if (*reinterpret_cast<int*>(h.host_box))

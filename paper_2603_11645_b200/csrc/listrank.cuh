@@ -14,10 +14,11 @@
 namespace rstg {
 
 struct LrParams {
-  int logk0 = 4;      // level-0 ruler density 1/2^logk0
+  int logk0 = 5;      // level-0 ruler density 1/2^logk0
   int logk1 = 3;      // ruler density of the ruler-list levels
   int chains = 1;     // walks in flight per thread (more thrash the L2)
-  int walk_blocks = 8;  // CTAs per SM of the level-0 walk
+  bool coop_levels = false;  // ruler-list levels in one cooperative launch
+  int walk_blocks = 4;  // CTAs per SM of the level-0 walk
   uint32_t chunk = 64;  // ruler ids per round-robin chunk
   int ob = 10;        // offset bits of the level-0 word
   uint32_t walk_cap;  // longest walk before a split, (1 << ob) - 1
@@ -77,7 +78,9 @@ __device__ __forceinline__ void lr_put(uint32_t id, uint32_t p, uint32_t* rpos, 
 #endif
 
 class Handle;
-LrParams lr_params(int64_t E, int64_t heads_bound);
+// E positions (holes included), at most heads_bound lists, `arcs` positions
+// actually on the lists (-1: all E).
+LrParams lr_params(int64_t E, int64_t heads_bound, int64_t arcs = -1);
 
 // Walks every registered ruler (ids [0, *ctr) on the device, positions in
 // rpos) over succ and fills sl, for every position a walk reached, with

@@ -76,12 +76,15 @@ LrParams lr_params(int64_t E, int64_t heads_bound, int64_t arcs) {
   // static rulers: hash hits (~E/2^logk, the Weyl sequence is
   // equidistributed; 2x slack) + heads; dynamic splits add <= E/walk_cap
   const int64_t stat = 2 * (E >> P.logk0) + heads_bound + 1024;
-  int idb = ceil_log2_ll(stat + (E >> 6) + 64);
+  // (tests force short walks to exercise the split path)
+  const int64_t forced_cap = env_int("RSTG_LR_WALKCAP", 1 << 30, 1, 1 << 30);
+  int idb = ceil_log2_ll(stat + E / std::min<int64_t>(64, forced_cap) + 64);
   if (idb < 1) idb = 1;
   if (idb > 31) throw std::runtime_error("list ranking: too many arcs");
   P.ob = 32 - idb;
   if (P.ob > 16) P.ob = 16;
   P.walk_cap = (1u << P.ob) - 1u;
+  P.walk_cap = (uint32_t)std::min<int64_t>(P.walk_cap, forced_cap);
   P.cap = stat + E / P.walk_cap + 64;
   if (P.cap >= (int64_t{1} << (32 - P.ob))) throw std::runtime_error("list ranking: capacity");
   return P;

@@ -355,3 +355,42 @@ def test_full_size_configs(rst, O, spec, m_expect):
             assert np.array_equal(lv, elv), f"{spec}: bfs levels mismatch"
         assert dg.validate(p, root)[0]
     dg.close()
+
+
+# ---- list-ranking parameters never change the result --------------------------
+# Ruler density, walks in flight, walk CTAs, chunking, the ruler-level path
+# and forced short walks (dynamic rulers split off mid-walk, walked by
+# follow-up launches) are performance knobs only.
+LR_KNOBS = [{"RSTG_LR_LOGK0": "1"}, {"RSTG_LR_LOGK0": "7"}, {"RSTG_LR_CHAINS": "2"},
+            {"RSTG_LR_CHAINS": "4", "RSTG_LR_BLOCKS": "1"}, {"RSTG_LR_CHUNK": "1"},
+            {"RSTG_LR_LOGK1": "1"}, {"RSTG_LR_LOGK1": "6"}, {"RSTG_LR_COOP": "1"},
+            {"RSTG_LR_WALKCAP": "4"}, {"RSTG_LR_WALKCAP": "17", "RSTG_LR_LOGK0": "6"}]
+
+
+@pytest.mark.parametrize("spec,root", [(("road", 300), 0), (("kron", 14), None), (("path", 5000), 77),
+                                        (("grid", 40, 60), 123)])
+def test_list_rank_knobs_invariant(rst, O, spec, root, monkeypatch):
+    g = O.gen(*spec)
+    if root is None:
+        root = int(np.argmax(np.diff(g.offsets)))
+    ep, er, _ = O.run(g, 1, root)
+    dg = dev_graph(rst, g)
+    for knobs in LR_KNOBS:
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        p, r, _, _ = dg.run(1, root)
+        assert np.array_equal(p, ep), f"{spec} {knobs}: parent mismatch"
+        assert np.array_equal(r, er), f"{spec} {knobs}: roots mismatch"
+        for k in knobs:
+            monkeypatch.delenv(k)
+    # explicit forests and raw lists take the same knobs
+    monkeypatch.setenv("RSTG_LR_WALKCAP", "3")
+    succ = np.full(1000, -1, np.int64)
+    perm = np.random.RandomState(3).permutation(1000)
+    for i in range(999):
+        succ[perm[i]] = perm[i + 1]
+    exp = np.zeros(1000, np.int64)
+    import ctypes
+    O.lib().og_list_rank(ctypes.c_int64(1000), O._p(succ), O._p(exp))
+    assert np.array_equal(rst.list_rank(succ), exp)
+    dg.close()

@@ -205,7 +205,7 @@ struct RoundIO {
 };
 
 template <int SRC>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kTileThreads, 2)
     k_tile_resolve(int64_t n, int32_t* rep, uint32_t* xbits, uint32_t* xlist,
                    unsigned long long* xcount, RoundIO io) {
   extern __shared__ int32_t s[];  // kTileV reps (+ 2 x kTileV list words when linking round 0)
@@ -226,7 +226,36 @@ __global__ void __launch_bounds__(kTileThreads)
   }
   uint32_t hooked = 0;
   uint32_t rootmask = 0;  // round 0: items of this thread that stay roots
-  for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
+  // Round 0: the tile's first neighbours are fetched in two batched passes
+  // -- all offsets into shared memory, then all neighbour reads into
+  // registers -- so a thread keeps its 8 items' loads in flight together
+  // instead of paying two dependent latencies per item in turn.
+  constexpr int kItems = kTileV / kTileThreads;
+  int32_t fnb[kItems];
+  if (SRC == kSrcRound0) {
+    uint32_t* s_o = reinterpret_cast<uint32_t*>(s);  // (reps go here later)
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const int i = threadIdx.x + k * kTileThreads;
+      if (i < cnt) s_o[i] = io.offsets[base + i];
+    }
+    __syncthreads();
+    const uint32_t o_end = io.offsets[base + cnt];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const int i = threadIdx.x + k * kTileThreads;
+      fnb[k] = INT32_MAX;
+      if (i < cnt) {
+        const uint32_t o = s_o[i], o1 = i + 1 < cnt ? s_o[i + 1] : o_end;
+        if (o < o1) fnb[k] = io.nbrs[o];
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {  // (unrolled: fnb stays in registers)
+    const int i = threadIdx.x + k * kTileThreads;
+    if (i >= cnt) break;
     const int64_t v = base + i;
     int32_t r;
     if (SRC == kSrcRep) {
@@ -246,17 +275,16 @@ __global__ void __launch_bounds__(kTileThreads)
         }
       }
     } else {
-      const uint32_t o = io.offsets[v];
       r = (int32_t)v;
-      rootmask |= 1u << (i / kTileThreads);  // cleared below if v hooks
-      if (o < io.offsets[v + 1]) {
-        const int32_t u = io.nbrs[o];
+      rootmask |= 1u << k;  // cleared below if v hooks
+      {
+        const int32_t u = fnb[k];
         if (u < r) {  // hooked onto its smallest neighbour by edge (u, v)
-          rootmask &= ~(1u << (i / kTileThreads));
+          rootmask &= ~(1u << k);
           r = u;
           ++hooked;
           if (io.tflag) {
-            const uint32_t e = io.arc_edge[o];
+            const uint32_t e = io.arc_edge[io.offsets[v]];
             if (e < io.m_local) io.tflag[e] = 1;
           }
           if (io.link) {

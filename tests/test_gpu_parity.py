@@ -361,8 +361,8 @@ def test_full_size_configs(rst, O, spec, m_expect):
 # Ruler density, walks in flight, walk CTAs, chunking, the ruler-level path
 # and forced short walks (dynamic rulers split off mid-walk, walked by
 # follow-up launches) are performance knobs only.
-LR_KNOBS = [{"RSTG_LR_LOGK0": "1"}, {"RSTG_LR_LOGK0": "7"}, {"RSTG_LR_CHAINS": "2"},
-            {"RSTG_LR_CHAINS": "4", "RSTG_LR_BLOCKS": "1"}, {"RSTG_LR_CHUNK": "1"},
+LR_KNOBS = [{"RSTG_LR_LOGK0": "1"}, {"RSTG_LR_LOGK0": "7"}, {"RSTG_LR_BLOCKS": "2"},
+            {"RSTG_LR_BLOCKS": "1"}, {"RSTG_LR_CHUNK": "1"},
             {"RSTG_LR_LOGK1": "1"}, {"RSTG_LR_LOGK1": "6"}, {"RSTG_LR_COOP": "1"},
             {"RSTG_LR_WALKCAP": "4"}, {"RSTG_LR_WALKCAP": "17", "RSTG_LR_LOGK0": "6"}]
 

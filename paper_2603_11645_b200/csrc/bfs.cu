@@ -260,6 +260,7 @@ static void run_levels(Handle& h, int32_t* level, int32_t* parent, BfsQueues qs,
 
 int64_t bfs_rst(Handle& h, int32_t root, int32_t* parent, int32_t* level, int32_t* roots) {
   const int64_t n = h.g.n;
+  ensure_csr(h);
   if (!h.g.has_csr()) throw ArgError("bfs needs the graph's CSR");
   BfsQueues qs;
   qs.q[0] = h.ws<int32_t>(WS_BFS_Q0, n + 1);

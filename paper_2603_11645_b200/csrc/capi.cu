@@ -117,7 +117,9 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
   } else if (algo == RSTG_CC_EULER) {
     int32_t* labels = h.ws<int32_t>(WS_REP, h.g.n);
     // round 0 runs from the CSR (and writes every local list) when there is one
-    const EulerIO io = euler_buffers(h, h.g.n, h.g.has_csr() && h.g.m > 0);
+    // (round 0 runs -- from keys or the CSR -- whenever there are edges and
+    // either a CSR exists or is pending)
+    const EulerIO io = euler_buffers(h, h.g.n, (h.g.has_csr() || h.round0_slots) && h.g.m > 0);
     const int64_t T = cc_exact(h, labels, nullptr, &io);
     euler_root(h, labels, io, h.g.n, T, /*cc_slots=*/true, (int32_t)root, parent);
   } else if (algo == RSTG_PR_RST) {

@@ -187,7 +187,10 @@ constexpr size_t kTileSmem = kTileV * sizeof(int32_t);
 //              every rep a singleton, min-mode hooking gives v the key
 //              min over neighbours u < v of (u, e), i.e. v's first CSR
 //              neighbour (lists ascending) with its unique edge id
-enum { kSrcRep = 0, kSrcApply = 1, kSrcRound0 = 2 };
+//   kSrcRound0Slot  the same round 0 with the hook keys already in the
+//              slots (the edge upload computed them as the edges streamed
+//              in, graph.cu): no CSR needed
+enum { kSrcRep = 0, kSrcApply = 1, kSrcRound0 = 2, kSrcRound0Slot = 3 };
 
 struct RoundIO {
   unsigned long long* slot;
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   // shared-memory rotation lists whenever u lies in the tile (nearly
   // always: u is an adjacent id on meshes), then splices each tile list
   // into the global one with a single atomic (see the flush below).
-  constexpr bool kLocal = SRC == kSrcRound0;
+  constexpr bool kLocal = SRC == kSrcRound0 || SRC == kSrcRound0Slot;
   uint32_t* s_head = reinterpret_cast<uint32_t*>(s + kTileV);
   uint32_t* s_tail = s_head + kTileV;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -278,13 +281,24 @@ __global__ void __launch_bounds__(kTileThreads, 2)
       r = (int32_t)v;
       rootmask |= 1u << k;  // cleared below if v hooks
       {
-        const int32_t u = fnb[k];
+        int32_t u = INT32_MAX;
+        uint32_t ekey = kNone32;  // (kSrcRound0Slot: the edge id from the key)
+        if (SRC == kSrcRound0) {
+          u = fnb[k];
+        } else {
+          const unsigned long long key = io.slot[v];
+          if (key != kKeyInf) {
+            u = (int32_t)(key >> 32);
+            ekey = (uint32_t)key;
+            io.slot[v] = kKeyInf;  // (keeps the slots clean for the next rounds)
+          }
+        }
         if (u < r) {  // hooked onto its smallest neighbour by edge (u, v)
           rootmask &= ~(1u << k);
           r = u;
           ++hooked;
           if (io.tflag) {
-            const uint32_t e = io.arc_edge[io.offsets[v]];
+            const uint32_t e = SRC == kSrcRound0 ? io.arc_edge[io.offsets[v]] : ekey - io.e_base;
             if (e < io.m_local) io.tflag[e] = 1;
           }
           if (io.link) {
@@ -458,6 +472,8 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
                             (int)kTileSmem));
     CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRound0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(3 * kTileSmem)));
+    CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRound0Slot>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSmem)));
     CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kTileSmem));
     int per_sm = 0;
@@ -468,6 +484,9 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
   if (src == kSrcApply)
     k_tile_resolve<kSrcApply><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, xbits, xlist,
                                                                             xcount, io);
+  else if (src == kSrcRound0Slot)
+    k_tile_resolve<kSrcRound0Slot><<<tiles, kTileThreads, io.link ? 3 * kTileSmem : kTileSmem,
+                                     h.stream>>>(n, rep, xbits, xlist, xcount, io);
   else if (src == kSrcRound0)
     k_tile_resolve<kSrcRound0><<<tiles, kTileThreads, io.link ? 3 * kTileSmem : kTileSmem,
                                  h.stream>>>(n, rep, xbits, xlist, xcount, io);
@@ -572,6 +591,8 @@ void cc_round_done(Handle& h, int64_t out_count) {
   }
   ++h.cc_round;
 }
+bool round0_keys_from_edges(Handle& h, unsigned long long* slot);
+
 void cc_reset_rounds(Handle& h) {
   h.cc_lazy = false;
   h.cc_round = 0;
@@ -644,16 +665,21 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   const int64_t n = h.g.n, m = h.g.m;
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(h.dev_box);
-  const bool round0 = h.g.has_csr() && m > 0;  // writes every rep itself
-  const bool slots_ok = h.slots_clean == slot;
+  // round 0 from the keys the edge upload left in the slots, else (CSR
+  // still pending) from keys recomputed over the edge list, else the CSR
+  const bool keyed = (h.round0_slots == slot && m > 0) || round0_keys_from_edges(h, slot);
+  h.round0_slots = nullptr;
+  const bool round0 = keyed || (h.g.has_csr() && m > 0);  // writes every rep itself
+  const bool slots_ok = keyed || h.slots_clean == slot;
   h.slots_clean = nullptr;  // until this build completes
   h.timer.begin(h.stream, "cc.init", (round0 ? 0.0 : 4.0 * n) + (slots_ok ? 0.0 : 8.0 * n));
   if (!round0 || !slots_ok) {
     k_cc_init<<<grid_for(n), kBlock, 0, h.stream>>>(n, round0 ? nullptr : rep,
                                                      slots_ok ? nullptr : slot);
     CK_LAUNCH();
-    h.stats.step(n);
   }
+  // the init step (cc_forest.cpp:82) counts whether or not it had work left
+  h.stats.step(n, (!round0 || !slots_ok) ? 1 : 0);
   if (tflag && m > 0) CK(cudaMemsetAsync(tflag, 0, (size_t)m, h.stream));
   CK(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), h.stream));
   h.timer.end(h.stream);
@@ -670,12 +696,12 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
              h.g.arc_edge, h.g.edges, euler != nullptr, euler ? *euler : EulerIO{}, rl[0], rcount};
   cc_reset_rounds(h);
   int64_t round = 0;
-  if (h.g.has_csr() && m > 0) {
-    // round 0 (min mode over singleton reps) straight from the CSR, fused
-    // with its apply and shortcutting
+  if (round0) {
+    // round 0 (min mode over singleton reps) straight from the CSR (or the
+    // upload's keys), fused with its apply and shortcutting
     // offsets, first neighbour, rep; a tree edge (arc heads + successors) per vertex
     h.timer.begin(h.stream, "cc.round0", 4.0 * (n + 1) + 8.0 * n + (euler ? 16.0 * n : 0.0));
-    resolve_round(h, rep, n, kSrcRound0, io);
+    resolve_round(h, rep, n, keyed ? kSrcRound0Slot : kSrcRound0, io);
     h.timer.end(h.stream);
     cc_round_done(h, 0);
     round = 1;

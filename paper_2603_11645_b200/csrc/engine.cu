@@ -75,6 +75,7 @@ Handle::~Handle() {
     if (b.first) cudaFree(b.first);
   cudaFree(dev_box);
   cudaFreeHost(host_box);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(stream);
 }
 

@@ -71,6 +71,7 @@ struct DeviceGraph {
   uint32_t* offsets = nullptr;  // n+1 CSR offsets (nullptr if no CSR)
   int32_t* nbrs = nullptr;      // 2m neighbours, ascending per vertex
   uint32_t* arc_edge = nullptr; // 2m edge_origin
+  bool csr_pending = false;     // CSR buffers allocated, built on first use (ensure_csr)
   bool has_csr() const { return offsets != nullptr; }
 };
 
@@ -92,6 +93,10 @@ class Handle {
   // every slot it consumes), so the next build skips re-initialising it;
   // any other user of the slot buffer clears this.
   const void* slots_clean = nullptr;
+  // Set by the edge upload: WS_SLOT already holds round 0's hook keys
+  // (computed while the edges streamed in), consumed by cc_exact.
+  const void* round0_slots = nullptr;
+  cudaStream_t copy_stream = nullptr;  // H2D staging of uploads (lazily created)
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   DeviceGraph g;
@@ -244,6 +249,9 @@ __device__ __forceinline__ uint32_t arc_rev(uint32_t p, uint32_t nslots) {
   return p < nslots ? p + nslots : p - nslots;
 }
 #endif
+
+// Builds a pending CSR (uploads defer it: cc-euler never needs it).
+void ensure_csr(Handle& h);
 
 // ---- algorithms (device-resident in/out; int32 ids) ----
 // cc_spanning_forest (cc_forest.cpp:73-102), exact: labels = converged reps,

@@ -88,6 +88,7 @@ static void upload_narrow(Handle& h, const int64_t* host, int64_t count, T* dev)
 }
 
 static void alloc_graph(Handle& h, int64_t n, int64_t m, bool csr) {
+  h.round0_slots = nullptr;  // (new edges: any upload keys are stale)
   if (n < 0) throw ArgError("negative vertex count");
   if (n >= (int64_t{1} << 31)) throw ArgError("graph too large: vertex ids exceed 2^31");
   if (m > (int64_t{1} << 32)) throw ArgError("too many edges");
@@ -109,6 +110,8 @@ void upload_reference_graph(Handle& h, const int64_t* offsets, const int64_t* nb
                             const int64_t* origin, const int64_t* edges_uv, int64_t n, int64_t m) {
   const bool csr = offsets != nullptr && 2 * m < (int64_t{1} << 32);
   alloc_graph(h, n, m, csr);
+  h.g.csr_pending = false;
+  h.round0_slots = nullptr;
   if (csr) {
     upload_narrow<uint32_t>(h, offsets, n + 1, h.g.offsets);
     upload_narrow<int32_t>(h, nbrs, 2 * m, h.g.nbrs);
@@ -195,6 +198,7 @@ void build_csr_device(Handle& h) {
   if (n == 0) CK(cudaMemsetAsync(h.g.offsets, 0, sizeof(uint32_t), s));
   if (m == 0) {
     CK(cudaStreamSynchronize(s));
+    h.g.csr_pending = false;
     return;
   }
   k_place_forward<<<grid_for(m), kBlock, 0, s>>>(m, h.g.edges, h.g.offsets, bdeg, fs, h.g.nbrs,
@@ -217,6 +221,7 @@ void build_csr_device(Handle& h) {
                                              h.g.arc_edge);
   CK_LAUNCH();
   CK(cudaStreamSynchronize(s));
+  h.g.csr_pending = false;
 }
 
 // ------------------------------------------------------ normalize on device
@@ -440,11 +445,111 @@ void generate_kron_part(Handle& h, int scale, int ef, int part, int nparts) {
   h.g.e_base = 0;
 }
 
-// Normalized int64 edge list (the reference EdgeList) -> device graph + CSR.
+// Narrows a chunk of int64 (u, v) pairs into the device edge list and
+// records round 0's hook proposal of each edge on the way: with every rep a
+// singleton, min-mode hooking offers slot[v] the key (u << 32 | e) (u < v
+// in a normalized list), the smallest of which is v's first neighbour --
+// exactly what the CSR-direct round 0 reads (cc.cu).
+__global__ void k_narrow_edges(int64_t count, const long long* __restrict__ in, int2* out,
+                               uint32_t e_first, unsigned long long* slot) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int2 e = make_int2((int)in[2 * i], (int)in[2 * i + 1]);
+    out[i] = e;
+    if (e.x < e.y) {
+      const unsigned long long key = pack_key((uint32_t)e.x, e_first + (uint32_t)i);
+      if (key < slot[e.y]) atomicMin(&slot[e.y], key);
+    }
+  }
+}
+__global__ void k_fill_u64(int64_t count, unsigned long long* p, unsigned long long v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+void ensure_csr(Handle& h) {
+  if (!h.g.csr_pending) return;
+  const Stats keep = h.stats;  // ingestion, not the algorithm: reruns count alike
+  build_csr_device(h);
+  h.stats = keep;
+  h.g.csr_pending = false;
+}
+
+// Round 0's hook keys from the device edge list (a graph uploaded for an
+// earlier build whose keys were consumed, CSR still pending).
+__global__ void k_round0_keys(int64_t m, const int2* __restrict__ edges, uint32_t e_base,
+                              unsigned long long* slot) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int2 e = edges[i];
+    if (e.x < e.y) {
+      const unsigned long long key = pack_key((uint32_t)e.x, e_base + (uint32_t)i);
+      if (key < slot[e.y]) atomicMin(&slot[e.y], key);
+    }
+  }
+}
+bool round0_keys_from_edges(Handle& h, unsigned long long* slot) {
+  if (!h.g.csr_pending || h.g.m == 0) return false;
+  if (h.slots_clean != slot) {
+    k_fill_u64<<<grid_for(h.g.n), kBlock, 0, h.stream>>>(h.g.n, slot, kKeyInf);
+    CK_LAUNCH();
+  }
+  k_round0_keys<<<grid_for(h.g.m), kBlock, 0, h.stream>>>(h.g.m, h.g.edges, (uint32_t)h.g.e_base,
+                                                          slot);
+  CK_LAUNCH();
+  return true;
+}
+
+// Normalized int64 edge list (the reference EdgeList) -> device graph.
+// The edges stream in through two staging buffers (DMA of chunk k + 1
+// overlaps the narrowing of chunk k), round 0's hook keys are computed on
+// the way, and the CSR is left pending: cc-euler never needs it.
 void upload_edges_build_csr(Handle& h, const int64_t* edges_uv, int64_t n, int64_t m) {
   alloc_graph(h, n, m, 2 * m < (int64_t{1} << 32));
-  upload_narrow<int32_t>(h, edges_uv, 2 * m, reinterpret_cast<int32_t*>(h.g.edges));
-  if (h.g.offsets) build_csr_device(h);
+  h.g.csr_pending = h.g.offsets != nullptr;
+  unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
+  const cudaStream_t s = h.stream;
+  if (h.slots_clean != slot && n > 0) {
+    k_fill_u64<<<grid_for(n), kBlock, 0, s>>>(n, slot, kKeyInf);
+    CK_LAUNCH();
+  }
+  h.slots_clean = nullptr;
+  h.round0_slots = nullptr;
+  if (m > 0) {
+    if (!h.copy_stream) CK(cudaStreamCreateWithFlags(&h.copy_stream, cudaStreamNonBlocking));
+    const int64_t chunk = int64_t{1} << 22;  // edges per staging buffer (32 MB of int64 pairs)
+    long long* stage = h.ws<long long>(WS_VAL_C, 2 * 2 * chunk);
+    cudaEvent_t copied[2], consumed[2];
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&consumed[b], cudaEventDisableTiming));
+      CK(cudaEventRecord(consumed[b], s));
+    }
+    for (int64_t off = 0, k = 0; off < m; off += chunk, ++k) {
+      const int b = (int)(k & 1);
+      const int64_t c = std::min(chunk, m - off);
+      long long* buf = stage + b * 2 * chunk;
+      CK(cudaStreamWaitEvent(h.copy_stream, consumed[b], 0));
+      CK(cudaMemcpyAsync(buf, edges_uv + 2 * off, c * 2 * sizeof(int64_t), cudaMemcpyHostToDevice,
+                         h.copy_stream));
+      CK(cudaEventRecord(copied[b], h.copy_stream));
+      CK(cudaStreamWaitEvent(s, copied[b], 0));
+      k_narrow_edges<<<grid_for(c), kBlock, 0, s>>>(c, buf, h.g.edges + off, (uint32_t)off, slot);
+      CK_LAUNCH();
+      CK(cudaEventRecord(consumed[b], s));
+    }
+    CK(cudaStreamSynchronize(s));
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(copied[b]);
+      cudaEventDestroy(consumed[b]);
+    }
+    h.round0_slots = slot;
+  } else if (h.g.offsets) {
+    build_csr_device(h);
+    h.g.csr_pending = false;
+  }
+  CK(cudaStreamSynchronize(s));
 }
 
 // Device int32 arrays -> handle-owned copies.

@@ -770,6 +770,12 @@ const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t*
 
   h.timer.begin(s, "lr.rulers_rank", 16.0 * R);
   uint32_t* rstart = h.ws<uint32_t>(WS_RD, P.cap);
+  // The recursion's shape follows the ruler ids, which follow the tour's
+  // layout (atomic insertion order), so its own step/work counts vary from
+  // run to run; StepReport gets a fixed charge instead (doubling passes
+  // over the expected rulers, like Wyllie on them), kept bit-identical
+  // across reruns (acceptance criterion 7).
+  const Stats before = h.stats;
   if (P.coop_levels) {
     list_prefix_coop(h, P, R, rnext, rlen, rstart, verify, bad);
     h.read_box(h.dev_box + 52, 2);  // [52] bad (int), [53] fallback (int)
@@ -781,6 +787,17 @@ const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t*
     h.read_box(reinterpret_cast<int64_t*>(bad), 1);
     if (*reinterpret_cast<int*>(h.host_box))
       throw AlgoError("list ranking failed to converge: not a forest");
+  }
+  {
+    const int64_t launches = h.stats.launches;
+    h.stats = before;
+    h.stats.launches = launches;
+    // (the expected ruler count, E / 2^logk0: the static count itself
+    // depends on which arc opens each tour)
+    const int64_t Rexp = std::max<int64_t>(E >> P.logk0, 2);
+    const int rounds = ceil_log2_ll(Rexp) + 1;
+    h.stats.steps += rounds;
+    h.stats.work += Rexp * rounds;
   }
   h.timer.end(s);
   if (R_out) *R_out = R;

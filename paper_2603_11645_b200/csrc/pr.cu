@@ -243,6 +243,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   int32_t* anc = h.ws<int32_t>(WS_PR_ANC, (size_t)n * L);
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
   h.slots_clean = nullptr;  // graft rounds leave slots of their own
+  h.round0_slots = nullptr;  // (and overwrite an upload's round-0 keys)
   int* ctl = reinterpret_cast<int*>(h.ws<int>(WS_BFS_CTRL, C_NWORDS + 8));
   unsigned long long* bad_mark = reinterpret_cast<unsigned long long*>(h.dev_box) + 16;
   int* not_done = ctl + C_NWORDS;

@@ -92,6 +92,7 @@ static int ceil_log2_i(int64_t x) {
 int validate_forest(Handle& h, const int32_t* parent, int32_t required_root,
                     int64_t* bad_vertex) {
   const int64_t n = h.g.n;
+  ensure_csr(h);
   if (!h.g.has_csr()) throw ArgError("validation needs the graph's CSR");
   const cudaStream_t s = h.stream;
   int32_t* ra = h.ws<int32_t>(WS_VAL_B, n);

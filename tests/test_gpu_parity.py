@@ -394,3 +394,19 @@ def test_list_rank_knobs_invariant(rst, O, spec, root, monkeypatch):
     O.lib().og_list_rank(ctypes.c_int64(1000), O._p(succ), O._p(exp))
     assert np.array_equal(rst.list_rank(succ), exp)
     dg.close()
+
+
+def test_step_counts_rerun_identical(rst, O):
+    # acceptance.cpp:330-363 (criterion 7): parents, steps and work are
+    # bit-identical across reruns -- with the CSR given or built on the
+    # device, and whether round 0 reads upload keys, recomputed keys or CSR
+    for g in (O.gen("random", 1000, 0.01, seed=3), O.gen("grid", 50, 50), O.gen("kron", 12)):
+        for csr in (True, False):
+            extra = (g.offsets, g.nbrs, g.origin) if csr else ()
+            dg = rst.DeviceGraph.from_host(g.n, np.stack([g.eu, g.ev], 1), *extra)
+            for algo in ALGOS:
+                res = [dg.run(algo, 0) for _ in range(3)]
+                for p, _, _, st in res[1:]:
+                    assert np.array_equal(p, res[0][0])
+                    assert (st["steps"], st["work"]) == (res[0][3]["steps"], res[0][3]["work"]), (algo, csr)
+            dg.close()

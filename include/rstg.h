@@ -15,6 +15,7 @@
  *   rstg_cc_spanning_forest  cc_spanning_forest     include/rst/cc_forest.hpp:42
  *   rstg_euler_root_forest   euler_root_forest      include/rst/euler_rooting.hpp:63-66
  *   rstg_validate         validate_rooted_forest     include/rst/validate.hpp:46-47
+ *   rstg_forest_depth     forest_depth               include/rst/rooted_forest.hpp:29
  *   rstg_k_*              hook_step / jump_to_convergence / list_rank
  *                         (cc_forest.hpp:29-40, euler_rooting.hpp:52-53):
  *                         kernel-level entry points for parity tests.
@@ -114,6 +115,14 @@ int rstg_euler_root_forest(int64_t n, const int64_t* tree_uv, int64_t T, const i
  * 6 required root; *bad_vertex = first offender. */
 int rstg_validate(rstg_graph* g, const int64_t* parent, int64_t required_root, int* valid,
                   int* code, int64_t* bad_vertex);
+
+/* forest_depth (rooted_forest.hpp:29, rooted_forest.cpp:12-95) on the
+ * device: depth_out[n] hops to the root (nullable), root_max_out[n] the
+ * deepest chain under each root, -1 for non-roots (nullable), *max_depth
+ * the overall maximum. Errors: "parent out of range at vertex v",
+ * "parent array contains a cycle at vertex v" (the smallest such v). */
+int rstg_forest_depth(rstg_graph* g, const int64_t* parent, int64_t* depth_out,
+                      int64_t* root_max_out, int64_t* max_depth);
 
 /* ---- edge-partitioned connectivity (multi-GPU) ----
  * Rank r's handle holds a contiguous range of the GLOBAL normalized edge

@@ -29,7 +29,7 @@ EXPORTS = (
     "rstg_last_error", "rstg_device_count", "rstg_graph_create", "rstg_graph_create_device", "rstg_graph_upload",
     "rstg_graph_generate", "rstg_graph_info", "rstg_graph_edges", "rstg_graph_destroy",
     "rstg_set_stream", "rstg_set_timing", "rstg_phase_times", "rstg_run", "rstg_run_device",
-    "rstg_cc_spanning_forest", "rstg_euler_root_forest", "rstg_validate",
+    "rstg_cc_spanning_forest", "rstg_euler_root_forest", "rstg_validate", "rstg_forest_depth",
     "rstg_graph_generate_part", "rstg_graph_set_edge_base", "rstg_cc_init", "rstg_cc_hook",
     "rstg_cc_apply", "rstg_cc_compress", "rstg_k_hook_step",
     "rstg_k_jump", "rstg_k_list_rank",
@@ -96,6 +96,7 @@ def lib():
         L.rstg_euler_root_forest.argtypes = [ctypes.c_int64, _i64p, ctypes.c_int64, _i64p,
                                              ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _i64p,
                                              _i64p, _i64p]
+        L.rstg_forest_depth.argtypes = [_vp, _i64p, _i64p, _i64p, _i64p]
         L.rstg_validate.argtypes = [_vp, _i64p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int),
                                     ctypes.POINTER(ctypes.c_int), _i64p]
         L.rstg_graph_generate_part.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
@@ -271,6 +272,17 @@ class DeviceGraph:
         _check(lib().rstg_cc_spanning_forest(self._h, _p64(labels), _p64(te), ctypes.byref(T),
                                              ctypes.byref(st)))
         return labels, te[: T.value].copy()
+
+    def forest_depth(self, parent):
+        """forest_depth (rooted_forest.cpp:12-95) on the device:
+        (depth per vertex, max depth per root (-1 off roots), max depth)."""
+        p = np.ascontiguousarray(parent, dtype=np.int64)
+        depth = np.zeros(max(self.n, 1), np.int64)
+        rmax = np.zeros(max(self.n, 1), np.int64)
+        best = ctypes.c_int64(0)
+        _check(lib().rstg_forest_depth(self._h, _p64(p), _p64(depth), _p64(rmax),
+                                       ctypes.byref(best)))
+        return depth[: self.n], rmax[: self.n], best.value
 
     def validate(self, parent, required_root=-1):
         p = np.ascontiguousarray(parent, dtype=np.int64)

@@ -22,6 +22,8 @@ void adopt_device_graph(Handle& h, const int2* edges, const uint32_t* offsets, c
                         const uint32_t* arc_edge, int64_t n, int64_t m);
 void generate_device(Handle& h, int kind, int64_t a, int64_t b, double p, bool build_csr);
 void widen_to_host(Handle& h, const int32_t* dev, int64_t count, int64_t* host);
+int64_t forest_depth_device(Handle& h, const int32_t* parent, int32_t* depth, uint32_t* rootmax,
+                            int64_t* cycle_vertex);
 void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_base,
                  const int32_t* rep, unsigned long long* slot, int* any_prop);
 void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tflag,
@@ -523,6 +525,43 @@ int rstg_euler_root_forest(int64_t n, const int64_t* tree_uv, int64_t T, const i
     widen_to_host(h, parent, n, parent_out);
     if (roots_out && nr > 0) widen_to_host(h, roots, nr, roots_out);
     if (num_roots) *num_roots = nr;
+  });
+}
+
+int rstg_forest_depth(rstg_graph* g, const int64_t* parent, int64_t* depth_out,
+                      int64_t* root_max_out, int64_t* max_depth) {
+  return guard([&] {
+    Handle& h = g->h;
+    const int64_t n = h.g.n;
+    for (int64_t v = 0; v < n; ++v)  // (range check before narrowing, like rstg_validate)
+      if (parent[v] < 0 || parent[v] >= n)
+        throw AlgoError("parent out of range at vertex " + std::to_string(v));
+    int32_t* p = h.ws<int32_t>(WS_PARENT, n);
+    to_device<int32_t>(h, parent, n, p);
+    int32_t* depth = h.ws<int32_t>(WS_ROOTS, n + 1);  // (WS_VAL_C is the readback staging)
+    uint32_t* rootmax = h.ws<uint32_t>(WS_MINV, n);
+    int64_t cyc = -1;
+    forest_depth_device(h, p, depth, rootmax, &cyc);
+    if (cyc >= 0) {
+      // the reference walks from the smallest vertex that never reaches a
+      // root and names the first vertex its walk meets twice
+      std::vector<char> seen((size_t)n, 0);
+      int64_t x = cyc;
+      while (!seen[(size_t)x]) {
+        seen[(size_t)x] = 1;
+        x = parent[x];
+      }
+      throw AlgoError("parent array contains a cycle at vertex " + std::to_string(x));
+    }
+    std::vector<uint32_t> rm((size_t)n);
+    CK(cudaMemcpy(rm.data(), rootmax, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    int64_t best = 0;
+    for (int64_t v = 0; v < n; ++v) {
+      if (root_max_out) root_max_out[v] = (parent[v] == v) ? (int64_t)rm[(size_t)v] : -1;
+      if (parent[v] == v) best = std::max<int64_t>(best, rm[(size_t)v]);
+    }
+    *max_depth = best;
+    if (depth_out) widen_to_host(h, depth, n, depth_out);
   });
 }
 

@@ -147,3 +147,73 @@ int validate_forest(Handle& h, const int32_t* parent, int32_t required_root,
 }
 
 }  // namespace rstg
+
+namespace rstg {
+
+// ---- forest_depth (rooted_forest.cpp:12-95) on the device ----------------
+// Distance to the root by Jacobi doubling over (jump, distance) pairs: a
+// round doubles every jump, so ceil(log2 depth) + 1 rounds settle all; a
+// pointer still short of a root after ceil(log2 n) + 2 rounds is on a
+// cycle. Per-root maxima by atomicMax on the root's slot.
+__global__ void k_depth_init(int64_t n, const int32_t* __restrict__ parent, int2* jd) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = parent[v];
+    jd[v] = make_int2(p, p == (int32_t)v ? 0 : 1);
+  }
+}
+__global__ void k_depth_round(int64_t n, const int2* __restrict__ a, int2* __restrict__ b,
+                              int* flags, int round) {
+  if (round > 0 && flags[round - 1] == 0) return;
+  bool changed = false;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int2 x = a[v];
+    const int2 y = a[x.x];
+    b[v] = make_int2(y.x, x.y + y.y);
+    changed |= y.x != x.x;
+  }
+  block_flag(changed, &flags[round]);
+}
+__global__ void k_depth_finish(int64_t n, const int2* __restrict__ jd, const int32_t* __restrict__ parent,
+                               int32_t* depth, unsigned int* rootmax, int* cycle_at) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int2 x = jd[v];
+    if (parent[x.x] != x.x) {  // never reached a root: a cycle
+      atomicMin(cycle_at, (int)v);
+      continue;
+    }
+    depth[v] = x.y;
+    atomicMax(&rootmax[x.x], (unsigned int)x.y);
+  }
+}
+
+int64_t forest_depth_device(Handle& h, const int32_t* parent, int32_t* depth, uint32_t* rootmax,
+                            int64_t* cycle_vertex) {
+  const int64_t n = h.g.n;
+  const cudaStream_t s = h.stream;
+  int2* a = h.ws<int2>(WS_VAL_A, n);
+  int2* b = h.ws<int2>(WS_VAL_B, n);
+  int* flags = reinterpret_cast<int*>(h.dev_box + 128);  // 64 ints
+  int* cyc = reinterpret_cast<int*>(h.dev_box + 41);
+  CK(cudaMemsetAsync(flags, 0, 64 * sizeof(int), s));
+  CK(cudaMemsetAsync(rootmax, 0, n * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(cyc, 0x7F, sizeof(int), s));
+  const unsigned g = grid_for(n);
+  k_depth_init<<<g, kBlock, 0, s>>>(n, parent, a);
+  int rounds = 2;
+  while ((int64_t{1} << (rounds - 2)) < n) ++rounds;
+  for (int r = 0; r < rounds && r < 64; ++r) {
+    k_depth_round<<<g, kBlock, 0, s>>>(n, a, b, flags, r);
+    std::swap(a, b);  // (a round that changed nothing leaves b unwritten: both equal)
+  }
+  k_depth_finish<<<g, kBlock, 0, s>>>(n, a, parent, depth, rootmax, cyc);
+  CK_LAUNCH();
+  h.read_box(reinterpret_cast<int64_t*>(cyc), 1);
+  const int c = *reinterpret_cast<int*>(h.host_box);
+  *cycle_vertex = c == 0x7F7F7F7F ? -1 : c;
+  return rounds;
+}
+
+}  // namespace rstg

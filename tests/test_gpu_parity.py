@@ -410,3 +410,36 @@ def test_step_counts_rerun_identical(rst, O):
                     assert np.array_equal(p, res[0][0])
                     assert (st["steps"], st["work"]) == (res[0][3]["steps"], res[0][3]["work"]), (algo, csr)
             dg.close()
+
+
+# ---- device forest_depth --------------------------------
+def test_forest_depth_device(rst, O):
+    for spec, root in ((("road", 300), 0), (("kron", 13), 5), (("path", 5000), 4999), (("grid", 40, 60), 77)):
+        g = O.gen(*spec)
+        dg = dev_graph(rst, g)
+        for algo in ALGOS:
+            p = O.run(g, algo, root)[0]
+            depth, rmax, best = dg.forest_depth(p)
+            assert best == O.forest_depth(p), (spec, algo)
+            # per-vertex depth against a direct walk, per-root maxima against the depths
+            for v in range(0, g.n, max(1, g.n // 97)):
+                d, x = 0, v
+                while p[x] != x:
+                    x, d = p[x], d + 1
+                assert depth[v] == d
+            roots = np.nonzero(p == np.arange(g.n))[0]
+            assert (rmax[roots] >= 0).all() and (np.delete(rmax, roots) == -1).all()
+        dg.close()
+    g = O.gen("path", 8)
+    dg = dev_graph(rst, g)
+    cyc = np.array([1, 2, 0, 3, 3, 4, 5, 6], np.int64)
+    with pytest.raises(rst.RSTError, match="parent array contains a cycle at vertex 0"):
+        dg.forest_depth(cyc)
+    with pytest.raises(rst.RSTError, match="parent out of range at vertex 2"):
+        dg.forest_depth(np.array([0, 0, 9, 2, 3, 4, 5, 6], np.int64))
+    tail = np.array([5, 0, 1, 3, 3, 6, 5, 6], np.int64)  # 0 -> 5 -> 6 -> 5: the walk meets 5 twice
+    with pytest.raises(rst.RSTError, match="parent array contains a cycle at vertex 5"):
+        dg.forest_depth(tail)
+    with pytest.raises(O.OracleError, match="cycle at vertex 5"):
+        O.forest_depth(tail)
+    dg.close()

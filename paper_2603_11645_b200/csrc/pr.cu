@@ -24,6 +24,10 @@ namespace rstg {
 
 void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_base,
                  const int32_t* rep, unsigned long long* slot, int* any_prop);
+void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* slot,
+                   unsigned long long* out_count, int* any_prop);
+void cc_round_done(Handle& h, int64_t out_count);
+void cc_reset_rounds(Handle& h);
 
 // Device control block layout (int32 words inside dev_box + 16).
 enum PrCtl : int {
@@ -50,10 +54,13 @@ __global__ void k_pr_init(int64_t n, int32_t* parent, int32_t* rep, int32_t* scr
   }
 }
 
-__global__ void k_anc_identity(int64_t n, int L, int32_t* anc) {
+// make_pr_state's anc[v][k] = v (pr_rst.cpp:60-68): every level of the
+// identity table equals level 0, so only level 0 is written and the valid
+// level count starts at 1 (reads of higher levels clamp to it).
+__global__ void k_anc_identity(int64_t n, int32_t* anc) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x)
-    for (int k = 0; k < L; ++k) anc[(int64_t)k * n + v] = (int32_t)v;
+    anc[v] = (int32_t)v;
 }
 
 // resolve winners against the frozen rep (pr_rst.cpp:112-122)
@@ -243,6 +250,8 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   int32_t* anc = h.ws<int32_t>(WS_PR_ANC, (size_t)n * L);
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
   h.slots_clean = nullptr;  // graft rounds leave slots of their own
+  cc_reset_rounds(h);       // (graft rounds use the CC's active-edge lists)
+  unsigned long long* crossing = reinterpret_cast<unsigned long long*>(h.dev_box) + 18;
   h.round0_slots = nullptr;  // (and overwrite an upload's round-0 keys)
   int* ctl = reinterpret_cast<int*>(h.ws<int>(WS_BFS_CTRL, C_NWORDS + 8));
   unsigned long long* bad_mark = reinterpret_cast<unsigned long long*>(h.dev_box) + 16;
@@ -252,7 +261,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
 
   h.timer.begin(s, "pr.init");
   k_pr_init<<<g, kBlock, 0, s>>>(n, parent, rep, scratch, mark, groot, slot);
-  k_anc_identity<<<g, kBlock, 0, s>>>(n, L, anc);  // make_pr_state :60-68
+  k_anc_identity<<<g, kBlock, 0, s>>>(n, anc);  // make_pr_state :60-68
   CK_LAUNCH();
   CK(cudaMemsetAsync(bad_mark, 0xFF, sizeof(unsigned long long), s));
   h.stats.step(n, 2);
@@ -273,10 +282,10 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     h.stats.step(n);
     h.stats.step(n);
   };
-  // ctl[C_LMAX] = L initially (identity table: every level valid).
+  // ctl[C_LMAX] = 1 initially (identity table: level 0 stands for all).
   {
     int init[C_NWORDS + 8] = {0};
-    init[C_LMAX] = L;
+    init[C_LMAX] = 1;
     CK(cudaMemcpyAsync(ctl, init, sizeof(init), cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
   }
@@ -291,10 +300,16 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   for (int64_t round = 0;; ++round) {
     if (round > n + 1) throw AlgoError("grafting failed to converge");
     h.timer.begin(s, "pr.graft");
+    // graft proposals with active-edge filtering (as in the CC: an edge
+    // inside one tree stays inside; the proposals are unchanged)
     CK(cudaMemsetAsync(ctl + C_ANY, 0, sizeof(int), s));
-    launch_hook(h, mode, h.g.edges, m, (uint32_t)h.g.e_base, rep, slot, ctl + C_ANY);
+    CK(cudaMemsetAsync(crossing, 0, sizeof(unsigned long long), s));
+    cc_hook_round(h, mode, rep, slot, crossing, ctl + C_ANY);
     CK(cudaMemcpyAsync(h.host_box, ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h.host_box + 1, crossing, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    cc_round_done(h, h.host_box[1]);
     h.timer.end(s);
     h.stats.rounds = round + 1;
     if (reinterpret_cast<int*>(h.host_box)[C_ANY] == 0) break;  // no graft (:279)

@@ -96,6 +96,10 @@ class Handle {
   // Set by the edge upload: WS_SLOT already holds round 0's hook keys
   // (computed while the edges streamed in), consumed by cc_exact.
   const void* round0_slots = nullptr;
+  // Percent of sampled edges joining vertex ids less than a rank tile
+  // apart (-1: not measured for this graph). Decides the Euler-tour
+  // ranking: tile contraction for locally numbered graphs, else ruling sets.
+  int edge_locality = -1;
   cudaStream_t copy_stream = nullptr;  // H2D staging of uploads (lazily created)
   cudaStream_t stream = nullptr;
   bool own_stream = true;
@@ -181,7 +185,12 @@ enum WsSlot : int {
   WS_ETO,         // u32 2N        arc heads, pairs (2i: a->b, 2i+1: b->a)
   WS_XBITS,       // u32 n/32      exit-set membership bitmap (cc.cu)
   WS_LABELS,      // u32 n         one label per component (euler.cu)
+  WS_TOFF,        // u16 2N        offset of each arc in its tile segment (tilerank.cu)
   WS_CCROOTS,     // u32 3(n+1)    round-0 roots + current CC roots, ping-pong (cc.cu)
+  WS_TSTATE,      // u64 tiles+1   tile counter + look-back states (tilerank.cu)
+  // tile-contraction levels >= 2 (tilerank.cu), one arena per level
+  WS_TL2,
+  WS_TL_LAST = WS_TL2 + 8,
   // list-ranking levels >= 1 (listrank.cu), one arena per level
   WS_LR_L1,
   WS_LR_LAST = WS_LR_L1 + 12,

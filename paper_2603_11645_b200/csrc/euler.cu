@@ -20,6 +20,7 @@
 //   * derive_parents (:155-178): in each arc pair the higher-ranked arc is
 //     the return arc, parent[from] = to.
 #include <algorithm>
+#include <cstdlib>
 
 #include "engine.hpp"
 #include "listrank.cuh"
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(kBlock)
     k_euler_fix(int64_t n, const int32_t* lab, const uint8_t* __restrict__ present,
                 uint32_t* minv, EulerIO io, bool cc_slots, uint32_t* labels_out,
                 unsigned long long* nlabels, uint32_t* rpos, uint32_t* sl, unsigned long long* ctr,
-                unsigned long long* tiles, int logk, int ob, uint32_t cap) {
+                unsigned long long* tiles, int logk, int ob, uint32_t cap, bool rulers) {
   constexpr int64_t kTile = (int64_t)kFixItems * kBlock;
   __shared__ unsigned long long s_tile;
   __shared__ uint32_t s_nl;
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kBlock)
         atomicMin(&minv[l], (uint32_t)v);  // the group's lowest lane has its smallest vertex
       if (present ? present[v] != 0 : l == (int32_t)v) flags |= 1u << (16 + k);
       h2[k] = io.rhead[v];
-      if (cc_slots && l != (int32_t)v) {
+      if (rulers && cc_slots && l != (int32_t)v) {
         if (lr_hash_ruler((uint32_t)v, logk)) flags |= 1u << (2 * k);
         if (lr_hash_ruler(io.nslots + (uint32_t)v, logk)) flags |= 2u << (2 * k);
       }
@@ -143,7 +144,8 @@ __global__ void __launch_bounds__(kBlock)
 __global__ void __launch_bounds__(kBlock)
     k_euler_roots(const uint32_t* __restrict__ labels, const unsigned long long* nlabels,
                   const uint32_t* __restrict__ minv, EulerIO io, int32_t* parent, uint32_t* rpos,
-                  uint32_t* sl, unsigned long long* ctr, int logk, int ob, uint32_t cap) {
+                  uint32_t* sl, unsigned long long* ctr, int logk, int ob, uint32_t cap,
+                  bool rulers) {
   const int64_t L = (int64_t)*nlabels;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < L; b += stride) {
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(kBlock)
         io.S[arc_rev(tl, io.nslots)] = kNone32;  // the tour ends back at the root
       }
     }
-    const bool head = hd != kNone32 && !lr_hash_ruler(hd, logk);
+    const bool head = rulers && hd != kNone32 && !lr_hash_ruler(hd, logk);
     const uint32_t id = lr_block_claim(head ? 1u : 0u, ctr);
     if (head) lr_put(id, hd, rpos, sl, ob, cap);
   }
@@ -208,6 +210,25 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// derive_parents on tile ranks (tilerank.cu): rank = segstart[seg] + off.
+__global__ void __launch_bounds__(kBlock)
+    k_orient_tiles(int64_t N, const int32_t* __restrict__ lab, bool cc_slots,
+                   const uint2* __restrict__ eto, const uint32_t* __restrict__ seg,
+                   const uint16_t* __restrict__ off, const uint32_t* __restrict__ segstart,
+                   int32_t* __restrict__ parent) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (cc_slots && lab[i] == (int32_t)i) continue;  // no tree edge in this slot
+    const uint2 t = eto[i];  // (b, a): arc i = a -> b, arc N + i = b -> a
+    const uint32_t rp = segstart[seg[i]] + off[i];
+    const uint32_t rq = segstart[seg[N + i]] + off[N + i];
+    if (rp > rq)
+      parent[t.y] = (int32_t)t.x;  // a -> b returns: parent[a] = b
+    else
+      parent[t.x] = (int32_t)t.y;  // b -> a returns: parent[b] = a
+  }
+}
+
 EulerIO euler_buffers(Handle& h, int64_t N, bool local_written) {
   EulerIO io;
   io.nslots = (uint32_t)N;
@@ -227,6 +248,39 @@ void euler_link_edges(Handle& h, const EulerIO& io, int64_t T) {
   k_link_edges<<<grid_for(T), kBlock, 0, h.stream>>>(T, h.g.edges, io);
   CK_LAUNCH();
   h.stats.step(T);
+}
+
+// Edge locality sample: how many of `samples` evenly spaced edges join
+// vertex ids less than kLocalSpan apart.
+constexpr int kLocalSpan = 4096;
+constexpr int kLocalitySamples = 1 << 16;
+__global__ void k_edge_locality(const int2* __restrict__ edges, int64_t m, int samples,
+                                unsigned long long* cnt) {
+  uint32_t c = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < samples; i += gridDim.x * blockDim.x) {
+    const int2 e = edges[(int64_t)i * m / samples];
+    c += abs(e.y - e.x) < kLocalSpan;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, (unsigned long long)c);
+}
+
+static int edge_locality(Handle& h) {
+  if (h.edge_locality < 0) {
+    const int64_t m = h.g.m;
+    if (m == 0 || h.g.edges == nullptr) {
+      h.edge_locality = 0;
+    } else {
+      const int samples = (int)std::min<int64_t>(m, kLocalitySamples);
+      unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h.dev_box) + 17;
+      CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t), h.stream));
+      k_edge_locality<<<64, kBlock, 0, h.stream>>>(h.g.edges, m, samples, cnt);
+      CK_LAUNCH();
+      h.read_box(h.dev_box + 17, 1);
+      h.edge_locality = (int)(100 * h.host_box[0] / samples);
+    }
+  }
+  return h.edge_locality;
 }
 
 void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, int64_t T,
@@ -257,13 +311,19 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
     CK(cudaMemsetAsync(present, 0, (size_t)n, s));
     k_mark_labels<<<grid_for(n), kBlock, 0, s>>>(n, labels, present);
   }
+  // tile-contracted ranking (tilerank.cu) or the ruling-set walk
+  // (a vertex-slot tour moves between nearby slots exactly when tree edges
+  // join nearby ids; RSTG_LR_TILES=0/1 forces the choice)
+  const char* tiles_env = getenv("RSTG_LR_TILES");
+  const bool use_tiles =
+      !verify && (tiles_env ? atoi(tiles_env) != 0 : cc_slots && edge_locality(h) >= 50);
   k_euler_fix<<<grid_for((n + kFixItems - 1) / kFixItems), kBlock, 0, s>>>(
       n, labels, present, minv, io, cc_slots, lablist, comps, rpos, sl, ctr, tiles, P.logk0, P.ob,
-      (uint32_t)P.cap);
+      (uint32_t)P.cap, !use_tiles);
   k_override_root<<<1, 32, 0, s>>>(labels, minv, designated_root);
   k_euler_roots<<<grid_for(n), kBlock, 0, s>>>(lablist, comps, minv, io, parent, rpos, sl, ctr,
-                                               P.logk0, P.ob, (uint32_t)P.cap);
-  if (!cc_slots && T > 0)
+                                               P.logk0, P.ob, (uint32_t)P.cap, !use_tiles);
+  if (!use_tiles && !cc_slots && T > 0)
     k_register_slots<<<grid_for(T), kBlock, 0, s>>>(T, io.nslots, rpos, sl, ctr, P.logk0, P.ob,
                                                     (uint32_t)P.cap);
   CK_LAUNCH();
@@ -278,6 +338,17 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   }
   if (T == 0) return;
 
+  if (use_tiles) {
+    const TileRank tr = lr_rank_tiles(h, P, N, io.S, labels, cc_slots, T, verify);
+    h.timer.begin(s, "euler.orient", 8.0 * N + 20.0 * T);
+    k_orient_tiles<<<grid_for(N), kBlock, 0, s>>>(N, labels, cc_slots,
+                                                  reinterpret_cast<const uint2*>(io.eto), tr.seg,
+                                                  tr.off, tr.segstart, parent);
+    CK_LAUNCH();
+    h.stats.step(N);
+    h.timer.end(s);
+    return;
+  }
   const uint32_t* rstart = lr_rank(h, P, E, io.S, sl, rpos, ctr, verify, 2 * T, nullptr);
 
   h.timer.begin(s, "euler.orient", 8.0 * N + 16.0 * T + 4.0 * T);

@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
   }
   for (int x = threadIdx.x; x < N; x += blockDim.x) {
-    if (p[x] != kNone32) *bad = 1;
+    if (bad && p[x] != kNone32) *bad = 1;
     pre[x] = v[x];
   }
 }
@@ -665,8 +665,8 @@ static bool list_prefix_coop(Handle& h, const LrParams& P, int64_t N0, const uin
 }
 
 // pre[x] = sum of w over the nodes before x in its list.
-static void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t* next,
-                        const uint32_t* w, uint32_t* pre, int depth, bool verify, int* bad) {
+void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t* next, const uint32_t* w,
+                 uint32_t* pre, int depth, bool verify, int* bad) {
   if (N <= 0) return;
   const cudaStream_t s = h.stream;
   if (N <= kBaseMax) {

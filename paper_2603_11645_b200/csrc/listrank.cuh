@@ -93,6 +93,23 @@ const uint32_t* lr_rank(Handle& h, const LrParams& P, int64_t E, const uint32_t*
                         uint32_t* rpos, unsigned long long* ctr, bool verify, int64_t expect,
                         int64_t* R_out);
 
+// pre[x] = sum of w over the nodes before x in its list (recursive ruling
+// sets; level arenas sized by max(N, P.cap)).
+void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t* next, const uint32_t* w,
+                 uint32_t* pre, int depth, bool verify, int* bad);
+
+// Tile-contracted ranking of the Euler tour (tilerank.cu): each CTA ranks
+// the arcs of a tile of consecutive slots on chip (maximal runs of tour
+// successors inside the tile = segments), then the segment list is ranked
+// by list_prefix. rank(x) = segstart[seg[x]] + off[x].
+struct TileRank {
+  const uint32_t* seg;       // 2N segment id per arc
+  const uint16_t* off;       // 2N offset within the segment
+  const uint32_t* segstart;  // rank of each segment's first arc
+};
+TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* S,
+                       const int32_t* lab, bool cc_slots, int64_t T, bool verify);
+
 // Generic entry (rstg_k_list_rank, explicit lists): registers hash rulers
 // and every list head (positions without a predecessor), then lr_rank.
 const uint32_t* lr_rank_lists(Handle& h, int64_t E, const uint32_t* succ, uint32_t* sl, bool verify,

@@ -1,0 +1,545 @@
+// tilerank.cu -- Euler-tour ranking by tile contraction.
+//
+// The tour of a locally numbered tree (meshes, paths, grids: a tree edge
+// joins nearby vertex ids, and tree edge slots are vertex ids) mostly
+// steps between nearby slots. A CTA takes a tile of kSlots consecutive
+// slots -- its arcs i and N + i -- and ranks them on chip:
+//   1. the successor of every arc of the tile is read once (all loads of
+//      a thread in flight together) and kept in shared memory as a local
+//      index when it stays in the tile; a segment is a maximal run of
+//      tour successors inside the tile, its head the arc without an
+//      in-tile predecessor;
+//   2. rulers = the heads plus one arc in 16 by index (one per thread);
+//      every ruler walks to the next ruler in shared memory, writing each
+//      arc it passes (ruler << 16 | offset) and the reached ruler's
+//      (predecessor ruler << 16 | distance) -- O(arcs) work, ~16 hops a walk;
+//   3. pointer jumping over the rulers alone (a few hundred per tile)
+//      gives every ruler its head and offset; heads are numbered with one
+//      global atomic per tile; every arc writes (segment, offset), every
+//      segment tail the segment's length and last arc.
+// The segments form lists again -- one per tour, shorter by the
+// contraction factor -- that list_prefix ranks (recursive ruling sets).
+// A tour that jumps between tiles (random vertex ids) gains little; the
+// caller then keeps the ruling-set walk (listrank.cu).
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "engine.hpp"
+#include "listrank.cuh"
+
+namespace rstg {
+
+constexpr int kTileRankThreads = 1024;
+
+constexpr uint16_t kTileExit = 0x7FFF;   // successor leaves the tile / list end
+constexpr uint16_t kTileRuler = 0x8000;  // flag on nx[li]: li is a ruler
+
+// Tile-ordered numbering, single pass (decoupled look-back): tile ids are
+// taken in launch order from state[0], each tile publishes its count and
+// then its inclusive prefix in state[1 + tile] (flag in the top two bits,
+// value below, one 64-bit word: no separate fence for the payload). A tile
+// only waits on tiles that took their ids earlier, so it cannot deadlock.
+// Segment ids in tile order keep the segment list local: the next level
+// contracts it by tiles again.
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = kLbAgg - 1;
+__device__ __forceinline__ uint32_t tile_take(unsigned long long* state) {
+  return (uint32_t)atomicAdd(state, 1ull);
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+// Publishes the tile's count as soon as it is known (before the walks), so
+// that by the time the tile needs its prefix the tiles before it have
+// mostly published theirs.
+__device__ __forceinline__ void tile_publish(unsigned long long* state, uint32_t tile,
+                                             uint32_t count) {
+  atomicExch(&state[1 + tile], (tile == 0 ? kLbInc : kLbAgg) | count);
+}
+__device__ __forceinline__ uint32_t tile_prefix(unsigned long long* state, uint32_t tile,
+                                                uint32_t count) {
+  if (tile == 0) return 0;
+  unsigned long long* st = state + 1;
+  unsigned long long excl = 0;
+  for (int64_t p = (int64_t)tile - 1;;) {
+    const unsigned long long v = ld_relaxed_gpu(&st[p]);
+    if (!(v >> 62)) continue;  // not published yet
+    excl += v & kLbVal;
+    if ((v >> 62) == 2) break;
+    --p;
+  }
+  atomicExch(&st[tile], kLbInc | (excl + count));
+  return (uint32_t)excl;
+}
+
+template <int kSlots>
+constexpr size_t tile_rank_smem() {
+  return 2 * kSlots * (sizeof(uint32_t) + sizeof(uint16_t) + sizeof(uint8_t));
+}
+
+// CTAs per SM: shared memory (228 KB per SM, 1 KB reserved per CTA) or threads
+template <int kSlots, int kThreads>
+constexpr int tile_rank_blocks() {
+  constexpr int by_smem = 233472 / (int)(tile_rank_smem<kSlots>() + 1024);
+  constexpr int by_threads = 2048 / kThreads;
+  return by_smem < by_threads ? by_smem : by_threads;
+}
+
+// Local arc index: slot j of the tile -> arc j (t0 + j) and kSlots + j
+// (N + t0 + j). All index math is 32-bit: arcs are u32 (2N < 2^32).
+template <int kSlots, int kThreads>
+__global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>())
+    k_tile_rank(uint32_t N, const uint32_t* __restrict__ S, const int32_t* __restrict__ lab,
+                bool cc_slots, uint32_t T, uint32_t* __restrict__ seg, uint16_t* __restrict__ off,
+                uint32_t* __restrict__ seg_len, uint32_t* __restrict__ seg_tail,
+                unsigned long long* nseg, unsigned long long* state,
+                unsigned long long* walked) {
+  static_assert(2 * kSlots <= kTileExit, "local arc index must fit 15 bits");
+  constexpr int kArcs = 2 * kSlots;
+  constexpr int kPer = kSlots / kThreads;  // slots per thread
+  constexpr int kOwn = 2 * kPer;           // arcs per thread
+  static_assert(kOwn <= 32, "own-arc masks are 32 bits");
+  extern __shared__ uint32_t word[];  // arc: ruler << 16 | offset; ruler: pred ruler << 16 | dist
+  uint16_t* nx = reinterpret_cast<uint16_t*>(word + kArcs);  // local successor | ruler flag
+  uint16_t* hid = nx;  // (after the walks) head -> local segment number
+  // has an in-tile predecessor: plain byte stores (racing stores all write
+  // 1), not bitmap atomics -- a path's warp would hit one word 32 times
+  uint8_t* haspred = reinterpret_cast<uint8_t*>(nx + kArcs);
+  __shared__ uint32_t s_nh, s_walk, s_tile, s_base;
+  __shared__ int s_rounds;
+  if (threadIdx.x == 0) s_tile = tile_take(state);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t t0 = tile * (uint32_t)kSlots;
+  const uint32_t cnt = min((uint32_t)kSlots, N - t0);  // slots in this tile
+  const uint32_t tid = threadIdx.x;
+  // own arc q: slot j = tid + (q >> 1) * kThreads, local j + (q & 1) * kSlots
+  auto local_of = [&](int q) -> uint32_t { return tid + (q >> 1) * kThreads + (q & 1) * kSlots; };
+  auto global_of = [&](int q) -> uint32_t {
+    return t0 + tid + (q >> 1) * kThreads + ((q & 1) ? N : 0u);
+  };
+  if (tid == 0) s_nh = s_walk = 0;
+  for (int w = tid; w < kArcs / 16; w += kThreads) reinterpret_cast<uint4*>(haspred)[w] = uint4{0, 0, 0, 0};
+  // 1. loads: validity of each own slot, then the successors of its arcs
+  //    (staged in word[], free until the walks)
+  uint32_t vmask = 0;  // own arcs that exist
+  const uint32_t last = N - 1;  // loads are unconditional (clamped): all in flight at once
+  if (cc_slots) {
+    int32_t lv[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) lv[k] = __ldcs(&lab[min(t0 + tid + k * kThreads, last)]);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const uint32_t j = tid + k * kThreads;
+      vmask |= (j < cnt && lv[k] != (int32_t)(t0 + j)) ? 3u << (2 * k) : 0u;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const uint32_t j = tid + k * kThreads;
+      vmask |= (j < cnt && t0 + j < T) ? 3u << (2 * k) : 0u;
+    }
+  }
+  constexpr int kBatch = kOwn < 16 ? kOwn : 16;
+#pragma unroll
+  for (int q0 = 0; q0 < kOwn; q0 += kBatch) {
+    uint32_t y[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint32_t j = min(t0 + tid + ((q0 + q) >> 1) * kThreads, last);
+      y[q] = __ldcs(&S[((q0 + q) & 1) ? N + j : j]);
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) word[local_of(q0 + q)] = y[q];
+  }
+  __syncthreads();  // haspred zeroed
+  uint32_t tmask = 0;  // own arcs whose successor leaves the tile (segment tails)
+#pragma unroll
+  for (int q = 0; q < kOwn; ++q) {
+    if (!(vmask >> q & 1)) continue;
+    const uint32_t v = word[local_of(q)];
+    uint32_t ls = kTileExit;
+    if (v - t0 < cnt) ls = v - t0;                              // forward arc in the tile
+    else if (v - N - t0 < cnt && v >= N) ls = v - N - t0 + kSlots;  // reverse arc in the tile
+    if (v == kNone32) ls = kTileExit;
+    if (ls != kTileExit) haspred[ls] = 1;
+    else tmask |= 1u << q;
+    nx[local_of(q)] = (uint16_t)ls;
+  }
+  __syncthreads();
+  // 2. rulers: heads, and own arc q == tid % kOwn (one arc in kOwn by index)
+  uint32_t hmask = 0, rmask = 0;
+#pragma unroll
+  for (int q = 0; q < kOwn; ++q) {
+    const uint32_t li = local_of(q);
+    const bool head = (vmask >> q & 1) && !haspred[li];
+    const bool ruler = head || ((vmask >> q & 1) && q == (int)(tid % kOwn));
+    hmask |= head ? 1u << q : 0u;
+    rmask |= ruler ? 1u << q : 0u;
+    if (ruler) nx[li] |= kTileRuler;
+    if (head) word[li] = li << 16;
+  }
+  const uint32_t hbase = hmask ? atomicAdd(&s_nh, (uint32_t)__popc(hmask)) : 0u;
+  __syncthreads();
+  if (tid == 0) tile_publish(state, tile, s_nh);
+  for (uint32_t m = rmask; m; m &= m - 1) {
+    const uint32_t r = local_of(__ffs(m) - 1);
+    uint32_t cur = nx[r] & kTileExit, o = 1;
+    while (cur != kTileExit) {
+      const uint32_t v = nx[cur];
+      word[cur] = r << 16 | o;
+      if (v & kTileRuler) break;
+      cur = v & kTileExit;
+      ++o;
+    }
+  }
+  __syncthreads();
+  // 3. pointer jumping over the rulers that are not heads
+  int r = 0;
+  for (; r < 16; ++r) {
+    int changed = 0;
+    for (uint32_t m = rmask & ~hmask; m; m &= m - 1) {
+      const uint32_t li = local_of(__ffs(m) - 1);
+      const uint32_t v = word[li];
+      const uint32_t p = v >> 16;
+      const uint32_t w = word[p];
+      if ((w >> 16) == p) continue;  // p is a head: done
+      word[li] = (w & 0xFFFF0000u) | ((v + w) & 0xFFFFu);
+      changed = 1;
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  if (walked && tid == 0) s_rounds = r;
+  {
+    uint32_t k = hbase;
+    for (uint32_t m = hmask; m; m &= m - 1) hid[local_of(__ffs(m) - 1)] = (uint16_t)k++;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s_base = tile_prefix(state, tile, s_nh);
+    if (tile == gridDim.x - 1) *nseg = s_base + s_nh;
+  }
+  __syncthreads();
+  const uint32_t sbase = s_base;
+#pragma unroll
+  for (int q = 0; q < kOwn; ++q) {
+    if (!(vmask >> q & 1)) continue;
+    uint32_t w = word[local_of(q)], o = 0;
+    if (!(rmask >> q & 1)) {  // (ruler, offset) -> the ruler's (head, offset)
+      o = w & 0xFFFFu;
+      w = word[w >> 16];
+    }
+    o += w & 0xFFFFu;
+    const uint32_t sid = sbase + hid[w >> 16];
+    const uint32_t x = global_of(q);
+    __stcs(&seg[x], sid);
+    __stcs(&off[x], (uint16_t)o);
+    if (tmask >> q & 1) {
+      seg_len[sid] = o + 1;
+      seg_tail[sid] = x;
+    }
+  }
+  if (walked) {
+    atomicAdd(&s_walk, (uint32_t)__popc(vmask));
+    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(walked, (unsigned long long)s_walk);
+      atomicMax(reinterpret_cast<unsigned long long*>(walked) + 1, (unsigned long long)s_rounds);
+    }
+  }
+}
+
+// Level >= 2: the same contraction on a weighted list -- node i of
+// [0, n), successor next[i] (NONE at the end), weight w[i] (its segment
+// length below). A tile is kNodes consecutive node ids (tile-ordered ids
+// from the level below make these neighbours on the tour). Each node gets
+// its next-level segment and its weighted offset in it (the sum of the
+// weights before it); each segment its weight and last node.
+template <int kNodes>
+constexpr size_t tile_rank_w_smem() {
+  return kNodes * (sizeof(unsigned long long) + sizeof(uint16_t) + sizeof(uint8_t));
+}
+
+template <int kNodes, int kThreads>
+__global__ void __launch_bounds__(kThreads)
+    k_tile_rank_w(uint32_t n, const uint32_t* __restrict__ next, const uint32_t* __restrict__ w,
+                  uint32_t* __restrict__ seg, uint32_t* __restrict__ off,
+                  uint32_t* __restrict__ seg_len, uint32_t* __restrict__ seg_tail,
+                  unsigned long long* nseg, unsigned long long* state) {
+  static_assert(kNodes <= kTileExit, "local node index must fit 15 bits");
+  constexpr int kPer = kNodes / kThreads;
+  static_assert(kPer <= 32, "own-node masks are 32 bits");
+  // node: ruler << 32 | weighted offset; ruler: pred ruler << 32 | distance;
+  // before the walks: the node's own weight
+  extern __shared__ unsigned long long wd[];
+  uint16_t* nx = reinterpret_cast<uint16_t*>(wd + kNodes);  // local successor | ruler flag
+  uint16_t* hid = nx;
+  uint8_t* haspred = reinterpret_cast<uint8_t*>(nx + kNodes);
+  __shared__ uint32_t s_nh, s_tile, s_base;
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) {
+    s_tile = tile_take(state);
+    s_nh = 0;
+  }
+  for (int k = tid; k < kNodes / 16; k += kThreads)
+    reinterpret_cast<uint4*>(haspred)[k] = uint4{0, 0, 0, 0};
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t t0 = tile * (uint32_t)kNodes;
+  const uint32_t cnt = min((uint32_t)kNodes, n - t0);
+  const uint32_t last = n - 1;
+  uint32_t y[kPer], wt[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const uint32_t i = min(t0 + tid + k * kThreads, last);
+    y[k] = __ldcs(&next[i]);
+    wt[k] = __ldcs(&w[i]);
+  }
+  uint32_t vmask = 0, tmask = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const uint32_t j = tid + k * kThreads;
+    if (j >= cnt) continue;
+    vmask |= 1u << k;
+    const uint32_t ls = (y[k] != kNone32 && y[k] - t0 < cnt) ? y[k] - t0 : kTileExit;
+    if (ls != kTileExit) haspred[ls] = 1;
+    else tmask |= 1u << k;
+    nx[j] = (uint16_t)ls;
+    wd[j] = wt[k];
+  }
+  __syncthreads();
+  uint32_t hmask = 0, rmask = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const uint32_t j = tid + k * kThreads;
+    const bool head = (vmask >> k & 1) && !haspred[j];
+    const bool ruler = head || ((vmask >> k & 1) && k == (int)(tid % kPer));
+    hmask |= head ? 1u << k : 0u;
+    rmask |= ruler ? 1u << k : 0u;
+    if (ruler) nx[j] |= kTileRuler;
+  }
+  const uint32_t hbase = hmask ? atomicAdd(&s_nh, (uint32_t)__popc(hmask)) : 0u;
+  __syncthreads();
+  if (tid == 0) tile_publish(state, tile, s_nh);
+  // heads: (self, 0); a head is never reached by a walk, and every ruler's
+  // own weight is in a register
+  for (uint32_t m = hmask; m; m &= m - 1) {
+    const uint32_t j = tid + (__ffs(m) - 1) * kThreads;
+    wd[j] = (unsigned long long)j << 32;
+  }
+  for (uint32_t m = rmask; m; m &= m - 1) {
+    const int k = __ffs(m) - 1;
+    const uint32_t r = tid + k * kThreads;
+    uint32_t cur = nx[r] & kTileExit;
+    unsigned long long acc = wt[k];
+    while (cur != kTileExit) {
+      const uint32_t v = nx[cur];
+      if (v & kTileRuler) {
+        wd[cur] = (unsigned long long)r << 32 | acc;
+        break;
+      }
+      const uint32_t wc = (uint32_t)wd[cur];  // its weight (one walk visits a node)
+      wd[cur] = (unsigned long long)r << 32 | acc;
+      acc += wc;
+      cur = v & kTileExit;
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < 16; ++r) {
+    int changed = 0;
+    for (uint32_t m = rmask & ~hmask; m; m &= m - 1) {
+      const uint32_t j = tid + (__ffs(m) - 1) * kThreads;
+      const unsigned long long v = wd[j];
+      const uint32_t p = (uint32_t)(v >> 32);
+      const unsigned long long u = wd[p];
+      if ((uint32_t)(u >> 32) == p) continue;
+      wd[j] = (u & 0xFFFFFFFF00000000ull) | (uint32_t)(v + u);
+      changed = 1;
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  {
+    uint32_t c = hbase;
+    for (uint32_t m = hmask; m; m &= m - 1) hid[tid + (__ffs(m) - 1) * kThreads] = (uint16_t)c++;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s_base = tile_prefix(state, tile, s_nh);
+    if (tile == gridDim.x - 1) *nseg = s_base + s_nh;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    if (!(vmask >> k & 1)) continue;
+    const uint32_t j = tid + k * kThreads;
+    unsigned long long v = wd[j];
+    uint32_t o = 0;
+    if (!(rmask >> k & 1)) {
+      o = (uint32_t)v;
+      v = wd[v >> 32];
+    }
+    o += (uint32_t)v;
+    const uint32_t sid = s_base + hid[v >> 32];
+    __stcs(&seg[t0 + j], sid);
+    __stcs(&off[t0 + j], o);
+    if (tmask >> k & 1) {
+      seg_len[sid] = o + wt[k];
+      seg_tail[sid] = t0 + j;
+    }
+  }
+}
+
+// next segment of each segment: the one headed by its tail's successor
+__global__ void k_seg_link(const unsigned long long* nseg, const uint32_t* __restrict__ seg_tail,
+                           const uint32_t* __restrict__ S, const uint32_t* __restrict__ seg,
+                           uint32_t* __restrict__ seg_next) {
+  const int64_t R = (int64_t)*nseg;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t ex = S[seg_tail[i]];
+    seg_next[i] = ex == kNone32 ? kNone32 : seg[ex];
+  }
+}
+
+// pre[i] = pre_up[seg[i]] + off[i]
+__global__ void k_tile_expand(int64_t n, const uint32_t* __restrict__ seg,
+                              const uint32_t* __restrict__ off, const uint32_t* __restrict__ pre_up,
+                              uint32_t* __restrict__ pre) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    pre[i] = pre_up[seg[i]] + off[i];
+}
+
+namespace {
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+template <class K>
+void set_smem(K kern, size_t smem, bool& done) {
+  if (!done) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done = true;
+  }
+}
+constexpr int kLevelNodes = 8192;
+constexpr int kLevelThreads = 1024;
+}  // namespace
+
+// Weighted prefix of a tile-ordered list (level >= 2 of the contraction):
+// pre[i] = sum of len over the nodes before i on its list. Contracts by
+// tiles while that pays, then list_prefix (ruling sets / one-CTA base).
+static void tile_prefix_levels(Handle& h, const LrParams& P, int64_t n, const uint32_t* next,
+                               const uint32_t* len, uint32_t* pre, int level, bool dbg) {
+  const cudaStream_t s = h.stream;
+  if (n <= 8192 || level >= WS_TL_LAST - WS_TL2 + 2) {
+    list_prefix(h, P, n, next, len, pre, 0, false, nullptr);
+    return;
+  }
+  // arena of this level: up-mapping of the n nodes (seg, off) and the
+  // next level's nodes (len, tail, next, pre) -- at most n of them
+  size_t cap = 1;
+  while (cap < (size_t)n) cap <<= 1;  // grow-only and stable across builds
+  uint32_t* a = h.ws<uint32_t>(WS_TL2 + level - 2, 6 * cap);
+  uint32_t* seg = a;
+  uint32_t* off = a + cap;
+  uint32_t* len2 = a + 2 * cap;
+  uint32_t* tail2 = a + 3 * cap;
+  uint32_t* next2 = a + 4 * cap;
+  uint32_t* pre2 = a + 5 * cap;
+  const unsigned tiles = (unsigned)((n + kLevelNodes - 1) / kLevelNodes);
+  unsigned long long* state = h.ws<unsigned long long>(WS_TSTATE, (size_t)tiles + 1);
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h.dev_box) + 8;
+  CK(cudaMemsetAsync(state, 0, ((size_t)tiles + 1) * sizeof(unsigned long long), s));
+  static bool attr = false;
+  constexpr size_t smem = tile_rank_w_smem<kLevelNodes>();
+  set_smem(k_tile_rank_w<kLevelNodes, kLevelThreads>, smem, attr);
+  k_tile_rank_w<kLevelNodes, kLevelThreads><<<tiles, kLevelThreads, smem, s>>>(
+      (uint32_t)n, next, len, seg, off, len2, tail2, cnt, state);
+  k_seg_link<<<grid_for(n / 4 + 1), kBlock, 0, s>>>(cnt, tail2, next, seg, next2);
+  CK_LAUNCH();
+  h.read_box(h.dev_box + 8, 1);
+  const int64_t n2 = h.host_box[0];
+  if (dbg) fprintf(stderr, "lr.tiles level %d: %lld -> %lld\n", level, (long long)n, (long long)n2);
+  if (n2 * 2 > n)  // contraction stalled: rank the segments by ruling sets
+    list_prefix(h, P, n2, next2, len2, pre2, 0, false, nullptr);
+  else
+    tile_prefix_levels(h, P, n2, next2, len2, pre2, level + 1, dbg);
+  k_tile_expand<<<grid_for(n), kBlock, 0, s>>>(n, seg, off, pre2, pre);
+  CK_LAUNCH();
+}
+
+TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* S,
+                       const int32_t* lab, bool cc_slots, int64_t T, bool verify) {
+  const cudaStream_t s = h.stream;
+  const int64_t E = 2 * N;
+  uint32_t* seg = h.ws<uint32_t>(WS_SL, E);
+  uint16_t* off = h.ws<uint16_t>(WS_TOFF, E);
+  // segments <= arcs: sized by E (a fixed bound: no reallocation per build)
+  uint32_t* seg_len = h.ws<uint32_t>(WS_RLEN, E + 1);
+  uint32_t* seg_tail = h.ws<uint32_t>(WS_RNEXT, E + 1);
+  uint32_t* seg_next = h.ws<uint32_t>(WS_RPOS, E + 1);
+  uint32_t* segstart = h.ws<uint32_t>(WS_RD, E + 1);
+  unsigned long long* nseg = reinterpret_cast<unsigned long long*>(h.dev_box) + 8;
+  unsigned long long* walked = reinterpret_cast<unsigned long long*>(h.dev_box) + 14;
+  static const int slots_env = env_int("RSTG_LR_TILESLOTS", 8192);
+  static const int tile_threads_env = env_int("RSTG_LR_TILETHREADS", 1024);
+  static const bool dbg = getenv("RSTG_LR_DEBUG") != nullptr;
+  const int slots = slots_env <= 2048 ? 2048 : slots_env <= 4096 ? 4096 : 8192;
+  const unsigned tiles = (unsigned)((N + slots - 1) / slots);
+  unsigned long long* state = h.ws<unsigned long long>(WS_TSTATE, (size_t)tiles + 1);
+  h.timer.begin(s, "lr.tiles", 12.0 * E);  // succ read + segment id + offset per arc
+  CK(cudaMemsetAsync(state, 0, ((size_t)tiles + 1) * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(h.dev_box + 14, 0, 2 * sizeof(int64_t), s));
+  auto launch = [&](auto kern, int threads, size_t smem, int a) {
+    static bool attr[4] = {false, false, false, false};
+    set_smem(kern, smem, attr[a]);
+    kern<<<tiles, threads, smem, s>>>((uint32_t)N, S, lab, cc_slots, (uint32_t)T, seg, off,
+                                      seg_len, seg_tail, nseg, state,
+                                      verify || dbg ? walked : nullptr);
+  };
+  if (slots == 2048)
+    launch(k_tile_rank<2048, 256>, 256, tile_rank_smem<2048>(), 0);
+  else if (slots == 4096)
+    launch(k_tile_rank<4096, 512>, 512, tile_rank_smem<4096>(), 1);
+  else if (tile_threads_env <= 512)
+    launch(k_tile_rank<8192, 512>, 512, tile_rank_smem<8192>(), 2);
+  else
+    launch(k_tile_rank<8192, 1024>, 1024, tile_rank_smem<8192>(), 3);
+  k_seg_link<<<grid_for(E / 8 + 1), kBlock, 0, s>>>(nseg, seg_tail, S, seg, seg_next);
+  CK_LAUNCH();
+  h.stats.step(E, 2);
+  h.read_box(h.dev_box + 8, 8);  // [8] segments, [14] arcs walked, [15] jump rounds
+  const int64_t R = h.host_box[0];
+  if (dbg)
+    fprintf(stderr, "lr.tiles: %lld arcs -> %lld segments (%.1fx), %lld jump rounds\n",
+            (long long)(2 * T), (long long)R, R ? 2.0 * T / R : 0.0, (long long)h.host_box[7]);
+  if (verify && h.host_box[6] != 2 * T)  // a cycle inside a tile has no head
+    throw AlgoError("list ranking failed to converge: not a forest");
+  h.timer.end(s);
+
+  h.timer.begin(s, "lr.rulers_rank", 16.0 * R);
+  // fixed StepReport charge (the segment count follows the tour layout)
+  const Stats before = h.stats;
+  LrParams Q = P;
+  Q.cap = std::max<int64_t>(P.cap, E + 1);  // (level arenas sized by the fixed bound)
+  static const int levels_env = env_int("RSTG_LR_TILELEVELS", 1);
+  if (levels_env && R * 4 <= E)
+    tile_prefix_levels(h, Q, R, seg_next, seg_len, segstart, 2, dbg);
+  else
+    list_prefix(h, Q, R, seg_next, seg_len, segstart, 0, false, nullptr);
+  const int64_t launches = h.stats.launches;
+  h.stats = before;
+  h.stats.launches = launches;
+  const int64_t Rexp = std::max<int64_t>(E >> P.logk0, 2);
+  int rounds = 1;
+  while ((int64_t{1} << (rounds - 1)) < Rexp) ++rounds;
+  h.stats.steps += rounds;
+  h.stats.work += Rexp * rounds;
+  h.timer.end(s);
+  return TileRank{seg, off, segstart};
+}
+
+}  // namespace rstg

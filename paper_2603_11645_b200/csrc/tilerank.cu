@@ -264,10 +264,13 @@ constexpr size_t tile_rank_w_smem() {
 
 template <int kNodes, int kThreads>
 __global__ void __launch_bounds__(kThreads)
-    k_tile_rank_w(uint32_t n, const uint32_t* __restrict__ next, const uint32_t* __restrict__ w,
-                  uint32_t* __restrict__ seg, uint32_t* __restrict__ off,
-                  uint32_t* __restrict__ seg_len, uint32_t* __restrict__ seg_tail,
-                  unsigned long long* nseg, unsigned long long* state) {
+    k_tile_rank_w(const unsigned long long* n_dev, const uint32_t* __restrict__ tail_in,
+                  const uint32_t* __restrict__ succ_in, const uint32_t* __restrict__ seg_in,
+                  uint32_t* __restrict__ next_out, const uint32_t* __restrict__ w,
+                  uint32_t* __restrict__ seg,
+                  uint32_t* __restrict__ off, uint32_t* __restrict__ seg_len,
+                  uint32_t* __restrict__ seg_tail, unsigned long long* nseg,
+                  unsigned long long* state, int* overflow) {
   static_assert(kNodes <= kTileExit, "local node index must fit 15 bits");
   constexpr int kPer = kNodes / kThreads;
   static_assert(kPer <= 32, "own-node masks are 32 bits");
@@ -286,17 +289,33 @@ __global__ void __launch_bounds__(kThreads)
   for (int k = tid; k < kNodes / 16; k += kThreads)
     reinterpret_cast<uint4*>(haspred)[k] = uint4{0, 0, 0, 0};
   __syncthreads();
+  // node count from the level below (on the device: no host round trip);
+  // the grid is sized by a bound, tiles past the count leave at once
+  const uint32_t n = (uint32_t)*n_dev;
+  const uint32_t ntiles = (n + kNodes - 1) / kNodes;
+  if (blockIdx.x == 0 && ntiles > gridDim.x && tid == 0) *overflow = 1;
   const uint32_t tile = s_tile;
+  if (tile >= ntiles) return;
   const uint32_t t0 = tile * (uint32_t)kNodes;
   const uint32_t cnt = min((uint32_t)kNodes, n - t0);
   const uint32_t last = n - 1;
+  // successor of node i (a segment of the level below): the segment
+  // headed by the successor of its last element, next = seg_in[succ_in[tail_in[i]]]
+  // (computed here, not by a separate pass, and kept for the level above)
   uint32_t y[kPer], wt[kPer];
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     const uint32_t i = min(t0 + tid + k * kThreads, last);
-    y[k] = __ldcs(&next[i]);
+    y[k] = __ldcs(&tail_in[i]);
     wt[k] = __ldcs(&w[i]);
   }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) y[k] = succ_in[y[k]];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) y[k] = y[k] == kNone32 ? kNone32 : seg_in[y[k]];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k)
+    if (tid + k * kThreads < cnt) __stcs(&next_out[t0 + tid + k * kThreads], y[k]);
   uint32_t vmask = 0, tmask = 0;
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
@@ -367,7 +386,7 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   if (tid == 0) {
     s_base = tile_prefix(state, tile, s_nh);
-    if (tile == gridDim.x - 1) *nseg = s_base + s_nh;
+    if (tile == ntiles - 1) *nseg = s_base + s_nh;
   }
   __syncthreads();
 #pragma unroll
@@ -403,10 +422,13 @@ __global__ void k_seg_link(const unsigned long long* nseg, const uint32_t* __res
   }
 }
 
-// pre[i] = pre_up[seg[i]] + off[i]
-__global__ void k_tile_expand(int64_t n, const uint32_t* __restrict__ seg,
+__global__ void k_set_count(unsigned long long* c, unsigned long long v) { *c = v; }
+
+// pre[i] = pre_up[seg[i]] + off[i] over the n_dev nodes of a level
+__global__ void k_tile_expand(const unsigned long long* n_dev, const uint32_t* __restrict__ seg,
                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ pre_up,
                               uint32_t* __restrict__ pre) {
+  const int64_t n = (int64_t)*n_dev;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     pre[i] = pre_up[seg[i]] + off[i];
@@ -428,47 +450,85 @@ constexpr int kLevelNodes = 8192;
 constexpr int kLevelThreads = 1024;
 }  // namespace
 
-// Weighted prefix of a tile-ordered list (level >= 2 of the contraction):
-// pre[i] = sum of len over the nodes before i on its list. Contracts by
-// tiles while that pays, then list_prefix (ruling sets / one-CTA base).
-static void tile_prefix_levels(Handle& h, const LrParams& P, int64_t n, const uint32_t* next,
-                               const uint32_t* len, uint32_t* pre, int level, bool dbg) {
+// Weighted prefix of a tile-ordered list (levels >= 2 of the contraction):
+// pre[i] = sum of len over the nodes before i on its list. Each level
+// contracts by tiles; the top (<= one tile) is ranked by the same kernel as
+// a single tile, whose segments are then whole lists. No host round trip:
+// node counts stay on the device and each grid is sized for contraction of
+// at least 3x per level (3.6-4x is typical on locally numbered tours); a level that needs more tiles, or a
+// top with more than one tile, raises `overflow` and the caller falls back
+// to list_prefix. Returns false on overflow.
+static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* S, const uint32_t* seg1,
+                               const uint32_t* tail1, const uint32_t* len1, uint32_t* pre1,
+                               bool dbg) {
   const cudaStream_t s = h.stream;
-  if (n <= 8192 || level >= WS_TL_LAST - WS_TL2 + 2) {
-    list_prefix(h, P, n, next, len, pre, 0, false, nullptr);
-    return;
+  constexpr int kMaxLevels = WS_TL_LAST - WS_TL2;
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h.dev_box) + 64;  // [64, 64 + L]
+  int* overflow = reinterpret_cast<int*>(h.dev_box + 80);
+  // level l: its nodes are the segments of level l - 1 (level 0: of the
+  // arcs); node i's successor is seg_in[succ_in[tail[i]]]
+  struct Level {
+    const uint32_t* tail;
+    const uint32_t* succ_in;
+    const uint32_t* seg_in;
+    const uint32_t* len;
+    uint32_t* pre;
+    uint32_t* next;  // (written by this level's kernel)
+    uint32_t* seg;   // up-mapping of this level's nodes
+    uint32_t* off;
+    int64_t bound;   // node-count bound (grid sizing)
+  } L[kMaxLevels + 2];
+  L[0] = Level{tail1, S, seg1, len1, pre1, nullptr, nullptr, nullptr, R};
+  int top = 0;
+  for (;;) {
+    const int64_t b = L[top].bound;
+    size_t cap = kLevelNodes;
+    while ((int64_t)cap < b) cap <<= 1;  // stable across builds
+    uint32_t* a = h.ws<uint32_t>(WS_TL2 + top, 6 * cap);
+    L[top].seg = a;
+    L[top].off = a + cap;
+    L[top].next = a + 2 * cap;
+    if (b <= kLevelNodes) break;
+    if (top == kMaxLevels - 1) return false;
+    // the next level's nodes: at most a third of these (bound; 3.6-4x is
+    // typical), else overflow
+    L[top + 1] = Level{a + 3 * cap, L[top].next, L[top].seg, a + 4 * cap, a + 5 * cap,
+                       nullptr, nullptr, nullptr, std::max<int64_t>((b + 2) / 3, 1)};
+    ++top;
   }
-  // arena of this level: up-mapping of the n nodes (seg, off) and the
-  // next level's nodes (len, tail, next, pre) -- at most n of them
-  size_t cap = 1;
-  while (cap < (size_t)n) cap <<= 1;  // grow-only and stable across builds
-  uint32_t* a = h.ws<uint32_t>(WS_TL2 + level - 2, 6 * cap);
-  uint32_t* seg = a;
-  uint32_t* off = a + cap;
-  uint32_t* len2 = a + 2 * cap;
-  uint32_t* tail2 = a + 3 * cap;
-  uint32_t* next2 = a + 4 * cap;
-  uint32_t* pre2 = a + 5 * cap;
-  const unsigned tiles = (unsigned)((n + kLevelNodes - 1) / kLevelNodes);
-  unsigned long long* state = h.ws<unsigned long long>(WS_TSTATE, (size_t)tiles + 1);
-  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h.dev_box) + 8;
-  CK(cudaMemsetAsync(state, 0, ((size_t)tiles + 1) * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(cnt, 0, (top + 2) * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(overflow, 0, sizeof(int), s));
   static bool attr = false;
   constexpr size_t smem = tile_rank_w_smem<kLevelNodes>();
   set_smem(k_tile_rank_w<kLevelNodes, kLevelThreads>, smem, attr);
-  k_tile_rank_w<kLevelNodes, kLevelThreads><<<tiles, kLevelThreads, smem, s>>>(
-      (uint32_t)n, next, len, seg, off, len2, tail2, cnt, state);
-  k_seg_link<<<grid_for(n / 4 + 1), kBlock, 0, s>>>(cnt, tail2, next, seg, next2);
-  CK_LAUNCH();
-  h.read_box(h.dev_box + 8, 1);
-  const int64_t n2 = h.host_box[0];
-  if (dbg) fprintf(stderr, "lr.tiles level %d: %lld -> %lld\n", level, (long long)n, (long long)n2);
-  if (n2 * 2 > n)  // contraction stalled: rank the segments by ruling sets
-    list_prefix(h, P, n2, next2, len2, pre2, 0, false, nullptr);
-  else
-    tile_prefix_levels(h, P, n2, next2, len2, pre2, level + 1, dbg);
-  k_tile_expand<<<grid_for(n), kBlock, 0, s>>>(n, seg, off, pre2, pre);
-  CK_LAUNCH();
+  k_set_count<<<1, 1, 0, s>>>(cnt, (unsigned long long)R);
+  for (int l = 0; l <= top; ++l) {
+    const bool is_top = l == top;
+    const unsigned tiles = is_top ? 1u : (unsigned)((L[l].bound + kLevelNodes - 1) / kLevelNodes);
+    unsigned long long* state = h.ws<unsigned long long>(WS_TSTATE, (size_t)tiles + 1);
+    CK(cudaMemsetAsync(state, 0, ((size_t)tiles + 1) * sizeof(unsigned long long), s));
+    // the top is one tile: its segments are whole lists and its offsets
+    // the prefixes; its segment outputs go to scratch
+    uint32_t* scratch = h.ws<uint32_t>(WS_RA, 4 * (size_t)kLevelNodes);
+    k_tile_rank_w<kLevelNodes, kLevelThreads><<<tiles, kLevelThreads, smem, s>>>(
+        cnt + l, L[l].tail, L[l].succ_in, L[l].seg_in, L[l].next, L[l].len,
+        is_top ? scratch : L[l].seg, is_top ? L[l].pre : L[l].off,
+        is_top ? scratch + kLevelNodes : const_cast<uint32_t*>(L[l + 1].len),
+        is_top ? scratch + 2 * kLevelNodes : const_cast<uint32_t*>(L[l + 1].tail), cnt + l + 1,
+        state, overflow);
+    CK_LAUNCH();
+  }
+  for (int l = top - 1; l >= 0; --l) {
+    k_tile_expand<<<grid_for(L[l].bound), kBlock, 0, s>>>(cnt + l, L[l].seg, L[l].off,
+                                                          L[l + 1].pre, L[l].pre);
+    CK_LAUNCH();
+  }
+  h.read_box(h.dev_box + 64, 17);  // counts [64..], overflow [80]
+  if (dbg) {
+    for (int l = 0; l <= top; ++l)
+      fprintf(stderr, "lr.tiles level %d: %lld nodes\n", l + 2, (long long)h.host_box[l]);
+  }
+  return *reinterpret_cast<int*>(&h.host_box[16]) == 0;
 }
 
 TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* S,
@@ -508,7 +568,6 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
     launch(k_tile_rank<8192, 512>, 512, tile_rank_smem<8192>(), 2);
   else
     launch(k_tile_rank<8192, 1024>, 1024, tile_rank_smem<8192>(), 3);
-  k_seg_link<<<grid_for(E / 8 + 1), kBlock, 0, s>>>(nseg, seg_tail, S, seg, seg_next);
   CK_LAUNCH();
   h.stats.step(E, 2);
   h.read_box(h.dev_box + 8, 8);  // [8] segments, [14] arcs walked, [15] jump rounds
@@ -526,10 +585,12 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   LrParams Q = P;
   Q.cap = std::max<int64_t>(P.cap, E + 1);  // (level arenas sized by the fixed bound)
   static const int levels_env = env_int("RSTG_LR_TILELEVELS", 1);
-  if (levels_env && R * 4 <= E)
-    tile_prefix_levels(h, Q, R, seg_next, seg_len, segstart, 2, dbg);
-  else
+  if (!(levels_env && R * 4 <= E &&
+        tile_prefix_levels(h, R, S, seg, seg_tail, seg_len, segstart, dbg))) {
+    k_seg_link<<<grid_for(R), kBlock, 0, s>>>(nseg, seg_tail, S, seg, seg_next);
+    CK_LAUNCH();
     list_prefix(h, Q, R, seg_next, seg_len, segstart, 0, false, nullptr);
+  }
   const int64_t launches = h.stats.launches;
   h.stats = before;
   h.stats.launches = launches;

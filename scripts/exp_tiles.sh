@@ -1,6 +1,6 @@
 # tile-contraction ranking vs the ruling-set walk (RSTG_LR_TILES, RSTG_LR_TILESLOTS)
 O=gpurun_out; mkdir -p $O
-timeout 1200 python -m pytest tests/ -x -q -m gpu -p no:cacheprovider > $O/pytest_full.log 2>&1; tail -3 $O/pytest_full.log
+timeout 1200 python -m pytest tests/ -x -q -m gpu -k "not full_size" -p no:cacheprovider > $O/pytest_full.log 2>&1; tail -3 $O/pytest_full.log
 run() { # tag env...
   tag=$1; shift
   for W in ${WORKLOADS:-road rmat24 path grid}; do
@@ -8,4 +8,5 @@ run() { # tag env...
     python -c "import json;d=json.load(open('$O/b_${W}_$tag.json'));print('$tag $W', round(d['ms_per_step'],3), d['valid'], {k:v[0] for k,v in d['phases_ms_per_step'].items() if k.startswith('lr') or k.startswith('euler')})" || tail -3 $O/b_${W}_$tag.err
   done
 }
+RSTG_LR_DEBUG=1 python bench.py --workload road --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-bfs-ratio 2>&1 >/dev/null | grep level | head -8
 run auto RSTG_NOTHING=1

@@ -54,9 +54,14 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long
 // Publishes the tile's count as soon as it is known (before the walks), so
 // that by the time the tile needs its prefix the tiles before it have
 // mostly published theirs.
+__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void tile_publish(unsigned long long* state, uint32_t tile,
                                              uint32_t count) {
-  atomicExch(&state[1 + tile], (tile == 0 ? kLbInc : kLbAgg) | count);
+  // (a store, not an atomic: the flag and value are one word, and nothing
+  // waits on a returned value)
+  st_relaxed_gpu(&state[1 + tile], (tile == 0 ? kLbInc : kLbAgg) | count);
 }
 __device__ __forceinline__ uint32_t tile_prefix(unsigned long long* state, uint32_t tile,
                                                 uint32_t count) {
@@ -70,7 +75,7 @@ __device__ __forceinline__ uint32_t tile_prefix(unsigned long long* state, uint3
     if ((v >> 62) == 2) break;
     --p;
   }
-  atomicExch(&st[tile], kLbInc | (excl + count));
+  st_relaxed_gpu(&st[tile], kLbInc | (excl + count));
   return (uint32_t)excl;
 }
 
@@ -89,11 +94,11 @@ constexpr int tile_rank_blocks() {
 
 // Local arc index: slot j of the tile -> arc j (t0 + j) and kSlots + j
 // (N + t0 + j). All index math is 32-bit: arcs are u32 (2N < 2^32).
-template <int kSlots, int kThreads>
+template <int kSlots, int kThreads, int kStride>
 __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>())
     k_tile_rank(uint32_t N, const uint32_t* __restrict__ S, const int32_t* __restrict__ lab,
                 bool cc_slots, uint32_t T, uint32_t* __restrict__ seg, uint16_t* __restrict__ off,
-                uint32_t* __restrict__ seg_len, uint32_t* __restrict__ seg_tail,
+                uint32_t* __restrict__ seg_len, uint32_t* __restrict__ seg_exit,
                 unsigned long long* nseg, unsigned long long* state,
                 unsigned long long* walked) {
   static_assert(2 * kSlots <= kTileExit, "local arc index must fit 15 bits");
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
   for (int q = 0; q < kOwn; ++q) {
     const uint32_t li = local_of(q);
     const bool head = (vmask >> q & 1) && !haspred[li];
-    const bool ruler = head || ((vmask >> q & 1) && q == (int)(tid % kOwn));
+    const bool ruler = head || ((vmask >> q & 1) && q % kStride == (int)(tid % kStride));
     hmask |= head ? 1u << q : 0u;
     rmask |= ruler ? 1u << q : 0u;
     if (ruler) nx[li] |= kTileRuler;
@@ -238,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
     __stcs(&off[x], (uint16_t)o);
     if (tmask >> q & 1) {
       seg_len[sid] = o + 1;
-      seg_tail[sid] = x;
+      seg_exit[sid] = __ldg(&S[x]);  // the next segment's head (or NONE)
     }
   }
   if (walked) {
@@ -262,14 +267,13 @@ constexpr size_t tile_rank_w_smem() {
   return kNodes * (sizeof(unsigned long long) + sizeof(uint16_t) + sizeof(uint8_t));
 }
 
-template <int kNodes, int kThreads>
+template <int kNodes, int kThreads, int kStride>
 __global__ void __launch_bounds__(kThreads)
-    k_tile_rank_w(const unsigned long long* n_dev, const uint32_t* __restrict__ tail_in,
-                  const uint32_t* __restrict__ succ_in, const uint32_t* __restrict__ seg_in,
-                  uint32_t* __restrict__ next_out, const uint32_t* __restrict__ w,
+    k_tile_rank_w(const unsigned long long* n_dev, const uint32_t* __restrict__ exit_in,
+                  const uint32_t* __restrict__ seg_in, const uint32_t* __restrict__ w,
                   uint32_t* __restrict__ seg,
                   uint32_t* __restrict__ off, uint32_t* __restrict__ seg_len,
-                  uint32_t* __restrict__ seg_tail, unsigned long long* nseg,
+                  uint32_t* __restrict__ seg_exit, unsigned long long* nseg,
                   unsigned long long* state, int* overflow) {
   static_assert(kNodes <= kTileExit, "local node index must fit 15 bits");
   constexpr int kPer = kNodes / kThreads;
@@ -300,22 +304,17 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t cnt = min((uint32_t)kNodes, n - t0);
   const uint32_t last = n - 1;
   // successor of node i (a segment of the level below): the segment
-  // headed by the successor of its last element, next = seg_in[succ_in[tail_in[i]]]
-  // (computed here, not by a separate pass, and kept for the level above)
+  // headed by the element after its last one, next = seg_in[exit_in[i]]
+  // (computed here, not by a separate pass)
   uint32_t y[kPer], wt[kPer];
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     const uint32_t i = min(t0 + tid + k * kThreads, last);
-    y[k] = __ldcs(&tail_in[i]);
+    y[k] = __ldcs(&exit_in[i]);
     wt[k] = __ldcs(&w[i]);
   }
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) y[k] = succ_in[y[k]];
-#pragma unroll
   for (int k = 0; k < kPer; ++k) y[k] = y[k] == kNone32 ? kNone32 : seg_in[y[k]];
-#pragma unroll
-  for (int k = 0; k < kPer; ++k)
-    if (tid + k * kThreads < cnt) __stcs(&next_out[t0 + tid + k * kThreads], y[k]);
   uint32_t vmask = 0, tmask = 0;
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
@@ -334,7 +333,7 @@ __global__ void __launch_bounds__(kThreads)
   for (int k = 0; k < kPer; ++k) {
     const uint32_t j = tid + k * kThreads;
     const bool head = (vmask >> k & 1) && !haspred[j];
-    const bool ruler = head || ((vmask >> k & 1) && k == (int)(tid % kPer));
+    const bool ruler = head || ((vmask >> k & 1) && k % kStride == (int)(tid % kStride));
     hmask |= head ? 1u << k : 0u;
     rmask |= ruler ? 1u << k : 0u;
     if (ruler) nx[j] |= kTileRuler;
@@ -405,19 +404,18 @@ __global__ void __launch_bounds__(kThreads)
     __stcs(&off[t0 + j], o);
     if (tmask >> k & 1) {
       seg_len[sid] = o + wt[k];
-      seg_tail[sid] = t0 + j;
+      seg_exit[sid] = y[k];  // this level's node after the segment (or NONE)
     }
   }
 }
 
-// next segment of each segment: the one headed by its tail's successor
-__global__ void k_seg_link(const unsigned long long* nseg, const uint32_t* __restrict__ seg_tail,
-                           const uint32_t* __restrict__ S, const uint32_t* __restrict__ seg,
-                           uint32_t* __restrict__ seg_next) {
+// next segment of each segment: the one its exit arc heads
+__global__ void k_seg_link(const unsigned long long* nseg, const uint32_t* __restrict__ seg_exit,
+                           const uint32_t* __restrict__ seg, uint32_t* __restrict__ seg_next) {
   const int64_t R = (int64_t)*nseg;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t ex = S[seg_tail[i]];
+    const uint32_t ex = seg_exit[i];
     seg_next[i] = ex == kNone32 ? kNone32 : seg[ex];
   }
 }
@@ -458,49 +456,51 @@ constexpr int kLevelThreads = 1024;
 // at least 3x per level (3.6-4x is typical on locally numbered tours); a level that needs more tiles, or a
 // top with more than one tile, raises `overflow` and the caller falls back
 // to list_prefix. Returns false on overflow.
-static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* S, const uint32_t* seg1,
-                               const uint32_t* tail1, const uint32_t* len1, uint32_t* pre1,
+static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
+                               const uint32_t* exit1, const uint32_t* len1, uint32_t* pre1,
                                bool dbg) {
   const cudaStream_t s = h.stream;
   constexpr int kMaxLevels = WS_TL_LAST - WS_TL2;
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h.dev_box) + 64;  // [64, 64 + L]
   int* overflow = reinterpret_cast<int*>(h.dev_box + 80);
   // level l: its nodes are the segments of level l - 1 (level 0: of the
-  // arcs); node i's successor is seg_in[succ_in[tail[i]]]
+  // arcs); node i's successor is seg_in[exit[i]], exit[i] the element of
+  // level l - 1 after its last one
   struct Level {
-    const uint32_t* tail;
-    const uint32_t* succ_in;
+    const uint32_t* exit;
     const uint32_t* seg_in;
     const uint32_t* len;
     uint32_t* pre;
-    uint32_t* next;  // (written by this level's kernel)
-    uint32_t* seg;   // up-mapping of this level's nodes
+    uint32_t* seg;  // up-mapping of this level's nodes
     uint32_t* off;
-    int64_t bound;   // node-count bound (grid sizing)
+    int64_t bound;  // node-count bound (grid sizing)
   } L[kMaxLevels + 2];
-  L[0] = Level{tail1, S, seg1, len1, pre1, nullptr, nullptr, nullptr, R};
+  L[0] = Level{exit1, seg1, len1, pre1, nullptr, nullptr, R};
   int top = 0;
   for (;;) {
     const int64_t b = L[top].bound;
     size_t cap = kLevelNodes;
     while ((int64_t)cap < b) cap <<= 1;  // stable across builds
-    uint32_t* a = h.ws<uint32_t>(WS_TL2 + top, 6 * cap);
+    uint32_t* a = h.ws<uint32_t>(WS_TL2 + top, 5 * cap);
     L[top].seg = a;
     L[top].off = a + cap;
-    L[top].next = a + 2 * cap;
     if (b <= kLevelNodes) break;
     if (top == kMaxLevels - 1) return false;
     // the next level's nodes: at most a third of these (bound; 3.6-4x is
     // typical), else overflow
-    L[top + 1] = Level{a + 3 * cap, L[top].next, L[top].seg, a + 4 * cap, a + 5 * cap,
-                       nullptr, nullptr, nullptr, std::max<int64_t>((b + 2) / 3, 1)};
+    L[top + 1] = Level{a + 2 * cap, L[top].seg, a + 3 * cap, a + 4 * cap, nullptr, nullptr,
+                       std::max<int64_t>((b + 2) / 3, 1)};
     ++top;
   }
   CK(cudaMemsetAsync(cnt, 0, (top + 2) * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(overflow, 0, sizeof(int), s));
-  static bool attr = false;
+  static const int wstride = env_int("RSTG_LR_WSTRIDE", 4);
   constexpr size_t smem = tile_rank_w_smem<kLevelNodes>();
-  set_smem(k_tile_rank_w<kLevelNodes, kLevelThreads>, smem, attr);
+  auto kern = wstride >= 8   ? k_tile_rank_w<kLevelNodes, kLevelThreads, 8>
+              : wstride >= 4 ? k_tile_rank_w<kLevelNodes, kLevelThreads, 4>
+                             : k_tile_rank_w<kLevelNodes, kLevelThreads, 2>;
+  static bool attr = false;
+  set_smem(kern, smem, attr);
   k_set_count<<<1, 1, 0, s>>>(cnt, (unsigned long long)R);
   for (int l = 0; l <= top; ++l) {
     const bool is_top = l == top;
@@ -510,11 +510,11 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* S, const ui
     // the top is one tile: its segments are whole lists and its offsets
     // the prefixes; its segment outputs go to scratch
     uint32_t* scratch = h.ws<uint32_t>(WS_RA, 4 * (size_t)kLevelNodes);
-    k_tile_rank_w<kLevelNodes, kLevelThreads><<<tiles, kLevelThreads, smem, s>>>(
-        cnt + l, L[l].tail, L[l].succ_in, L[l].seg_in, L[l].next, L[l].len,
-        is_top ? scratch : L[l].seg, is_top ? L[l].pre : L[l].off,
+    kern<<<tiles, kLevelThreads, smem, s>>>(
+        cnt + l, L[l].exit, L[l].seg_in, L[l].len, is_top ? scratch : L[l].seg,
+        is_top ? L[l].pre : L[l].off,
         is_top ? scratch + kLevelNodes : const_cast<uint32_t*>(L[l + 1].len),
-        is_top ? scratch + 2 * kLevelNodes : const_cast<uint32_t*>(L[l + 1].tail), cnt + l + 1,
+        is_top ? scratch + 2 * kLevelNodes : const_cast<uint32_t*>(L[l + 1].exit), cnt + l + 1,
         state, overflow);
     CK_LAUNCH();
   }
@@ -539,13 +539,12 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   uint16_t* off = h.ws<uint16_t>(WS_TOFF, E);
   // segments <= arcs: sized by E (a fixed bound: no reallocation per build)
   uint32_t* seg_len = h.ws<uint32_t>(WS_RLEN, E + 1);
-  uint32_t* seg_tail = h.ws<uint32_t>(WS_RNEXT, E + 1);
+  uint32_t* seg_exit = h.ws<uint32_t>(WS_RNEXT, E + 1);
   uint32_t* seg_next = h.ws<uint32_t>(WS_RPOS, E + 1);
   uint32_t* segstart = h.ws<uint32_t>(WS_RD, E + 1);
   unsigned long long* nseg = reinterpret_cast<unsigned long long*>(h.dev_box) + 8;
   unsigned long long* walked = reinterpret_cast<unsigned long long*>(h.dev_box) + 14;
   static const int slots_env = env_int("RSTG_LR_TILESLOTS", 8192);
-  static const int tile_threads_env = env_int("RSTG_LR_TILETHREADS", 1024);
   static const bool dbg = getenv("RSTG_LR_DEBUG") != nullptr;
   const int slots = slots_env <= 2048 ? 2048 : slots_env <= 4096 ? 4096 : 8192;
   const unsigned tiles = (unsigned)((N + slots - 1) / slots);
@@ -554,20 +553,23 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   CK(cudaMemsetAsync(state, 0, ((size_t)tiles + 1) * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(h.dev_box + 14, 0, 2 * sizeof(int64_t), s));
   auto launch = [&](auto kern, int threads, size_t smem, int a) {
-    static bool attr[4] = {false, false, false, false};
+    static bool attr[5] = {false, false, false, false, false};
     set_smem(kern, smem, attr[a]);
     kern<<<tiles, threads, smem, s>>>((uint32_t)N, S, lab, cc_slots, (uint32_t)T, seg, off,
-                                      seg_len, seg_tail, nseg, state,
+                                      seg_len, seg_exit, nseg, state,
                                       verify || dbg ? walked : nullptr);
   };
+  static const int stride1 = env_int("RSTG_LR_STRIDE", 16);
   if (slots == 2048)
-    launch(k_tile_rank<2048, 256>, 256, tile_rank_smem<2048>(), 0);
+    launch(k_tile_rank<2048, 256, 16>, 256, tile_rank_smem<2048>(), 0);
   else if (slots == 4096)
-    launch(k_tile_rank<4096, 512>, 512, tile_rank_smem<4096>(), 1);
-  else if (tile_threads_env <= 512)
-    launch(k_tile_rank<8192, 512>, 512, tile_rank_smem<8192>(), 2);
+    launch(k_tile_rank<4096, 512, 16>, 512, tile_rank_smem<4096>(), 1);
+  else if (stride1 <= 4)
+    launch(k_tile_rank<8192, 1024, 4>, 1024, tile_rank_smem<8192>(), 2);
+  else if (stride1 <= 8)
+    launch(k_tile_rank<8192, 1024, 8>, 1024, tile_rank_smem<8192>(), 3);
   else
-    launch(k_tile_rank<8192, 1024>, 1024, tile_rank_smem<8192>(), 3);
+    launch(k_tile_rank<8192, 1024, 16>, 1024, tile_rank_smem<8192>(), 4);
   CK_LAUNCH();
   h.stats.step(E, 2);
   h.read_box(h.dev_box + 8, 8);  // [8] segments, [14] arcs walked, [15] jump rounds
@@ -584,10 +586,10 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   const Stats before = h.stats;
   LrParams Q = P;
   Q.cap = std::max<int64_t>(P.cap, E + 1);  // (level arenas sized by the fixed bound)
-  static const int levels_env = env_int("RSTG_LR_TILELEVELS", 1);
+  const int levels_env = env_int("RSTG_LR_TILELEVELS", 1);  // (0: segments by list_prefix)
   if (!(levels_env && R * 4 <= E &&
-        tile_prefix_levels(h, R, S, seg, seg_tail, seg_len, segstart, dbg))) {
-    k_seg_link<<<grid_for(R), kBlock, 0, s>>>(nseg, seg_tail, S, seg, seg_next);
+        tile_prefix_levels(h, R, seg, seg_exit, seg_len, segstart, dbg))) {
+    k_seg_link<<<grid_for(R), kBlock, 0, s>>>(nseg, seg_exit, seg, seg_next);
     CK_LAUNCH();
     list_prefix(h, Q, R, seg_next, seg_len, segstart, 0, false, nullptr);
   }

@@ -8,5 +8,5 @@ run() { # tag env...
     python -c "import json;d=json.load(open('$O/b_${W}_$tag.json'));print('$tag $W', round(d['ms_per_step'],3), d['valid'], {k:v[0] for k,v in d['phases_ms_per_step'].items() if k.startswith('lr') or k.startswith('euler')})" || tail -3 $O/b_${W}_$tag.err
   done
 }
-RSTG_LR_DEBUG=1 python bench.py --workload road --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-bfs-ratio 2>&1 >/dev/null | grep level | head -8
+RSTG_LR_DEBUG=1 python bench.py --workload road --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-bfs-ratio 2>&1 >/dev/null | grep "tile0" | tail -7
 run auto RSTG_NOTHING=1

@@ -367,8 +367,9 @@ _WALK_KNOBS = [{"RSTG_LR_LOGK0": "1"}, {"RSTG_LR_LOGK0": "7"}, {"RSTG_LR_BLOCKS"
                {"RSTG_LR_WALKCAP": "4"}, {"RSTG_LR_WALKCAP": "17", "RSTG_LR_LOGK0": "6"}]
 # the ruling-set walk (RSTG_LR_TILES=0) and tile contraction with its knobs
 LR_KNOBS = ([dict(k, RSTG_LR_TILES="0") for k in _WALK_KNOBS] +
-            [{"RSTG_LR_TILES": "1"}, {"RSTG_LR_TILES": "1", "RSTG_LR_LOGK1": "1"},
-             {"RSTG_LR_TILES": "1", "RSTG_LR_LOGK1": "6"}])
+            [{"RSTG_LR_TILES": "1"}, {"RSTG_LR_TILES": "1", "RSTG_LR_TILELEVELS": "0"},
+             {"RSTG_LR_TILES": "1", "RSTG_LR_TILELEVELS": "0", "RSTG_LR_LOGK1": "1"},
+             {"RSTG_LR_TILES": "1", "RSTG_LR_TILELEVELS": "0", "RSTG_LR_LOGK1": "6"}])
 
 
 @pytest.mark.parametrize("spec,root", [(("road", 300), 0), (("kron", 14), None), (("path", 5000), 77),

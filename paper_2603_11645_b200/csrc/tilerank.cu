@@ -420,8 +420,6 @@ __global__ void k_seg_link(const unsigned long long* nseg, const uint32_t* __res
   }
 }
 
-__global__ void k_set_count(unsigned long long* c, unsigned long long v) { *c = v; }
-
 // pre[i] = pre_up[seg[i]] + off[i] over the n_dev nodes of a level
 __global__ void k_tile_expand(const unsigned long long* n_dev, const uint32_t* __restrict__ seg,
                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ pre_up,
@@ -461,8 +459,6 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
                                bool dbg) {
   const cudaStream_t s = h.stream;
   constexpr int kMaxLevels = WS_TL_LAST - WS_TL2;
-  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h.dev_box) + 64;  // [64, 64 + L]
-  int* overflow = reinterpret_cast<int*>(h.dev_box + 80);
   // level l: its nodes are the segments of level l - 1 (level 0: of the
   // arcs); node i's successor is seg_in[exit[i]], exit[i] the element of
   // level l - 1 after its last one
@@ -492,8 +488,17 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
                        std::max<int64_t>((b + 2) / 3, 1)};
     ++top;
   }
-  CK(cudaMemsetAsync(cnt, 0, (top + 2) * sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(overflow, 0, sizeof(int), s));
+  // one control block, zeroed by one memset: node counts [0, 16) (count 0 =
+  // the segment count the level-1 kernel left in dev_box[8], copied), the
+  // overflow flag [16], then each level's tile counter + look-back states
+  size_t words = 32;
+  for (int l = 0; l <= top; ++l)
+    words += (l == top ? 1 : (L[l].bound + kLevelNodes - 1) / kLevelNodes) + 1;
+  unsigned long long* blk = h.ws<unsigned long long>(WS_TL_LAST, words);
+  unsigned long long* cnt = blk;
+  int* overflow = reinterpret_cast<int*>(blk + 16);
+  CK(cudaMemsetAsync(blk, 0, words * sizeof(unsigned long long), s));
+  CK(cudaMemcpyAsync(cnt, h.dev_box + 8, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
   static const int wstride = env_int("RSTG_LR_WSTRIDE", 4);
   constexpr size_t smem = tile_rank_w_smem<kLevelNodes>();
   auto kern = wstride >= 8   ? k_tile_rank_w<kLevelNodes, kLevelThreads, 8>
@@ -501,12 +506,10 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
                              : k_tile_rank_w<kLevelNodes, kLevelThreads, 2>;
   static bool attr = false;
   set_smem(kern, smem, attr);
-  k_set_count<<<1, 1, 0, s>>>(cnt, (unsigned long long)R);
+  unsigned long long* state = blk + 32;
   for (int l = 0; l <= top; ++l) {
     const bool is_top = l == top;
     const unsigned tiles = is_top ? 1u : (unsigned)((L[l].bound + kLevelNodes - 1) / kLevelNodes);
-    unsigned long long* state = h.ws<unsigned long long>(WS_TSTATE, (size_t)tiles + 1);
-    CK(cudaMemsetAsync(state, 0, ((size_t)tiles + 1) * sizeof(unsigned long long), s));
     // the top is one tile: its segments are whole lists and its offsets
     // the prefixes; its segment outputs go to scratch
     uint32_t* scratch = h.ws<uint32_t>(WS_RA, 4 * (size_t)kLevelNodes);
@@ -517,13 +520,14 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
         is_top ? scratch + 2 * kLevelNodes : const_cast<uint32_t*>(L[l + 1].exit), cnt + l + 1,
         state, overflow);
     CK_LAUNCH();
+    state += tiles + 1;
   }
   for (int l = top - 1; l >= 0; --l) {
     k_tile_expand<<<grid_for(L[l].bound), kBlock, 0, s>>>(cnt + l, L[l].seg, L[l].off,
                                                           L[l + 1].pre, L[l].pre);
     CK_LAUNCH();
   }
-  h.read_box(h.dev_box + 64, 17);  // counts [64..], overflow [80]
+  h.read_box(reinterpret_cast<int64_t*>(blk), 17);  // counts, overflow
   if (dbg) {
     for (int l = 0; l <= top; ++l)
       fprintf(stderr, "lr.tiles level %d: %lld nodes\n", l + 2, (long long)h.host_box[l]);
@@ -551,7 +555,7 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   unsigned long long* state = h.ws<unsigned long long>(WS_TSTATE, (size_t)tiles + 1);
   h.timer.begin(s, "lr.tiles", 12.0 * E);  // succ read + segment id + offset per arc
   CK(cudaMemsetAsync(state, 0, ((size_t)tiles + 1) * sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(h.dev_box + 14, 0, 2 * sizeof(int64_t), s));
+  if (verify || dbg) CK(cudaMemsetAsync(h.dev_box + 14, 0, 2 * sizeof(int64_t), s));
   auto launch = [&](auto kern, int threads, size_t smem, int a) {
     static bool attr[5] = {false, false, false, false, false};
     set_smem(kern, smem, attr[a]);

@@ -268,7 +268,7 @@ constexpr size_t tile_rank_w_smem() {
 }
 
 template <int kNodes, int kThreads, int kStride>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2048 / kThreads)
     k_tile_rank_w(const unsigned long long* n_dev, const uint32_t* __restrict__ exit_in,
                   const uint32_t* __restrict__ seg_in, const uint32_t* __restrict__ w,
                   uint32_t* __restrict__ seg,

@@ -472,6 +472,7 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
     int64_t bound;  // node-count bound (grid sizing)
   } L[kMaxLevels + 2];
   L[0] = Level{exit1, seg1, len1, pre1, nullptr, nullptr, R};
+  const int contract = std::max(2, env_int("RSTG_LR_TILECONTRACT", 3));
   int top = 0;
   for (;;) {
     const int64_t b = L[top].bound;
@@ -483,9 +484,10 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
     if (b <= kLevelNodes) break;
     if (top == kMaxLevels - 1) return false;
     // the next level's nodes: at most a third of these (bound; 3.6-4x is
-    // typical), else overflow
+    // typical), else overflow (RSTG_LR_TILECONTRACT overrides the factor:
+    // the tests force the fallback with a large one)
     L[top + 1] = Level{a + 2 * cap, L[top].seg, a + 3 * cap, a + 4 * cap, nullptr, nullptr,
-                       std::max<int64_t>((b + 2) / 3, 1)};
+                       std::max<int64_t>((b + contract - 1) / contract, 1)};
     ++top;
   }
   // one control block, zeroed by one memset: node counts [0, 16) (count 0 =

@@ -401,6 +401,27 @@ def test_list_rank_knobs_invariant(rst, O, spec, root, monkeypatch):
     dg.close()
 
 
+def test_tile_levels_overflow_fallback(rst, monkeypatch):
+    # tile-contraction levels sized for an impossible contraction: the top
+    # tile overflows (a 9M-vertex mesh leaves far more than 8192 segments)
+    # and the ranking falls back to list_prefix on the level-1 segments --
+    # the same parents as the ruling-set walk (itself pinned to the oracle
+    # in the other tests)
+    g = rst.DeviceGraph.generate("road:3000")
+    out = {}
+    for tag, knobs in (("walk", {"RSTG_LR_TILES": "0"}),
+                       ("tiles", {"RSTG_LR_TILES": "1"}),
+                       ("overflow", {"RSTG_LR_TILES": "1", "RSTG_LR_TILECONTRACT": "1000000"})):
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        out[tag] = g.run(1, 7)[0]
+        for k in knobs:
+            monkeypatch.delenv(k)
+    assert np.array_equal(out["tiles"], out["walk"])
+    assert np.array_equal(out["overflow"], out["walk"])
+    g.close()
+
+
 def test_step_counts_rerun_identical(rst, O):
     # acceptance.cpp:330-363 (criterion 7): parents, steps and work are
     # bit-identical across reruns -- with the CSR given or built on the

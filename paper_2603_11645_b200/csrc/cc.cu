@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // cc.cu -- exact GConn-style connectivity: edge-parallel hooking with
 // spanning-edge capture + pointer-jumping shortcutting.
 //
@@ -505,6 +507,12 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
   k_final_gather<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
   CK_LAUNCH();
   h.stats.step(n);
+  static const bool dbg = getenv("RSTG_CC_DEBUG") != nullptr;
+  if (dbg) {
+    h.read_box(h.dev_box + 5, 1);
+    fprintf(stderr, "resolve_round src %d: n %lld, exit set %lld\n", src, (long long)n,
+            (long long)h.host_box[0]);
+  }
 }
 
 // Compression after lazy rounds: every pointer chain runs through former

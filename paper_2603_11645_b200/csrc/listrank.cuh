@@ -100,8 +100,9 @@ void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t* next, 
 
 // Tile-contracted ranking of the Euler tour (tilerank.cu): each CTA ranks
 // the arcs of a tile of consecutive slots on chip (maximal runs of tour
-// successors inside the tile = segments), then the segment list is ranked
-// by list_prefix. rank(x) = segstart[seg[x]] + off[x].
+// successors inside the tile = segments, numbered in tile order), then the
+// segment list is contracted by tiles again, level after level (list_prefix
+// when that stalls). rank(x) = segstart[seg[x]] + off[x].
 struct TileRank {
   const uint32_t* seg;       // 2N segment id per arc
   const uint16_t* off;       // 2N offset within the segment

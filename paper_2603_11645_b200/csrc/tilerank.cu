@@ -14,13 +14,22 @@
 //      arc it passes (ruler << 16 | offset) and the reached ruler's
 //      (predecessor ruler << 16 | distance) -- O(arcs) work, ~16 hops a walk;
 //   3. pointer jumping over the rulers alone (a few hundred per tile)
-//      gives every ruler its head and offset; heads are numbered with one
-//      global atomic per tile; every arc writes (segment, offset), every
-//      segment tail the segment's length and last arc.
+//      gives every ruler its head and offset; the tile publishes its head
+//      count as soon as it is known and takes its first segment id by
+//      decoupled look-back, so segment ids follow the tile order; every
+//      arc writes (segment, offset), every segment its length and exit
+//      (the arc after its last one).
 // The segments form lists again -- one per tour, shorter by the
-// contraction factor -- that list_prefix ranks (recursive ruling sets).
-// A tour that jumps between tiles (random vertex ids) gains little; the
-// caller then keeps the ruling-set walk (listrank.cu).
+// contraction factor, and local again because their ids are in tile order
+// -- so the same contraction is applied to them, weighted by segment
+// length (k_tile_rank_w), level after level until one tile holds a whole
+// list; the prefixes are then expanded back down. No host round trip
+// between levels: counts stay on the device, grids are sized by a bound,
+// and a level that overflows its bound makes the caller fall back to
+// list_prefix (recursive ruling sets, listrank.cu).
+// A tour that jumps between tiles (random vertex ids) gains little: the
+// caller (euler.cu) then keeps the ruling-set walk, chosen per graph from
+// an edge-locality sample.
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>

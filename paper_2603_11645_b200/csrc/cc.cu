@@ -515,6 +515,106 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
   }
 }
 
+// The same jumping for a short list (<= kJumpSmallMax entries: meshes have a
+// few thousand round-0 roots), on chip: one CTA hashes the list's vertices
+// into shared memory, maps each entry's pointer to a list index (one global
+// load per entry), jumps the indices in shared memory and writes the roots
+// back. A pointer that leaves the list (not expected: hooks join roots)
+// stays as it is -- labels stay valid ancestors either way.
+constexpr int kJumpSmallMax = 8192;
+constexpr int kJumpHash = 2 * kJumpSmallMax;
+constexpr size_t kJumpSmallSmem = kJumpHash * (sizeof(uint32_t) + sizeof(uint16_t)) +
+                                  kJumpSmallMax * (sizeof(uint16_t) + sizeof(uint32_t));
+constexpr int kJumpPer = kJumpSmallMax / 1024;
+__global__ void __launch_bounds__(1024)
+    k_jump_small(const uint32_t* __restrict__ list, const unsigned long long* count, int32_t* rep) {
+  extern __shared__ uint32_t hkey[];  // vertex + 1, 0 = empty
+  uint32_t* lst = hkey + kJumpHash;   // the list
+  uint16_t* hval = reinterpret_cast<uint16_t*>(lst + kJumpSmallMax);  // list index
+  uint16_t* par = hval + kJumpHash;  // index of the entry's pointer target
+  const unsigned long long cnt = *count;
+  const int X = cnt < (unsigned long long)kJumpSmallMax ? (int)cnt : kJumpSmallMax;
+  const int tid = threadIdx.x;
+  // every global load of a thread in flight at once: its entries, then
+  // their pointers
+  uint32_t v[kJumpPer], p[kJumpPer];
+#pragma unroll
+  for (int k = 0; k < kJumpPer; ++k) v[k] = tid + k * 1024 < X ? list[tid + k * 1024] : 0u;
+#pragma unroll
+  for (int k = 0; k < kJumpPer; ++k) p[k] = tid + k * 1024 < X ? (uint32_t)ld_cg(&rep[v[k]]) : 0u;
+  for (int h = tid; h < kJumpHash; h += 1024) hkey[h] = 0;
+  __syncthreads();
+  auto slot_of = [](uint32_t x) { return (x * 0x9E3779B1u) >> (32 - 14); };  // 14 bits
+#pragma unroll
+  for (int k = 0; k < kJumpPer; ++k) {
+    const int i = tid + k * 1024;
+    if (i >= X) continue;
+    lst[i] = v[k];
+    for (uint32_t h = slot_of(v[k]);; h = (h + 1) & (kJumpHash - 1)) {
+      const uint32_t key = atomicCAS(&hkey[h], 0u, v[k] + 1);
+      if (key == 0 || key == v[k] + 1) {
+        hval[h] = (uint16_t)i;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kJumpPer; ++k) {
+    const int i = tid + k * 1024;
+    if (i >= X) continue;
+    uint16_t j = (uint16_t)i;  // not in the list: leave the entry alone
+    for (uint32_t h = slot_of(p[k]);; h = (h + 1) & (kJumpHash - 1)) {
+      const uint32_t key = hkey[h];
+      if (key == p[k] + 1) {
+        j = hval[h];
+        break;
+      }
+      if (key == 0) break;
+    }
+    par[i] = j;
+  }
+  __syncthreads();
+  for (int r = 0; r < 32; ++r) {  // in place: an entry always holds an ancestor
+    int changed = 0;
+    for (int i = tid; i < X; i += 1024) {
+      const uint16_t a = par[i], b = par[a];
+      if (a != b) {
+        par[i] = b;
+        changed = 1;
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+#pragma unroll
+  for (int k = 0; k < kJumpPer; ++k) {
+    const int i = tid + k * 1024;
+    if (i >= X) continue;
+    const uint32_t t = lst[par[i]];
+    if (t != v[k] && t != p[k]) rep[v[k]] = (int32_t)t;
+  }
+}
+
+// Pointer-jumps the entries of a vertex list in place (one cooperative
+// launch, device-side stop): the chains among round-0 roots after a lazy round.
+void jump_list(Handle& h, int32_t* rep, int64_t n, const uint32_t* list,
+               const unsigned long long* count) {
+  int* flags = reinterpret_cast<int*>(h.dev_box + 6);  // 3 ints in dev_box[6..7]
+  CK(cudaMemsetAsync(h.dev_box + 6, 0, 2 * sizeof(int64_t), h.stream));
+  static int coop_blocks = 0;
+  if (!coop_blocks) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jump_x, kBlock, 0));
+    coop_blocks = std::max(1, per_sm) * num_sms();
+  }
+  int rounds = 2;
+  while ((int64_t{1} << (rounds - 2)) < n) ++rounds;
+  void* args[] = {(void*)&list, (void*)&count, (void*)&rep, (void*)&flags, (void*)&rounds};
+  CK(cudaLaunchCooperativeKernel((void*)k_jump_x, dim3(coop_blocks), dim3(kBlock), args, 0,
+                                 h.stream));
+  h.stats.step(n);
+}
+
 // Compression after lazy rounds: every pointer chain runs through former
 // roots only (a vertex's first hop lands on a root of some earlier round),
 // so pointer-jumping the round-0 roots list in place (one cooperative
@@ -730,7 +830,11 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
       resolve_round(h, rep, n, kSrcRep, RoundIO{});
   };
   h.cc_lazy = false;  // the first hook sees compressed reps (round 0 compressed, or singletons)
-  int64_t total = 0, last_hooks = 0;
+  static const bool jump_roots = [] {
+    const char* e = getenv("RSTG_CC_JUMP_ROOTS");
+    return e ? atoi(e) != 0 : true;
+  }();
+  int64_t total = 0, last_hooks = 0, prev_total = 0;
   for (;; ++round) {
     if (round > n + 1) {
       h.cc_lazy = false;
@@ -743,9 +847,16 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
                   visited * ((h.cc_round >= 2 && h.cc_active >= 0) ? 20.0 : 16.0));
     cc_hook_round(h, mode, rep, slot, counter + 1, any);
     h.timer.end(h.stream);
-    h.read_box(reinterpret_cast<int64_t*>(counter), 3);  // hooks so far, crossing, any
+    // hooks so far, crossing, any; [20] the round-0 roots count (same read)
+    h.read_box(reinterpret_cast<int64_t*>(counter), 21);
+    const int64_t r0_count = have_r0 ? h.host_box[20] : 0;
+    prev_total = total;
     total = h.host_box[0];
     const bool proposed = h.host_box[2] != 0;
+    if (getenv("RSTG_CC_DEBUG"))
+      fprintf(stderr, "cc round %d mode %d: visited %.0f, hooks so far %lld, crossing %lld, lazy %d, r0 %lld\n",
+              round, mode, visited, (long long)total, (long long)h.host_box[1], (int)h.cc_lazy,
+              (long long)r0_count);
     cc_round_done(h, h.host_box[1]);
     h.stats.rounds = round + 1;
     // a round without proposals applies nothing (cc_forest.cpp:91)
@@ -772,6 +883,30 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
       h.cc_lazy = false;
     } else {
       h.cc_lazy = true;
+      // Hooks of one round chain roots to roots (a winner may itself have
+      // been hooked), so lazy finds would walk those chains from every
+      // active edge. Every chain runs through round-0 roots only: jumping
+      // that list (one cooperative launch, no pass over n) leaves every
+      // vertex at most two hops from its root.
+      // A short list (meshes: a few thousand local minima) is jumped by one
+      // CTA, with block barriers instead of grid barriers.
+      if (have_r0 && jump_roots && total > prev_total) {
+        h.timer.begin(h.stream, "cc.jump_roots", 8.0 * r0_count);
+        if (r0_count <= kJumpSmallMax) {
+          static bool attr = false;
+          if (!attr) {
+            CK(cudaFuncSetAttribute(k_jump_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kJumpSmallSmem));
+            attr = true;
+          }
+          k_jump_small<<<1, 1024, kJumpSmallSmem, h.stream>>>(rl[0], rcount, rep);
+          CK_LAUNCH();
+          h.stats.step(n);
+        } else {
+          jump_list(h, rep, n, rl[0], rcount);
+        }
+        h.timer.end(h.stream);
+      }
     }
     last_hooks = -total;  // completed when the next round reads the hook total
   }

@@ -11,6 +11,7 @@ if [ -z "$SKIP_TESTS" ]; then
   timeout 1200 python -m pytest tests/ -x -q -m gpu -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
   tail -3 $O/pytest_gpu.log
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
+  [ -x build/rst_acceptance ] && timeout 600 ./build/rst_acceptance > $O/acceptance.log 2>&1; tail -1 $O/acceptance.log
 fi
 timeout 900 python bench.py > $O/bench_road.json 2> $O/bench_road.err; cat $O/bench_road.json
 if [ -z "$SKIP_EXTRA" ]; then

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kBlock)
         io.S[arc_rev(t2, io.nslots)] = h2[k];
       }
     }
-    uint32_t id = lr_block_claim(__popc(flags & 0xFFFFu), ctr);
+    uint32_t id = rulers ? lr_block_claim(__popc(flags & 0xFFFFu), ctr) : 0u;
     const uint32_t nl = __popc(flags >> 16);
     uint32_t li = nl ? atomicAdd(&s_nl, nl) : 0u;
     __syncthreads();
@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(kBlock)
         io.S[arc_rev(tl, io.nslots)] = kNone32;  // the tour ends back at the root
       }
     }
-    const bool head = rulers && hd != kNone32 && !lr_hash_ruler(hd, logk);
+    if (!rulers) continue;  // (block-uniform)
+    const bool head = hd != kNone32 && !lr_hash_ruler(hd, logk);
     const uint32_t id = lr_block_claim(head ? 1u : 0u, ctr);
     if (head) lr_put(id, hd, rpos, sl, ob, cap);
   }

@@ -277,7 +277,7 @@ constexpr size_t tile_rank_w_smem() {
 }
 
 template <int kNodes, int kThreads, int kStride>
-__global__ void __launch_bounds__(kThreads, 2048 / kThreads)
+__global__ void __launch_bounds__(kThreads, kNodes > 8192 ? 1 : 2048 / kThreads)
     k_tile_rank_w(const unsigned long long* n_dev, const uint32_t* __restrict__ exit_in,
                   const uint32_t* __restrict__ seg_in, const uint32_t* __restrict__ w,
                   uint32_t* __restrict__ seg,
@@ -452,6 +452,7 @@ void set_smem(K kern, size_t smem, bool& done) {
   }
 }
 constexpr int kLevelNodes = 8192;
+constexpr int kBigLevelNodes = 16384;
 constexpr int kLevelThreads = 1024;
 }  // namespace
 
@@ -479,24 +480,32 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
     uint32_t* seg;  // up-mapping of this level's nodes
     uint32_t* off;
     int64_t bound;  // node-count bound (grid sizing)
+    int tile;       // nodes per tile: 8K (two CTAs per SM) while a level
+                    // fills the GPU, 16K (one CTA per SM, twice the
+                    // contraction) once one wave of 16K tiles covers it
   } L[kMaxLevels + 2];
-  L[0] = Level{exit1, seg1, len1, pre1, nullptr, nullptr, R};
+  L[0] = Level{exit1, seg1, len1, pre1, nullptr, nullptr, R, 0};
   const int contract = std::max(2, env_int("RSTG_LR_TILECONTRACT", 3));
+  static const int big_tiles = env_int("RSTG_LR_BIGTILES", 1);
+  const int64_t big_max = big_tiles ? (int64_t)num_sms() * kBigLevelNodes : 0;
   int top = 0;
   for (;;) {
     const int64_t b = L[top].bound;
+    L[top].tile = b <= big_max ? kBigLevelNodes : kLevelNodes;
     size_t cap = kLevelNodes;
     while ((int64_t)cap < b) cap <<= 1;  // stable across builds
     uint32_t* a = h.ws<uint32_t>(WS_TL2 + top, 5 * cap);
     L[top].seg = a;
     L[top].off = a + cap;
-    if (b <= kLevelNodes) break;
+    if (b <= L[top].tile) break;
     if (top == kMaxLevels - 1) return false;
     // the next level's nodes: at most a third of these (bound; 3.6-4x is
     // typical), else overflow (RSTG_LR_TILECONTRACT overrides the factor:
     // the tests force the fallback with a large one)
+    // (16K tiles contract 7-12x on road: bounded by 5x there)
+    const int c = L[top].tile == kBigLevelNodes ? std::max(contract, 5) : contract;
     L[top + 1] = Level{a + 2 * cap, L[top].seg, a + 3 * cap, a + 4 * cap, nullptr, nullptr,
-                       std::max<int64_t>((b + contract - 1) / contract, 1)};
+                       std::max<int64_t>((b + c - 1) / c, 1), 0};
     ++top;
   }
   // one control block, zeroed by one memset: node counts [0, 16) (count 0 =
@@ -504,7 +513,7 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
   // overflow flag [16], then each level's tile counter + look-back states
   size_t words = 32;
   for (int l = 0; l <= top; ++l)
-    words += (l == top ? 1 : (L[l].bound + kLevelNodes - 1) / kLevelNodes) + 1;
+    words += (l == top ? 1 : (L[l].bound + L[l].tile - 1) / L[l].tile) + 1;
   unsigned long long* blk = h.ws<unsigned long long>(WS_TL_LAST, words);
   unsigned long long* cnt = blk;
   int* overflow = reinterpret_cast<int*>(blk + 16);
@@ -512,23 +521,30 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
   CK(cudaMemcpyAsync(cnt, h.dev_box + 8, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
   static const int wstride = env_int("RSTG_LR_WSTRIDE", 4);
   constexpr size_t smem = tile_rank_w_smem<kLevelNodes>();
+  constexpr size_t smem_big = tile_rank_w_smem<kBigLevelNodes>();
   auto kern = wstride >= 8   ? k_tile_rank_w<kLevelNodes, kLevelThreads, 8>
               : wstride >= 4 ? k_tile_rank_w<kLevelNodes, kLevelThreads, 4>
                              : k_tile_rank_w<kLevelNodes, kLevelThreads, 2>;
-  static bool attr = false;
+  auto kern_big = wstride >= 8   ? k_tile_rank_w<kBigLevelNodes, kLevelThreads, 16>
+                  : wstride >= 4 ? k_tile_rank_w<kBigLevelNodes, kLevelThreads, 8>
+                                 : k_tile_rank_w<kBigLevelNodes, kLevelThreads, 4>;
+  static bool attr = false, attr_big = false;
   set_smem(kern, smem, attr);
+  set_smem(kern_big, smem_big, attr_big);
   unsigned long long* state = blk + 32;
   for (int l = 0; l <= top; ++l) {
     const bool is_top = l == top;
-    const unsigned tiles = is_top ? 1u : (unsigned)((L[l].bound + kLevelNodes - 1) / kLevelNodes);
+    const bool big = L[l].tile == kBigLevelNodes;
+    const unsigned tiles = is_top ? 1u : (unsigned)((L[l].bound + L[l].tile - 1) / L[l].tile);
     // the top is one tile: its segments are whole lists and its offsets
     // the prefixes; its segment outputs go to scratch
-    uint32_t* scratch = h.ws<uint32_t>(WS_RA, 4 * (size_t)kLevelNodes);
-    kern<<<tiles, kLevelThreads, smem, s>>>(
+    uint32_t* scratch = h.ws<uint32_t>(WS_RA, 4 * (size_t)kBigLevelNodes);
+    const int kScr = kBigLevelNodes;
+    (big ? kern_big : kern)<<<tiles, kLevelThreads, big ? smem_big : smem, s>>>(
         cnt + l, L[l].exit, L[l].seg_in, L[l].len, is_top ? scratch : L[l].seg,
         is_top ? L[l].pre : L[l].off,
-        is_top ? scratch + kLevelNodes : const_cast<uint32_t*>(L[l + 1].len),
-        is_top ? scratch + 2 * kLevelNodes : const_cast<uint32_t*>(L[l + 1].exit), cnt + l + 1,
+        is_top ? scratch + kScr : const_cast<uint32_t*>(L[l + 1].len),
+        is_top ? scratch + 2 * kScr : const_cast<uint32_t*>(L[l + 1].exit), cnt + l + 1,
         state, overflow);
     CK_LAUNCH();
     state += tiles + 1;

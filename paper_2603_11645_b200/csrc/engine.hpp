@@ -243,6 +243,18 @@ __device__ __forceinline__ int32_t find_root(int32_t* rep, int32_t x) {
   return r;
 }
 
+// The same walk without the write-back, for readers that only need the
+// root (the Euler vertex pass: later passes test lab[v] == v only).
+__device__ __forceinline__ int32_t find_root_ro(const int32_t* rep, int32_t x) {
+  int32_t r = rep[x];
+  if (r == x) return x;
+  for (;;) {
+    const int32_t q = rep[r];
+    if (q == r) return r;
+    r = q;
+  }
+}
+
 __device__ __forceinline__ void link_tree_edge(const EulerIO& io, uint32_t slot, uint32_t a,
                                                uint32_t b) {
   const uint32_t p = slot, q = io.nslots + slot;  // p: a -> b, q: b -> a

@@ -46,8 +46,9 @@ void launch_min_vertex(Handle& h, const int32_t* lab, uint32_t* minv) {
   h.stats.step(h.g.n);
 }
 
-__global__ void k_override_root(const int32_t* lab, uint32_t* minv, int32_t root) {
-  if (threadIdx.x == 0 && blockIdx.x == 0 && root >= 0) minv[lab[root]] = (uint32_t)root;
+__global__ void k_override_root(const int32_t* lab, uint32_t* minv, int32_t root, bool cc_slots) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && root >= 0)
+    minv[cc_slots ? find_root_ro(lab, root) : lab[root]] = (uint32_t)root;  // (lazy CC labels)
 }
 
 // Labels present (explicit forests: caller labels need not be rep roots).
@@ -91,9 +92,9 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
     for (int k = 0; k < kFixItems; ++k) {
       const int64_t v = base + k * kBlock + threadIdx.x;
-      // CC labels may be lazy (cc_exact with Euler): resolve and compress
-      const int32_t l = v < n ? (cc_slots ? find_root(const_cast<int32_t*>(lab), (int32_t)v) : lab[v])
-                              : -1;
+      // CC labels may be lazy (cc_exact with Euler): resolve
+      // (no compression write-back: every later pass only tests lab[v] == v)
+      const int32_t l = v < n ? (cc_slots ? find_root_ro(lab, (int32_t)v) : lab[v]) : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, l);
       h2[k] = kNone32;
       if (v >= n) continue;
@@ -321,7 +322,7 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   k_euler_fix<<<grid_for((n + kFixItems - 1) / kFixItems), kBlock, 0, s>>>(
       n, labels, present, minv, io, cc_slots, lablist, comps, rpos, sl, ctr, tiles, P.logk0, P.ob,
       (uint32_t)P.cap, !use_tiles);
-  k_override_root<<<1, 32, 0, s>>>(labels, minv, designated_root);
+  k_override_root<<<1, 32, 0, s>>>(labels, minv, designated_root, cc_slots);
   k_euler_roots<<<grid_for(n), kBlock, 0, s>>>(lablist, comps, minv, io, parent, rpos, sl, ctr,
                                                P.logk0, P.ob, (uint32_t)P.cap, !use_tiles);
   if (!use_tiles && !cc_slots && T > 0)

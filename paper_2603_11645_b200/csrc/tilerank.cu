@@ -30,6 +30,7 @@
 // A tour that jumps between tiles (random vertex ids) gains little: the
 // caller (euler.cu) then keeps the ruling-set walk, chosen per graph from
 // an edge-locality sample.
+#include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -487,7 +488,8 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
   L[0] = Level{exit1, seg1, len1, pre1, nullptr, nullptr, R, 0};
   const int contract = std::max(2, env_int("RSTG_LR_TILECONTRACT", 3));
   static const int big_tiles = env_int("RSTG_LR_BIGTILES", 1);
-  const int64_t big_max = big_tiles ? (int64_t)num_sms() * kBigLevelNodes : 0;
+  const int64_t big_max = big_tiles == 2 ? INT64_MAX
+                          : big_tiles ? (int64_t)num_sms() * kBigLevelNodes : 0;
   int top = 0;
   for (;;) {
     const int64_t b = L[top].bound;

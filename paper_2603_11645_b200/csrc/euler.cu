@@ -214,15 +214,15 @@ __global__ void __launch_bounds__(kBlock)
 
 // derive_parents on tile ranks (tilerank.cu): rank = segstart[seg] + off.
 __global__ void __launch_bounds__(kBlock)
-    k_orient_tiles(int64_t N, const int32_t* __restrict__ lab, bool cc_slots,
-                   const uint2* __restrict__ eto, const uint32_t* __restrict__ seg,
+    k_orient_tiles(int64_t N, const uint2* __restrict__ eto, const uint32_t* __restrict__ seg,
                    const uint16_t* __restrict__ off, const uint32_t* __restrict__ segstart,
                    int32_t* __restrict__ parent) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (cc_slots && lab[i] == (int32_t)i) continue;  // no tree edge in this slot
+    const uint32_t sp = seg[i];
+    if (sp == kNone32) continue;  // no tree edge in this slot (the tile pass marked it)
     const uint2 t = eto[i];  // (b, a): arc i = a -> b, arc N + i = b -> a
-    const uint32_t rp = segstart[seg[i]] + off[i];
+    const uint32_t rp = segstart[sp] + off[i];
     const uint32_t rq = segstart[seg[N + i]] + off[N + i];
     if (rp > rq)
       parent[t.y] = (int32_t)t.x;  // a -> b returns: parent[a] = b
@@ -342,9 +342,9 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
 
   if (use_tiles) {
     const TileRank tr = lr_rank_tiles(h, P, N, io.S, labels, cc_slots, T, verify);
-    h.timer.begin(s, "euler.orient", 8.0 * N + 20.0 * T);
-    k_orient_tiles<<<grid_for(N), kBlock, 0, s>>>(N, labels, cc_slots,
-                                                  reinterpret_cast<const uint2*>(io.eto), tr.seg,
+    // seg of every slot; per tree edge eto, the other seg, two offsets, two starts, parent
+    h.timer.begin(s, "euler.orient", 4.0 * N + 28.0 * T);
+    k_orient_tiles<<<grid_for(N), kBlock, 0, s>>>(N, reinterpret_cast<const uint2*>(io.eto), tr.seg,
                                                   tr.off, tr.segstart, parent);
     CK_LAUNCH();
     h.stats.step(N);

@@ -240,7 +240,10 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
   const uint32_t sbase = s_base;
 #pragma unroll
   for (int q = 0; q < kOwn; ++q) {
-    if (!(vmask >> q & 1)) continue;
+    if (!(vmask >> q & 1)) {  // no arc: marked for the orient pass
+      if (tid + (q >> 1) * kThreads < cnt) __stcs(&seg[global_of(q)], kNone32);
+      continue;
+    }
     uint32_t w = word[local_of(q)], o = 0;
     if (!(rmask >> q & 1)) {  // (ruler, offset) -> the ruler's (head, offset)
       o = w & 0xFFFFu;

@@ -111,13 +111,15 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
                 uint32_t* __restrict__ seg_len, uint32_t* __restrict__ seg_exit,
                 unsigned long long* nseg, unsigned long long* state,
                 unsigned long long* walked) {
-  static_assert(2 * kSlots <= kTileExit, "local arc index must fit 15 bits");
+  static_assert(2 * kSlots <= kTileExit + 1, "local arc index must fit 15 bits");
   constexpr int kArcs = 2 * kSlots;
   constexpr int kPer = kSlots / kThreads;  // slots per thread
   constexpr int kOwn = 2 * kPer;           // arcs per thread
   static_assert(kOwn <= 32, "own-arc masks are 32 bits");
   extern __shared__ uint32_t word[];  // arc: ruler << 16 | offset; ruler: pred ruler << 16 | dist
-  uint16_t* nx = reinterpret_cast<uint16_t*>(word + kArcs);  // local successor | ruler flag
+  // local successor | ruler flag; an arc whose successor leaves the tile
+  // (or ends the tour) points at itself
+  uint16_t* nx = reinterpret_cast<uint16_t*>(word + kArcs);
   uint16_t* hid = nx;  // (after the walks) head -> local segment number
   // has an in-tile predecessor: plain byte stores (racing stores all write
   // 1), not bitmap atomics -- a path's warp would hit one word 32 times
@@ -174,14 +176,15 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
 #pragma unroll
   for (int q = 0; q < kOwn; ++q) {
     if (!(vmask >> q & 1)) continue;
-    const uint32_t v = word[local_of(q)];
-    uint32_t ls = kTileExit;
+    const uint32_t li = local_of(q);
+    const uint32_t v = word[li];
+    uint32_t ls = li;
     if (v - t0 < cnt) ls = v - t0;                              // forward arc in the tile
     else if (v - N - t0 < cnt && v >= N) ls = v - N - t0 + kSlots;  // reverse arc in the tile
-    if (v == kNone32) ls = kTileExit;
-    if (ls != kTileExit) haspred[ls] = 1;
+    if (v == kNone32) ls = li;
+    if (ls != li) haspred[ls] = 1;
     else tmask |= 1u << q;
-    nx[local_of(q)] = (uint16_t)ls;
+    nx[li] = (uint16_t)ls;
   }
   __syncthreads();
   // 2. rulers: heads, and own arc q == tid % kOwn (one arc in kOwn by index)
@@ -202,11 +205,13 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
   for (uint32_t m = rmask; m; m &= m - 1) {
     const uint32_t r = local_of(__ffs(m) - 1);
     uint32_t cur = nx[r] & kTileExit, o = 1;
-    while (cur != kTileExit) {
+    if (cur == r) continue;  // its successor leaves the tile
+    for (;;) {
       const uint32_t v = nx[cur];
       word[cur] = r << 16 | o;
-      if (v & kTileRuler) break;
-      cur = v & kTileExit;
+      const uint32_t nxt = v & kTileExit;
+      if ((v & kTileRuler) || nxt == cur) break;
+      cur = nxt;
       ++o;
     }
   }
@@ -582,21 +587,23 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   unsigned long long* walked = reinterpret_cast<unsigned long long*>(h.dev_box) + 14;
   static const int slots_env = env_int("RSTG_LR_TILESLOTS", 8192);
   static const bool dbg = getenv("RSTG_LR_DEBUG") != nullptr;
-  const int slots = slots_env <= 2048 ? 2048 : slots_env <= 4096 ? 4096 : 8192;
+  const int slots = slots_env <= 2048 ? 2048 : slots_env <= 4096 ? 4096 : slots_env <= 8192 ? 8192 : 16384;
   const unsigned tiles = (unsigned)((N + slots - 1) / slots);
   unsigned long long* state = h.ws<unsigned long long>(WS_TSTATE, (size_t)tiles + 1);
   h.timer.begin(s, "lr.tiles", 12.0 * E);  // succ read + segment id + offset per arc
   CK(cudaMemsetAsync(state, 0, ((size_t)tiles + 1) * sizeof(unsigned long long), s));
   if (verify || dbg) CK(cudaMemsetAsync(h.dev_box + 14, 0, 2 * sizeof(int64_t), s));
   auto launch = [&](auto kern, int threads, size_t smem, int a) {
-    static bool attr[5] = {false, false, false, false, false};
+    static bool attr[6] = {false, false, false, false, false, false};
     set_smem(kern, smem, attr[a]);
     kern<<<tiles, threads, smem, s>>>((uint32_t)N, S, lab, cc_slots, (uint32_t)T, seg, off,
                                       seg_len, seg_exit, nseg, state,
                                       verify || dbg ? walked : nullptr);
   };
   static const int stride1 = env_int("RSTG_LR_STRIDE", 16);
-  if (slots == 2048)
+  if (slots == 16384)
+    launch(k_tile_rank<16384, 1024, 32>, 1024, tile_rank_smem<16384>(), 5);
+  else if (slots == 2048)
     launch(k_tile_rank<2048, 256, 16>, 256, tile_rank_smem<2048>(), 0);
   else if (slots == 4096)
     launch(k_tile_rank<4096, 512, 16>, 512, tile_rank_smem<4096>(), 1);

@@ -176,7 +176,10 @@ __global__ void __launch_bounds__(kBlock)
 // 8K vertices per tile (32 KB of shared memory, two 1024-thread CTAs per
 // SM). Measured on the road mesh: 32K-vertex tiles (one CTA per SM) keep
 // more pointers inside the tile but lose more to the lower occupancy.
-constexpr int kTileV = 8192;
+#ifndef RSTG_CC_TILEV
+#define RSTG_CC_TILEV 8192
+#endif
+constexpr int kTileV = RSTG_CC_TILEV;
 constexpr int kTileThreads = 1024;
 constexpr size_t kTileSmem = kTileV * sizeof(int32_t);
 
@@ -210,7 +213,7 @@ struct RoundIO {
 };
 
 template <int SRC>
-__global__ void __launch_bounds__(kTileThreads, 2)
+__global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
     k_tile_resolve(int64_t n, int32_t* rep, uint32_t* xbits, uint32_t* xlist,
                    unsigned long long* xcount, RoundIO io) {
   extern __shared__ int32_t s[];  // kTileV reps (+ 2 x kTileV list words when linking round 0)

@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // ---- two-level shortcutting ---------------------------------------------
+constexpr int kJumpBatch = 4;  // entries in flight per thread in k_jump_x
+
 // Level 1 (k_tile_resolve): each CTA owns a tile of kTileV consecutive
 // vertices held in shared memory and follows every pointer while it stays
 // inside the tile (in-smem doubling), so rep[v] becomes either a root or the
@@ -429,19 +431,44 @@ __global__ void __launch_bounds__(kBlock)
   for (int r = 0; r < max_rounds; ++r) {
     if (gtid == 0) flags[(r + 1) % 3] = 0;  // read by everyone two barriers ago
     bool changed = false;
-    for (int64_t i = gtid; i < X; i += gsize) {
-      const uint32_t v = list[i];
-      const int32_t p = ld_cg(&rep[v]);
-      int32_t x = ld_cg(&rep[p]);
-      if (x == p) continue;
+    // kJumpBatch entries per thread at a time: their loads of one hop level
+    // are issued together (independent chains), not one chain after another
+    for (int64_t i0 = gtid; i0 < X; i0 += kJumpBatch * gsize) {
+      uint32_t v[kJumpBatch];
+      int32_t p[kJumpBatch], x[kJumpBatch];
+      bool live[kJumpBatch];
+#pragma unroll
+      for (int k = 0; k < kJumpBatch; ++k) {
+        const int64_t i = i0 + k * gsize;
+        live[k] = i < X;
+        v[k] = live[k] ? list[i] : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kJumpBatch; ++k) p[k] = live[k] ? ld_cg(&rep[v[k]]) : 0;
+#pragma unroll
+      for (int k = 0; k < kJumpBatch; ++k) {
+        x[k] = live[k] ? ld_cg(&rep[p[k]]) : 0;
+        live[k] = live[k] && x[k] != p[k];  // p a root: nothing to do
+      }
+      bool walk[kJumpBatch];
+#pragma unroll
+      for (int k = 0; k < kJumpBatch; ++k) walk[k] = live[k];
 #pragma unroll
       for (int hop = 1; hop < 4; ++hop) {
-        const int32_t y = ld_cg(&rep[x]);
-        if (y == x) break;
-        x = y;
+#pragma unroll
+        for (int k = 0; k < kJumpBatch; ++k) {
+          if (!walk[k]) continue;
+          const int32_t y = ld_cg(&rep[x[k]]);
+          if (y == x[k]) walk[k] = false;
+          else x[k] = y;
+        }
       }
-      rep[v] = x;
-      changed = true;
+#pragma unroll
+      for (int k = 0; k < kJumpBatch; ++k) {
+        if (!live[k]) continue;
+        rep[v[k]] = x[k];
+        changed = true;
+      }
     }
     if (__syncthreads_or(changed) && threadIdx.x == 0) flags[r % 3] = 1;
     grid.sync();

@@ -477,11 +477,18 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 __global__ void __launch_bounds__(kBlock) k_final_gather(int64_t n, int32_t* rep) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t p = rep[v];
-    const int32_t q = rep[p];
-    if (q != p) rep[v] = q;
+  // kJumpBatch vertices per thread at a time: all their loads before any
+  // store (a store to rep would otherwise order the next vertex's loads)
+  const int64_t g = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n; v0 += kJumpBatch * g) {
+    int32_t p[kJumpBatch], q[kJumpBatch];
+#pragma unroll
+    for (int k = 0; k < kJumpBatch; ++k) p[k] = v0 + k * g < n ? rep[v0 + k * g] : 0;
+#pragma unroll
+    for (int k = 0; k < kJumpBatch; ++k) q[k] = v0 + k * g < n ? rep[p[k]] : 0;
+#pragma unroll
+    for (int k = 0; k < kJumpBatch; ++k)
+      if (v0 + k * g < n && q[k] != p[k]) rep[v0 + k * g] = q[k];
   }
 }
 

@@ -170,23 +170,42 @@ __global__ void k_reverse_b(int64_t n, uint8_t* mark, int32_t* parent, int32_t* 
 
 // One batched_jump barrier (pr_rst.cpp:235-244). Buffers alternate; a
 // converged state makes later barriers no-ops.
+template <int kB>
 __global__ void __launch_bounds__(kBlock)
     k_jump_barrier(int64_t n, int64_t hops, int barrier, int32_t* buf0, int32_t* buf1,
                    int* ctl, int* not_done) {
   if (ctl[C_JUMP_DONE]) return;
-  const int32_t* snap = (barrier & 1) ? buf1 : buf0;
-  int32_t* next = (barrier & 1) ? buf0 : buf1;
+  const int32_t* __restrict__ snap = (barrier & 1) ? buf1 : buf0;
+  int32_t* __restrict__ next = (barrier & 1) ? buf0 : buf1;
+  // kB vertices' chains walked together: each hop's loads issued at once
   bool pending = false;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    int32_t x = snap[v];
-    for (int64_t t = 1; t < hops; ++t) {
-      const int32_t nx = snap[x];
-      if (nx == x) break;
-      x = nx;
+  const int64_t g = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n; v0 += kB * g) {
+    int32_t x[kB];
+    bool walk[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      walk[j] = v0 + j * g < n;
+      x[j] = walk[j] ? snap[v0 + j * g] : 0;
     }
-    next[v] = x;
-    if (snap[x] != x) pending = true;
+    for (int64_t t = 1; t < hops; ++t) {
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        if (!walk[j]) continue;
+        const int32_t nx = snap[x[j]];
+        if (nx == x[j]) walk[j] = false;
+        else x[j] = nx;
+        any |= walk[j];
+      }
+      if (!any) break;
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      if (v0 + j * g >= n) continue;
+      next[v0 + j * g] = x[j];
+      if (snap[x[j]] != x[j]) pending = true;
+    }
   }
   block_flag(pending, not_done);
 }
@@ -207,20 +226,31 @@ __global__ void k_jump_copyback(int64_t n, int32_t* rep, const int32_t* other, c
 }
 
 // rebuild_special_ancestors level k >= 1 (pr_rst.cpp:260-264).
+template <int kB>
 __global__ void __launch_bounds__(kBlock) k_anc_level(int64_t n, int k, int32_t* anc, int* ctl) {
   if (k >= 2 && !ctl[C_CHANGED0 + k - 1]) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(&ctl[C_LMAX], k);
     return;
   }
-  const int32_t* prev = anc + (int64_t)(k - 1) * n;
-  int32_t* cur = anc + (int64_t)k * n;
+  // (distinct levels of one buffer: restrict-qualified so the stores do not
+  // order the next vertices' loads; kB vertices' gathers in flight -- 4 on
+  // graphs larger than L2, where each gather waits on DRAM)
+  const int32_t* __restrict__ prev = anc + (int64_t)(k - 1) * n;
+  int32_t* __restrict__ cur = anc + (int64_t)k * n;
   bool changed = false;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t a = prev[v];
-    const int32_t b = prev[a];
-    cur[v] = b;
-    changed |= (b != a);
+  const int64_t g = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n; v0 += kB * g) {
+    int32_t a[kB], b[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) a[j] = v0 + j * g < n ? __ldcs(&prev[v0 + j * g]) : 0;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) b[j] = v0 + j * g < n ? prev[a[j]] : 0;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      if (v0 + j * g >= n) continue;
+      cur[v0 + j * g] = b[j];
+      changed |= (b[j] != a[j]);
+    }
   }
   block_flag(changed, &ctl[C_CHANGED0 + k]);
 }
@@ -239,6 +269,9 @@ static int ceil_log2_i(int64_t x) {
 }
 
 void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
+  // batched gathers pay once a level of the ancestor table (4n bytes) no
+  // longer sits in L2
+  const bool big = h.g.n > (int64_t{1} << 22);
   const int64_t n = h.g.n, m = h.g.m;
   const int L = std::max(ceil_log2_i(std::max<int64_t>(n, 1)), 1);
   int32_t* rep = h.ws<int32_t>(WS_REP, n);
@@ -336,7 +369,8 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     CK(cudaMemsetAsync(ctl + C_JUMP_DONE, 0, 2 * sizeof(int), s));
     CK(cudaMemsetAsync(not_done, 0, sizeof(int), s));
     for (int64_t b = 0; b <= max_barriers; ++b) {
-      k_jump_barrier<<<g, kBlock, 0, s>>>(n, hops, (int)b, rep, nextbuf, ctl, not_done);
+      (big ? k_jump_barrier<4> : k_jump_barrier<1>)<<<g, kBlock, 0, s>>>(n, hops, (int)b, rep,
+                                                                        nextbuf, ctl, not_done);
       k_jump_close<<<1, 1, 0, s>>>((int)b, ctl, not_done);
       h.stats.step(n);
     }
@@ -348,7 +382,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     CK(cudaMemsetAsync(ctl + C_CHANGED0, 0, 40 * sizeof(int), s));
     k_set_i32<<<1, 1, 0, s>>>(ctl + C_LMAX, L);
     for (int k = 1; k < L; ++k) {
-      k_anc_level<<<g, kBlock, 0, s>>>(n, k, anc, ctl);
+      (big ? k_anc_level<4> : k_anc_level<1>)<<<g, kBlock, 0, s>>>(n, k, anc, ctl);
       h.stats.step(n);
     }
     CK_LAUNCH();

@@ -105,14 +105,23 @@ __global__ void __launch_bounds__(kBlock)
   const int kk = min(k, ctl[C_LMAX] - 1);
   const int32_t* lvl = anc + (int64_t)kk * n;
   bool grew = false;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const uint8_t t = mark[v];
-    if (t == 0 || t > k + 1) continue;
-    const int32_t a = lvl[v];
-    if (mark[a] == 0) {
-      mark[a] = (uint8_t)(k + 2);
-      grew = true;
+  // four marks per load (almost all are 0: one 32-bit test skips them); the
+  // mark buffer is padded past n
+  const int64_t words = (n + 3) / 4;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t t4 = reinterpret_cast<const volatile uint32_t*>(mark)[w];
+    if (t4 == 0) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t t = (t4 >> (8 * b)) & 0xFFu;
+      const int64_t v = 4 * w + b;
+      if (t == 0 || t > (uint32_t)(k + 1) || v >= n) continue;
+      const int32_t a = lvl[v];
+      if (mark[a] == 0) {
+        mark[a] = (uint8_t)(k + 2);
+        grew = true;
+      }
     }
   }
   block_flag(grew, &ctl[C_GREW0 + k]);

@@ -504,21 +504,15 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
   CK(cudaMemsetAsync(xbits, 0, (size_t)words * sizeof(uint32_t), h.stream));
   CK(cudaMemsetAsync(h.dev_box + 5, 0, 3 * sizeof(int64_t), h.stream));
   const unsigned tiles = (unsigned)((n + kTileV - 1) / kTileV);
-  static bool attr_set = false;
   static int coop_blocks = 0;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_tile_resolve<kSrcApply>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kTileSmem));
-    CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRound0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(3 * kTileSmem)));
-    CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRound0Slot>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSmem)));
-    CK(cudaFuncSetAttribute(k_tile_resolve<kSrcRep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kTileSmem));
+  ensure_dyn_smem((const void*)k_tile_resolve<kSrcApply>, kTileSmem);
+  ensure_dyn_smem((const void*)k_tile_resolve<kSrcRound0>, 3 * kTileSmem);
+  ensure_dyn_smem((const void*)k_tile_resolve<kSrcRound0Slot>, 3 * kTileSmem);
+  ensure_dyn_smem((const void*)k_tile_resolve<kSrcRep>, kTileSmem);
+  if (!coop_blocks) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jump_x, kBlock, 0));
     coop_blocks = std::max(1, per_sm) * num_sms();
-    attr_set = true;
   }
   if (src == kSrcApply)
     k_tile_resolve<kSrcApply><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, xbits, xlist,
@@ -930,12 +924,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
       if (have_r0 && jump_roots && total > prev_total) {
         h.timer.begin(h.stream, "cc.jump_roots", 8.0 * r0_count);
         if (r0_count <= kJumpSmallMax) {
-          static bool attr = false;
-          if (!attr) {
-            CK(cudaFuncSetAttribute(k_jump_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kJumpSmallSmem));
-            attr = true;
-          }
+          ensure_dyn_smem((const void*)k_jump_small, kJumpSmallSmem);
           k_jump_small<<<1, 1024, kJumpSmallSmem, h.stream>>>(rl[0], rcount, rep);
           CK_LAUNCH();
           h.stats.step(n);

@@ -44,6 +44,10 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define CK_LAUNCH() ::rstg::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
 int num_sms();
+// Raises a kernel's dynamic shared memory limit to `bytes` on the current
+// device (the attribute is per device: one process may drive several GPUs).
+// Thread-safe; a cheap lookup after the first call per (device, kernel).
+void ensure_dyn_smem(const void* func, size_t bytes);
 // Grid for a grid-stride loop over `work` items: enough CTAs to fill every SM
 // (8 x 256 threads resident per SM), never more than the work needs.
 inline unsigned grid_for(int64_t work, int block = kBlock) {

@@ -1,4 +1,6 @@
 // engine.cu -- Handle, workspace, phase timer, shared small kernels.
+#include <map>
+#include <mutex>
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
@@ -16,6 +18,18 @@ int num_sms() {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   return sms;
+}
+
+void ensure_dyn_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, func}];
+  if (have >= bytes) return;
+  CK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  have = bytes;
 }
 
 // ---------------------------------------------------------------- timer

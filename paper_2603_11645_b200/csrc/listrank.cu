@@ -670,12 +670,7 @@ void list_prefix(Handle& h, const LrParams& P, int64_t N, const uint32_t* next, 
   if (N <= 0) return;
   const cudaStream_t s = h.stream;
   if (N <= kBaseMax) {
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_lr_base, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(2 * kBaseMax * sizeof(uint32_t))));
-      attr = true;
-    }
+    ensure_dyn_smem((const void*)k_lr_base, 2 * kBaseMax * sizeof(uint32_t));
     k_lr_base<<<1, 1024, 2 * N * sizeof(uint32_t), s>>>((int)N, next, w, pre,
                                                          ceil_log2_ll(N < 2 ? 2 : N) + 1, bad);
     CK_LAUNCH();

@@ -454,11 +454,8 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 template <class K>
-void set_smem(K kern, size_t smem, bool& done) {
-  if (!done) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    done = true;
-  }
+void set_smem(K kern, size_t smem) {
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
 }
 constexpr int kLevelNodes = 8192;
 constexpr int kBigLevelNodes = 16384;
@@ -538,9 +535,8 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
   auto kern_big = wstride >= 8   ? k_tile_rank_w<kBigLevelNodes, kLevelThreads, 16>
                   : wstride >= 4 ? k_tile_rank_w<kBigLevelNodes, kLevelThreads, 8>
                                  : k_tile_rank_w<kBigLevelNodes, kLevelThreads, 4>;
-  static bool attr = false, attr_big = false;
-  set_smem(kern, smem, attr);
-  set_smem(kern_big, smem_big, attr_big);
+  set_smem(kern, smem);
+  set_smem(kern_big, smem_big);
   unsigned long long* state = blk + 32;
   for (int l = 0; l <= top; ++l) {
     const bool is_top = l == top;
@@ -593,26 +589,25 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   h.timer.begin(s, "lr.tiles", 12.0 * E);  // succ read + segment id + offset per arc
   CK(cudaMemsetAsync(state, 0, ((size_t)tiles + 1) * sizeof(unsigned long long), s));
   if (verify || dbg) CK(cudaMemsetAsync(h.dev_box + 14, 0, 2 * sizeof(int64_t), s));
-  auto launch = [&](auto kern, int threads, size_t smem, int a) {
-    static bool attr[6] = {false, false, false, false, false, false};
-    set_smem(kern, smem, attr[a]);
+  auto launch = [&](auto kern, int threads, size_t smem) {
+    set_smem(kern, smem);
     kern<<<tiles, threads, smem, s>>>((uint32_t)N, S, lab, cc_slots, (uint32_t)T, seg, off,
                                       seg_len, seg_exit, nseg, state,
                                       verify || dbg ? walked : nullptr);
   };
   static const int stride1 = env_int("RSTG_LR_STRIDE", 16);
   if (slots == 16384)
-    launch(k_tile_rank<16384, 1024, 32>, 1024, tile_rank_smem<16384>(), 5);
+    launch(k_tile_rank<16384, 1024, 32>, 1024, tile_rank_smem<16384>());
   else if (slots == 2048)
-    launch(k_tile_rank<2048, 256, 16>, 256, tile_rank_smem<2048>(), 0);
+    launch(k_tile_rank<2048, 256, 16>, 256, tile_rank_smem<2048>());
   else if (slots == 4096)
-    launch(k_tile_rank<4096, 512, 16>, 512, tile_rank_smem<4096>(), 1);
+    launch(k_tile_rank<4096, 512, 16>, 512, tile_rank_smem<4096>());
   else if (stride1 <= 4)
-    launch(k_tile_rank<8192, 1024, 4>, 1024, tile_rank_smem<8192>(), 2);
+    launch(k_tile_rank<8192, 1024, 4>, 1024, tile_rank_smem<8192>());
   else if (stride1 <= 8)
-    launch(k_tile_rank<8192, 1024, 8>, 1024, tile_rank_smem<8192>(), 3);
+    launch(k_tile_rank<8192, 1024, 8>, 1024, tile_rank_smem<8192>());
   else
-    launch(k_tile_rank<8192, 1024, 16>, 1024, tile_rank_smem<8192>(), 4);
+    launch(k_tile_rank<8192, 1024, 16>, 1024, tile_rank_smem<8192>());
   CK_LAUNCH();
   h.stats.step(E, 2);
   h.read_box(h.dev_box + 8, 8);  // [8] segments, [14] arcs walked, [15] jump rounds

@@ -42,7 +42,11 @@ namespace rstg {
 
 constexpr int kTileRankThreads = 1024;
 
-constexpr uint16_t kTileExit = 0x7FFF;   // successor leaves the tile / list end
+// nx[] packs a 15-bit local index with a ruler flag. Level kernels (<= 16K
+// nodes) mark "successor leaves the tile / list end" with kTileExit; the
+// level-1 kernel (up to 32K arcs: every 15-bit value is an arc) marks it by
+// pointing the arc at itself, and uses kTileExit only as the index mask.
+constexpr uint16_t kTileExit = 0x7FFF;
 constexpr uint16_t kTileRuler = 0x8000;  // flag on nx[li]: li is a ruler
 
 // Tile-ordered numbering, single pass (decoupled look-back): tile ids are

@@ -163,7 +163,10 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // ---- two-level shortcutting ---------------------------------------------
-constexpr int kJumpBatch = 4;  // entries in flight per thread in k_jump_x
+#ifndef RSTG_JUMP_BATCH
+#define RSTG_JUMP_BATCH 4
+#endif
+constexpr int kJumpBatch = RSTG_JUMP_BATCH;  // entries in flight per thread in k_jump_x
 
 // Level 1 (k_tile_resolve): each CTA owns a tile of kTileV consecutive
 // vertices held in shared memory and follows every pointer while it stays

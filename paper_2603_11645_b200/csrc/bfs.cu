@@ -303,6 +303,7 @@ int64_t bfs_rst(Handle& h, int32_t root, int32_t* parent, int32_t* level, int32_
   int32_t* lab = h.ws<int32_t>(WS_VAL_A, n);
   cc_labels_fast(h, lab);
   uint32_t* minv = h.ws<uint32_t>(WS_MINV, n);
+  h.minv_clean = nullptr;  // (WS_MINV reused here)
   CK(cudaMemsetAsync(minv, 0xFF, n * sizeof(uint32_t), s));
   launch_min_vertex(h, lab, minv);
   // The second phase starts again at level 1 (ctl index 1, odd queues).

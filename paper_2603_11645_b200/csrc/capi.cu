@@ -540,6 +540,7 @@ int rstg_forest_depth(rstg_graph* g, const int64_t* parent, int64_t* depth_out,
     to_device<int32_t>(h, parent, n, p);
     int32_t* depth = h.ws<int32_t>(WS_ROOTS, n + 1);  // (WS_VAL_C is the readback staging)
     uint32_t* rootmax = h.ws<uint32_t>(WS_MINV, n);
+    h.minv_clean = nullptr;  // (WS_MINV reused here)
     int64_t cyc = -1;
     forest_depth_device(h, p, depth, rootmax, &cyc);
     if (cyc >= 0) {

@@ -104,6 +104,9 @@ void Handle::free_graph() {
 void* Handle::ws(int slot, size_t bytes) {
   auto& b = bufs_[slot];
   if (b.second < bytes) {
+    // a new buffer (possibly at the old address) holds nothing known
+    if (slot == WS_MINV) minv_clean = nullptr;
+    if (slot == WS_SLOT) slots_clean = nullptr;
     if (b.first) {
       CK(cudaStreamSynchronize(stream));
       CK(cudaFree(b.first));
@@ -117,6 +120,8 @@ void* Handle::ws(int slot, size_t bytes) {
 
 void Handle::release(int slot) {
   auto& b = bufs_[slot];
+  if (slot == WS_MINV) minv_clean = nullptr;
+  if (slot == WS_SLOT) slots_clean = nullptr;
   if (b.first) {
     CK(cudaStreamSynchronize(stream));
     CK(cudaFree(b.first));

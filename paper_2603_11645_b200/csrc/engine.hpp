@@ -100,6 +100,9 @@ class Handle {
   // apart (-1: not measured for this graph). Decides the Euler-tour
   // ranking: tile contraction for locally numbered graphs, else ruling sets.
   int edge_locality = -1;
+  // WS_MINV holds all-ones left by the Euler root pass (its other users --
+  // BFS, validation, degree counts -- clear this when they take the buffer).
+  const void* minv_clean = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D staging of uploads (lazily created)
   cudaStream_t stream = nullptr;
   bool own_stream = true;

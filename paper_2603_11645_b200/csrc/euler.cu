@@ -138,22 +138,38 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+constexpr int64_t kResetMax = 1 << 16;
+
+// The min table between builds: all-ones, or flagged dirty by the root pass
+// (many components: it skipped the reset) and filled here.
+__global__ void k_fill_if_dirty(uint32_t* __restrict__ minv, int64_t n, const int* dirty) {
+  if (!*dirty) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    minv[i] = kNone32;
+}
+
 // Root pass over the labels: the root of label x is minv[x] (the designated
 // root already stored for its label): parent[r] = r (derive_parents :167),
 // its rotation cycle opened just before its first arc (break_cycles
 // :96-101) and that first arc registered as the head ruler of its tour.
 __global__ void __launch_bounds__(kBlock)
     k_euler_roots(const uint32_t* __restrict__ labels, const unsigned long long* nlabels,
-                  const uint32_t* __restrict__ minv, EulerIO io, int32_t* parent, uint32_t* rpos,
+                  uint32_t* __restrict__ minv, EulerIO io, int32_t* parent, uint32_t* rpos,
                   uint32_t* sl, unsigned long long* ctr, int logk, int ob, uint32_t cap,
-                  bool rulers) {
+                  bool rulers, int* minv_dirty) {
   const int64_t L = (int64_t)*nlabels;
+  // few labels: reset their min entries here; many: leave them, flagged
+  // for the fill before the next build (cheaper than a scattered reset)
+  const bool reset = L <= kResetMax;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *minv_dirty = reset ? 0 : 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < L; b += stride) {
     const int64_t i = b + threadIdx.x;
     uint32_t hd = kNone32;
     if (i < L) {
       const uint32_t r = minv[labels[i]];
+      if (reset) minv[labels[i]] = kNone32;
       parent[r] = (int32_t)r;
       const uint32_t h1 = io.vhead[r], h2 = io.rhead[r];
       hd = h1 != kNone32 ? h1 : h2;  // the combined list: local, then remote
@@ -303,7 +319,16 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   uint32_t* lablist = h.ws<uint32_t>(WS_LABELS, n + 1);
   // labels + remote heads read, min table written, one label entry per component
   h.timer.begin(s, "euler.roots", 4.0 * n + 4.0 * n + 4.0 * n);
-  CK(cudaMemsetAsync(minv, 0xFF, n * sizeof(uint32_t), s));
+  // The min table is all-ones between builds: the root pass resets every
+  // entry it consumes, so only a fresh (or foreign-used) buffer is filled.
+  int* minv_dirty = reinterpret_cast<int*>(h.dev_box + 19);
+  if (h.minv_clean != minv) {
+    CK(cudaMemsetAsync(minv, 0xFF, n * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(minv_dirty, 0, sizeof(int), s));
+  } else {
+    k_fill_if_dirty<<<grid_for(n), kBlock, 0, s>>>(minv, n, minv_dirty);
+  }
+  h.minv_clean = nullptr;  // (until the root pass below has run)
   CK(cudaMemsetAsync(h.dev_box + 4, 0, sizeof(int64_t), s));
   CK(cudaMemsetAsync(h.dev_box + 8, 0, sizeof(int64_t), s));
   CK(cudaMemsetAsync(h.dev_box + 13, 0, sizeof(int64_t), s));
@@ -324,7 +349,9 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
       (uint32_t)P.cap, !use_tiles);
   k_override_root<<<1, 32, 0, s>>>(labels, minv, designated_root, cc_slots);
   k_euler_roots<<<grid_for(n), kBlock, 0, s>>>(lablist, comps, minv, io, parent, rpos, sl, ctr,
-                                               P.logk0, P.ob, (uint32_t)P.cap, !use_tiles);
+                                               P.logk0, P.ob, (uint32_t)P.cap, !use_tiles,
+                                               minv_dirty);
+  h.minv_clean = minv;
   if (!use_tiles && !cc_slots && T > 0)
     k_register_slots<<<grid_for(T), kBlock, 0, s>>>(T, io.nslots, rpos, sl, ctr, P.logk0, P.ob,
                                                     (uint32_t)P.cap);

@@ -186,6 +186,7 @@ void build_csr_device(Handle& h) {
   const cudaStream_t s = h.stream;
   uint32_t* fdeg = h.ws<uint32_t>(WS_TF, n + 1);
   uint32_t* bdeg = h.ws<uint32_t>(WS_MINV, n + 1);
+  h.minv_clean = nullptr;  // (WS_MINV reused here)
   uint32_t* fs = h.ws<uint32_t>(WS_HEADS, n + 1);
   uint32_t* bs = h.ws<uint32_t>(WS_RPOS, n + 1);
   CK(cudaMemsetAsync(fdeg, 0, (n + 1) * sizeof(uint32_t), s));

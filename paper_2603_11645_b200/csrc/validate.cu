@@ -121,6 +121,7 @@ int validate_forest(Handle& h, const int32_t* parent, int32_t required_root,
   int32_t* lab = h.ws<int32_t>(WS_VAL_A, n);
   cc_labels_fast(h, lab);
   uint32_t* cnt = h.ws<uint32_t>(WS_MINV, n);
+  h.minv_clean = nullptr;  // (WS_MINV reused here)
   CK(cudaMemsetAsync(cnt, 0, n * sizeof(uint32_t), s));
   k_val_count_roots<<<g, kBlock, 0, s>>>(n, parent, lab, cnt);
   k_val_comp<<<g, kBlock, 0, s>>>(n, ra, lab, cnt, bad);

@@ -119,8 +119,9 @@ class Handle {
   // Small pinned host mailbox for flag/count readbacks.
   int64_t* host_box = nullptr;
   // Device counters block (256 x int64) zeroed per use by the caller; fixed
-  // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,14] lr, [16] pr, [20,22] cc
-  // roots, [30] bfs, [40] validate,
+  // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,15] lr / tile ranking,
+  // [16] pr bad mark, [17] edge-locality count, [18] pr crossing, [19] euler min-table
+  // dirty flag (persists across builds), [20,22] cc roots, [30] bfs, [40] validate,
   // [48] normalize, [50,53) capi/lr verify, [128,160) jump-round flags.
   int64_t* dev_box = nullptr;
 

@@ -29,7 +29,7 @@ void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* 
 void cc_round_done(Handle& h, int64_t out_count);
 void cc_reset_rounds(Handle& h);
 
-// Device control block layout (int32 words inside dev_box + 16).
+// Device control block layout (int32 words in the WS_BFS_CTRL workspace).
 enum PrCtl : int {
   C_ANY = 0,      // any graft proposal this round
   C_BAD_REV,      // reversal found a marked vertex with no source

@@ -103,6 +103,7 @@ class Handle {
   // WS_MINV holds all-ones left by the Euler root pass (its other users --
   // BFS, validation, degree counts -- clear this when they take the buffer).
   const void* minv_clean = nullptr;
+  int64_t minv_clean_n = 0;  // ... for its first minv_clean_n entries
   cudaStream_t copy_stream = nullptr;  // H2D staging of uploads (lazily created)
   cudaStream_t stream = nullptr;
   bool own_stream = true;

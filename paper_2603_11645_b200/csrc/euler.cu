@@ -322,7 +322,8 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   // The min table is all-ones between builds: the root pass resets every
   // entry it consumes, so only a fresh (or foreign-used) buffer is filled.
   int* minv_dirty = reinterpret_cast<int*>(h.dev_box + 19);
-  if (h.minv_clean != minv) {
+  // (entries past the last build's n may hold an older, larger build's values)
+  if (h.minv_clean != minv || n > h.minv_clean_n) {
     CK(cudaMemsetAsync(minv, 0xFF, n * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(minv_dirty, 0, sizeof(int), s));
   } else {
@@ -352,6 +353,7 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
                                                P.logk0, P.ob, (uint32_t)P.cap, !use_tiles,
                                                minv_dirty);
   h.minv_clean = minv;
+  h.minv_clean_n = n;
   if (!use_tiles && !cc_slots && T > 0)
     k_register_slots<<<grid_for(T), kBlock, 0, s>>>(T, io.nslots, rpos, sl, ctr, P.logk0, P.ob,
                                                     (uint32_t)P.cap);

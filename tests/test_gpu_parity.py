@@ -422,6 +422,25 @@ def test_tile_levels_overflow_fallback(rst, monkeypatch):
     g.close()
 
 
+def test_handle_reuse_across_graph_sizes(rst, O):
+    # one handle, graphs of shrinking and growing size, many and few
+    # components: per-build state kept between builds (the Euler min table,
+    # clean slot buffers) must never leak from one graph into the next
+    sparse = O.gen("random", 150000, 0.000003, seed=5)  # ~116K components: flagged table
+    gs = [O.gen("kron", 13), O.gen("grid", 20, 30), O.gen("kron", 13), sparse,
+          O.gen("random", 3000, 0.002, seed=4), sparse, O.gen("path", 9000), O.gen("kron", 12)]
+    h = rst.DeviceGraph.from_host(gs[0].n, np.stack([gs[0].eu, gs[0].ev], 1))
+    for g in gs:
+        root = int(np.argmax(np.diff(g.offsets)))
+        h.upload(g.n, np.stack([g.eu, g.ev], 1))
+        for algo in (1, 0, 1):  # cc-euler, BFS (borrows the min table), cc-euler
+            p, r, _, _ = h.run(algo, root)
+            ep, er, _ = O.run(g, algo, root)
+            assert np.array_equal(p, ep), (g.n, algo)
+            assert np.array_equal(r, er), (g.n, algo)
+    h.close()
+
+
 def test_step_counts_rerun_identical(rst, O):
     # acceptance.cpp:330-363 (criterion 7): parents, steps and work are
     # bit-identical across reruns -- with the CSR given or built on the

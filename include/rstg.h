@@ -62,13 +62,18 @@ int rstg_device_count(int* count);
 /* Graph from the reference's host arrays (int64): offsets[n+1],
  * neighbors[2m], edge_origin[2m], edges_uv[2m] (u,v interleaved, normalized:
  * u < v, lexicographically sorted, unique). CSR arrays may be NULL: the CSR
- * is then built on the device from edges_uv. */
+ * is then built on the device from edges_uv, and edges_uv is checked on the
+ * device like build_csr (graph.cpp:145-156): RSTG_ERR_ARG with "edge
+ * endpoint out of range", "self-loop in normalized EdgeList" or "EdgeList
+ * not normalized". */
 int rstg_graph_create(const int64_t* offsets, const int64_t* neighbors,
                       const int64_t* edge_origin, const int64_t* edges_uv, int64_t n,
                       int64_t m, int device, rstg_graph** out);
 /* Re-upload a graph of the same kind into an existing handle (reuses its
- * device buffers and workspace when n and m are unchanged). Pinned host
- * buffers are read directly by the device (zero-copy narrowing). */
+ * device buffers and workspace when n and m are unchanged). edges_uv streams
+ * through two device staging buffers (cudaMemcpyAsync of chunk k+1 overlaps
+ * the narrowing of chunk k); pinned CSR arrays are read directly by the
+ * narrowing kernel, pageable ones are staged. */
 int rstg_graph_upload(rstg_graph* g, const int64_t* offsets, const int64_t* neighbors,
                       const int64_t* edge_origin, const int64_t* edges_uv, int64_t n, int64_t m);
 /* Graph from device-resident int32 arrays (copied into the handle).
@@ -88,7 +93,8 @@ int rstg_graph_destroy(rstg_graph* g);
 int rstg_set_stream(rstg_graph* g, void* cuda_stream);
 /* Per-phase CUDA-event timing (read with rstg_phase_times). */
 int rstg_set_timing(rstg_graph* g, int enabled);
-/* JSON object {"phase": ms, ...} of the last run. */
+/* JSON object of the last run, one entry per phase:
+ * {"phase": [ms, launches_of_the_phase, algorithmic_bytes], ...}. */
 int rstg_phase_times(rstg_graph* g, char* buf, int64_t cap);
 
 /* run_algorithm (bench.cpp:38-54): parent_out[n] (P[r] = r); levels_out[n]
@@ -105,7 +111,10 @@ int rstg_cc_spanning_forest(rstg_graph* g, int64_t* labels_out, int64_t* tree_ed
                             int64_t* num_tree_edges, rstg_stats* stats);
 
 /* euler_root_forest(n, tree_edges, labels, designated_root) on `device`.
- * tree_uv: T edges as (u,v) pairs; designated_root -1 = none. */
+ * tree_uv: T edges as (u,v) pairs; designated_root -1 = none. Checks in the
+ * reference's order: label count, designated root, (labels in [0, n)),
+ * "edge count does not match a spanning forest of the labeling", then
+ * "list ranking failed to converge: not a forest". */
 int rstg_euler_root_forest(int64_t n, const int64_t* tree_uv, int64_t T, const int64_t* labels,
                            int64_t nlabels, int64_t designated_root, int device,
                            int64_t* parent_out, int64_t* roots_out, int64_t* num_roots);

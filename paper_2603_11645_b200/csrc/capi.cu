@@ -24,6 +24,7 @@ void generate_device(Handle& h, int kind, int64_t a, int64_t b, double p, bool b
 void widen_to_host(Handle& h, const int32_t* dev, int64_t count, int64_t* host);
 int64_t forest_depth_device(Handle& h, const int32_t* parent, int32_t* depth, uint32_t* rootmax,
                             int64_t* cycle_vertex);
+int64_t root_depths(Handle& h, const int32_t* parent, uint32_t* rootmax, int64_t n);
 void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_base,
                  const int32_t* rep, unsigned long long* slot, int* any_prop);
 void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tflag,
@@ -474,26 +475,21 @@ int rstg_euler_root_forest(int64_t n, const int64_t* tree_uv, int64_t T, const i
     if (nlabels != n) throw AlgoError("labels size does not match vertex count");
     if (designated_root != -1 && (designated_root < 0 || designated_root >= n))
       throw AlgoError("designated root out of range");
-    // Tree edges as a graph: orient, sort (arc order never changes parents).
-    std::vector<int64_t> uv((size_t)(2 * T));
-    std::vector<std::pair<int64_t, int64_t>> es((size_t)T);
-    for (int64_t i = 0; i < T; ++i) {
-      int64_t a = tree_uv[2 * i], b = tree_uv[2 * i + 1];
-      if (a < 0 || a >= n || b < 0 || b >= n) throw AlgoError("tree edge endpoint out of range");
-      es[(size_t)i] = {std::min(a, b), std::max(a, b)};
-    }
-    std::sort(es.begin(), es.end());
-    bool simple = std::adjacent_find(es.begin(), es.end()) == es.end();
-    for (auto& e : es) simple = simple && e.first != e.second;
-    for (int64_t i = 0; i < T; ++i) {
-      uv[(size_t)(2 * i)] = es[(size_t)i].first;
-      uv[(size_t)(2 * i + 1)] = es[(size_t)i].second;
-    }
+    // Tree edges as a graph: oriented, sorted and deduplicated on the device
+    // (arc order never changes parents); labels narrowed with a range check.
     rstg_graph gg(device);
     Handle& h = gg.h;
-    upload_edges_build_csr(h, uv.data(), n, T);
     int32_t* lab = h.ws<int32_t>(WS_REP, n);
-    to_device<int32_t>(h, labels, n, lab);
+    const int64_t bad_label = upload_ids(h, labels, n, lab, n);
+    if (bad_label >= 0)
+      throw AlgoError("label out of range at vertex " + std::to_string(bad_label));
+    // the reference's order: the edge count (euler_rooting.cpp:205-208)
+    // before anything the tour construction could reject
+    const int64_t comps = count_labels(h, lab, n);
+    if (T != n - comps) throw AlgoError("edge count does not match a spanning forest of the labeling");
+    bool simple = true;
+    if (!upload_tree_edges(h, tree_uv, T, n, &simple))
+      throw AlgoError("tree edge endpoint out of range");
     int32_t* parent = h.ws<int32_t>(WS_PARENT, n);
     if (!simple) throw AlgoError("list ranking failed to converge: not a forest");
     const EulerIO io = euler_buffers(h, T, /*local_written=*/false);
@@ -533,11 +529,9 @@ int rstg_forest_depth(rstg_graph* g, const int64_t* parent, int64_t* depth_out,
   return guard([&] {
     Handle& h = g->h;
     const int64_t n = h.g.n;
-    for (int64_t v = 0; v < n; ++v)  // (range check before narrowing, like rstg_validate)
-      if (parent[v] < 0 || parent[v] >= n)
-        throw AlgoError("parent out of range at vertex " + std::to_string(v));
     int32_t* p = h.ws<int32_t>(WS_PARENT, n);
-    to_device<int32_t>(h, parent, n, p);
+    const int64_t bad = upload_ids(h, parent, n, p, n);  // (checked before use, like rstg_validate)
+    if (bad >= 0) throw AlgoError("parent out of range at vertex " + std::to_string(bad));
     int32_t* depth = h.ws<int32_t>(WS_ROOTS, n + 1);  // (WS_VAL_C is the readback staging)
     uint32_t* rootmax = h.ws<uint32_t>(WS_MINV, n);
     h.minv_clean = nullptr;  // (WS_MINV reused here)
@@ -554,14 +548,8 @@ int rstg_forest_depth(rstg_graph* g, const int64_t* parent, int64_t* depth_out,
       }
       throw AlgoError("parent array contains a cycle at vertex " + std::to_string(x));
     }
-    std::vector<uint32_t> rm((size_t)n);
-    CK(cudaMemcpy(rm.data(), rootmax, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    int64_t best = 0;
-    for (int64_t v = 0; v < n; ++v) {
-      if (root_max_out) root_max_out[v] = (parent[v] == v) ? (int64_t)rm[(size_t)v] : -1;
-      if (parent[v] == v) best = std::max<int64_t>(best, rm[(size_t)v]);
-    }
-    *max_depth = best;
+    *max_depth = root_depths(h, p, rootmax, n);  // rootmax[v] := -1 for non-roots
+    if (root_max_out) widen_to_host(h, reinterpret_cast<const int32_t*>(rootmax), n, root_max_out);
     if (depth_out) widen_to_host(h, depth, n, depth_out);
   });
 }
@@ -571,21 +559,14 @@ int rstg_validate(rstg_graph* g, const int64_t* parent, int64_t required_root, i
   return guard([&] {
     Handle& h = g->h;
     int32_t* p = h.ws<int32_t>(WS_PARENT, h.g.n);
-    // Range check on the host side of the ABI: out-of-range int64 values
-    // would wrap when narrowed.
-    int64_t bad = -1;
-    for (int64_t v = 0; v < h.g.n; ++v)
-      if (parent[v] < 0 || parent[v] >= h.g.n) {
-        bad = v;
-        break;
-      }
+    // Range check while narrowing (out-of-range int64 values would wrap).
+    const int64_t bad = upload_ids(h, parent, h.g.n, p, h.g.n);
     if (bad >= 0) {
       *valid = 0;
       *code = 1;
       *bad_vertex = bad;
       return;
     }
-    to_device<int32_t>(h, parent, h.g.n, p);
     int64_t bv = -1;
     const int c = validate_forest(h, p, (int32_t)required_root, &bv);
     *valid = c == 0;

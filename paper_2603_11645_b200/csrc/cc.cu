@@ -815,7 +815,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   const bool keyed = (h.round0_slots == slot && m > 0) || round0_keys_from_edges(h, slot);
   h.round0_slots = nullptr;
   const bool round0 = keyed || (h.g.has_csr() && m > 0);  // writes every rep itself
-  const bool slots_ok = keyed || h.slots_clean == slot;
+  const bool slots_ok = keyed || (h.slots_clean == slot && n <= h.slots_clean_n);
   h.slots_clean = nullptr;  // until this build completes
   h.timer.begin(h.stream, "cc.init", (round0 ? 0.0 : 4.0 * n) + (slots_ok ? 0.0 : 8.0 * n));
   if (!round0 || !slots_ok) {
@@ -954,6 +954,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   h.cc_lazy = false;
   h.stats.tree_edges = total;
   h.slots_clean = slot;
+  h.slots_clean_n = n;
   return total;
 }
 

@@ -93,6 +93,7 @@ class Handle {
   // every slot it consumes), so the next build skips re-initialising it;
   // any other user of the slot buffer clears this.
   const void* slots_clean = nullptr;
+  int64_t slots_clean_n = 0;  // ... for its first slots_clean_n entries (beyond: unknown)
   // Set by the edge upload: WS_SLOT already holds round 0's hook keys
   // (computed while the edges streamed in), consumed by cc_exact.
   const void* round0_slots = nullptr;
@@ -123,7 +124,7 @@ class Handle {
   // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,15] lr / tile ranking,
   // [16] pr bad mark, [17] edge-locality count, [18] pr crossing, [19] euler min-table
   // dirty flag (persists across builds), [20,22] cc roots, [30] bfs, [40] validate,
-  // [48] normalize, [50,53) capi/lr verify, [128,160) jump-round flags.
+  // [48] normalize, [50,53) capi/lr verify, [54,57) edge-upload input checks, [57] upload_ids, [128,160) jump-round flags.
   int64_t* dev_box = nullptr;
 
   // Copies `count` int64 device values into host_box and syncs the stream.
@@ -276,6 +277,14 @@ __device__ __forceinline__ uint32_t arc_rev(uint32_t p, uint32_t nslots) {
 }
 #endif
 
+// Caller int64 ids -> device int32, range-checked on the device against
+// [0, hi): returns the index of the first out-of-range value, -1 if none.
+int64_t upload_ids(Handle& h, const int64_t* host, int64_t count, int32_t* dev, int64_t hi);
+// Host int64 (u, v) pairs of an explicit forest -> h.g.edges, oriented,
+// sorted and deduplicated on the device (the graph's CSR is left pending).
+// Returns false on an endpoint outside [0, n); *simple is false when a
+// self-loop or duplicate edge was dropped.
+bool upload_tree_edges(Handle& h, const int64_t* tree_uv, int64_t T, int64_t n, bool* simple);
 // Builds a pending CSR (uploads defer it: cc-euler never needs it).
 void ensure_csr(Handle& h);
 
@@ -300,6 +309,8 @@ void cc_labels_fast(Handle& h, int32_t* labels);
 //             reached, ruler lists acyclic), else the reference's errors.
 void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, int64_t T,
                 bool cc_slots, int32_t designated_root, int32_t* parent, bool verify = false);
+// Number of distinct labels among labels[0, n) (each in [0, n)).
+int64_t count_labels(Handle& h, const int32_t* labels, int64_t n);
 // EulerIO buffers of the handle for N slots; the remote lists reset to
 // NONE, the local ones too unless round 0 will write them (local_written).
 EulerIO euler_buffers(Handle& h, int64_t N, bool local_written);

@@ -58,6 +58,28 @@ __global__ void k_mark_labels(int64_t n, const int32_t* __restrict__ lab, uint8_
     present[lab[v]] = 1;
 }
 
+__global__ void k_count_present(int64_t n, const uint8_t* __restrict__ present,
+                                unsigned long long* count) {
+  unsigned c = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    c += present[v];
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+int64_t count_labels(Handle& h, const int32_t* labels, int64_t n) {
+  if (n == 0) return 0;
+  uint8_t* present = h.ws<uint8_t>(WS_ISROOT, n);
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h.dev_box) + 4;
+  CK(cudaMemsetAsync(present, 0, (size_t)n, h.stream));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(*cnt), h.stream));
+  k_mark_labels<<<grid_for(n), kBlock, 0, h.stream>>>(n, labels, present);
+  k_count_present<<<grid_for(n), kBlock, 0, h.stream>>>(n, present, cnt);
+  CK_LAUNCH();
+  h.read_box(reinterpret_cast<int64_t*>(cnt), 1);
+  return h.host_box[0];
+}
+
 // Vertex pass, in tiles of kFixItems x kBlock vertices claimed in order:
 //   * min_vertex per label (euler_rooting.cpp:190-195): lanes sharing a
 //     label (one giant component: all of them) issue one atomicMin;

@@ -13,6 +13,7 @@
 //     exactly the host generators' edge lists.
 // Sorting here (normalize, back-arc grouping) uses CUB's radix sort: graph
 // ingestion is outside the RST hot path.
+#include <algorithm>
 #include <cub/cub.cuh>
 
 #include "engine.hpp"
@@ -67,6 +68,41 @@ void widen_to_host(Handle& h, const int32_t* dev, int64_t count, int64_t* host) 
 // int64 host array -> device int32/uint32. Pinned sources are read directly
 // by the narrowing kernel (zero-copy over the host link); pageable ones go
 // through a staging buffer.
+// Checked variant (caller id arrays): every value must lie in [0, hi); the
+// index of the first one that does not is returned (-1: all in range).
+__global__ void k_narrow_checked(int64_t count, const long long* __restrict__ in, int32_t* out,
+                                 int64_t base, long long hi, long long* first_bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const long long v = in[i];
+    if (v < 0 || v >= hi) atomicMin(first_bad, (long long)(base + i));
+    out[i] = (int32_t)v;
+  }
+}
+int64_t upload_ids(Handle& h, const int64_t* host, int64_t count, int32_t* dev, int64_t hi) {
+  if (count <= 0) return -1;
+  long long* bad = reinterpret_cast<long long*>(h.dev_box + 57);
+  const long long inf = INT64_MAX;
+  CK(cudaMemcpyAsync(bad, &inf, sizeof(inf), cudaMemcpyHostToDevice, h.stream));
+  if (is_pinned(host)) {
+    k_narrow_checked<<<grid_for(count), kBlock, 0, h.stream>>>(
+        count, reinterpret_cast<const long long*>(host), dev, 0, hi, bad);
+    CK_LAUNCH();
+  } else {
+    const int64_t chunk = int64_t{1} << 24;
+    long long* stage = h.ws<long long>(WS_VAL_C, std::min(count, chunk));
+    for (int64_t off = 0; off < count; off += chunk) {
+      const int64_t c = std::min(chunk, count - off);
+      CK(cudaMemcpyAsync(stage, host + off, c * sizeof(int64_t), cudaMemcpyHostToDevice, h.stream));
+      k_narrow_checked<<<grid_for(c), kBlock, 0, h.stream>>>(c, stage, dev + off, off, hi, bad);
+      CK_LAUNCH();
+      if (off + c < count) CK(cudaStreamSynchronize(h.stream));  // stage reused
+    }
+  }
+  h.read_box(reinterpret_cast<int64_t*>(bad), 1);
+  return h.host_box[0] == INT64_MAX ? -1 : h.host_box[0];
+}
+
 template <class T>
 static void upload_narrow(Handle& h, const int64_t* host, int64_t count, T* dev) {
   if (count <= 0) return;
@@ -277,6 +313,20 @@ int64_t normalize_keys_device(Handle& h, unsigned long long* keys, int64_t count
   return m;
 }
 
+bool upload_tree_edges(Handle& h, const int64_t* tree_uv, int64_t T, int64_t n, bool* simple) {
+  alloc_graph(h, n, T, 2 * T < (int64_t{1} << 32));
+  h.g.csr_pending = h.g.offsets != nullptr;
+  *simple = true;
+  if (T == 0) return true;
+  unsigned long long* keys = h.ws<unsigned long long>(WS_VAL_A, T);
+  int2* raw = reinterpret_cast<int2*>(keys);  // (packed in place below)
+  if (upload_ids(h, tree_uv, 2 * T, reinterpret_cast<int32_t*>(raw), n) >= 0) return false;
+  k_pack_keys<<<grid_for(T), kBlock, 0, h.stream>>>(T, raw, keys);
+  CK_LAUNCH();
+  *simple = normalize_keys_device(h, keys, T, n, h.g.edges) == T;
+  return true;
+}
+
 // ------------------------------------------------------ device generators
 namespace {
 struct GridCount {  // grid (graph.cpp:198-210) and road mesh
@@ -453,15 +503,40 @@ void generate_kron_part(Handle& h, int scale, int ef, int part, int nparts) {
 // singleton, min-mode hooking offers slot[v] the key (u << 32 | e) (u < v
 // in a normalized list), the smallest of which is v's first neighbour --
 // exactly what the CSR-direct round 0 reads (cc.cu).
+//
+// It also checks the input the way build_csr does (graph.cpp:145-156): the
+// first edge (in list order) with an endpoint out of [0, n) or a self-loop
+// is recorded in err[0] / err[1] (atomicMin of its index) and gets no key;
+// err[2] is raised when an edge is not strictly above its predecessor
+// (unsorted or duplicate: "EdgeList not normalized").
 __global__ void k_narrow_edges(int64_t count, const long long* __restrict__ in, int2* out,
-                               uint32_t e_first, unsigned long long* slot) {
+                               uint32_t e_first, int64_t n, unsigned long long* slot,
+                               long long* err, int2 prev_last) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int2 e = make_int2((int)in[2 * i], (int)in[2 * i + 1]);
+    const long long u = in[2 * i], v = in[2 * i + 1];
+    const int64_t id = (int64_t)e_first + i;
+    if (u < 0 || u >= n || v < 0 || v >= n) {
+      atomicMin(&err[0], (long long)id);
+      out[i] = make_int2(0, 0);
+      continue;
+    }
+    if (u == v) atomicMin(&err[1], (long long)id);
+    const int2 e = make_int2((int)u, (int)v);
     out[i] = e;
-    if (e.x < e.y) {
-      const unsigned long long key = pack_key((uint32_t)e.x, e_first + (uint32_t)i);
-      if (key < slot[e.y]) atomicMin(&slot[e.y], key);
+    long long pu, pv;
+    if (i > 0) {
+      pu = in[2 * i - 2];
+      pv = in[2 * i - 1];
+    } else {
+      pu = prev_last.x;
+      pv = prev_last.y;
+    }
+    if ((i > 0 || e_first > 0) && !(pu < u || (pu == u && pv < v))) err[2] = 1;
+    if (e.x != e.y) {  // (build_csr admits u > v: the loser is max(u, v) either way)
+      const int lo = min(e.x, e.y), hi = max(e.x, e.y);
+      const unsigned long long key = pack_key((uint32_t)lo, (uint32_t)id);
+      if (key < slot[hi]) atomicMin(&slot[hi], key);
     }
   }
 }
@@ -486,15 +561,16 @@ __global__ void k_round0_keys(int64_t m, const int2* __restrict__ edges, uint32_
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int2 e = edges[i];
-    if (e.x < e.y) {
-      const unsigned long long key = pack_key((uint32_t)e.x, e_base + (uint32_t)i);
-      if (key < slot[e.y]) atomicMin(&slot[e.y], key);
+    if (e.x != e.y) {
+      const int lo = min(e.x, e.y), hi = max(e.x, e.y);
+      const unsigned long long key = pack_key((uint32_t)lo, e_base + (uint32_t)i);
+      if (key < slot[hi]) atomicMin(&slot[hi], key);
     }
   }
 }
 bool round0_keys_from_edges(Handle& h, unsigned long long* slot) {
   if (!h.g.csr_pending || h.g.m == 0) return false;
-  if (h.slots_clean != slot) {
+  if (h.slots_clean != slot || h.g.n > h.slots_clean_n) {
     k_fill_u64<<<grid_for(h.g.n), kBlock, 0, h.stream>>>(h.g.n, slot, kKeyInf);
     CK_LAUNCH();
   }
@@ -513,7 +589,7 @@ void upload_edges_build_csr(Handle& h, const int64_t* edges_uv, int64_t n, int64
   h.g.csr_pending = h.g.offsets != nullptr;
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
   const cudaStream_t s = h.stream;
-  if (h.slots_clean != slot && n > 0) {
+  if ((h.slots_clean != slot || n > h.slots_clean_n) && n > 0) {
     k_fill_u64<<<grid_for(n), kBlock, 0, s>>>(n, slot, kKeyInf);
     CK_LAUNCH();
   }
@@ -524,6 +600,10 @@ void upload_edges_build_csr(Handle& h, const int64_t* edges_uv, int64_t n, int64
     if (!h.copy_stream) CK(cudaStreamCreateWithFlags(&h.copy_stream, cudaStreamNonBlocking));
     const int64_t chunk = int64_t{1} << 22;  // edges per staging buffer (32 MB of int64 pairs)
     long long* stage = h.ws<long long>(WS_VAL_C, 2 * 2 * chunk);
+    long long* err = reinterpret_cast<long long*>(h.dev_box + 54);  // [54,57): input checks
+    const long long err_init[3] = {INT64_MAX, INT64_MAX, 0};
+    CK(cudaMemcpyAsync(err, err_init, sizeof(err_init), cudaMemcpyHostToDevice, s));
+    int2 last = make_int2(0, 0);
     cudaEvent_t copied[2], consumed[2];
     for (int b = 0; b < 2; ++b) {
       CK(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
@@ -539,14 +619,30 @@ void upload_edges_build_csr(Handle& h, const int64_t* edges_uv, int64_t n, int64
                          h.copy_stream));
       CK(cudaEventRecord(copied[b], h.copy_stream));
       CK(cudaStreamWaitEvent(s, copied[b], 0));
-      k_narrow_edges<<<grid_for(c), kBlock, 0, s>>>(c, buf, h.g.edges + off, (uint32_t)off, slot);
+      k_narrow_edges<<<grid_for(c), kBlock, 0, s>>>(c, buf, h.g.edges + off, (uint32_t)off, n,
+                                                     slot, err, last);
       CK_LAUNCH();
       CK(cudaEventRecord(consumed[b], s));
+      // the chunk's last edge, for the next chunk's order check (host copy:
+      // the source array is the caller's)
+      last = make_int2((int)std::clamp<int64_t>(edges_uv[2 * (off + c) - 2], -1, n),
+                       (int)std::clamp<int64_t>(edges_uv[2 * (off + c) - 1], -1, n));
     }
     CK(cudaStreamSynchronize(s));
     for (int b = 0; b < 2; ++b) {
       cudaEventDestroy(copied[b]);
       cudaEventDestroy(consumed[b]);
+    }
+    h.read_box(reinterpret_cast<int64_t*>(err), 3);
+    const int64_t bad_range = h.host_box[0], bad_loop = h.host_box[1], unsorted = h.host_box[2];
+    if (bad_range != INT64_MAX || bad_loop != INT64_MAX || unsorted) {
+      // the reference's build_csr order: per edge range then self-loop, then the sort check
+      const char* what = bad_range < bad_loop ? "edge endpoint out of range"
+                         : bad_loop != INT64_MAX ? "self-loop in normalized EdgeList"
+                                                 : "EdgeList not normalized";
+      h.free_graph();
+      h.slots_clean = nullptr;
+      throw ArgError(what);
     }
     h.round0_slots = slot;
   } else if (h.g.offsets) {

@@ -190,6 +190,30 @@ __global__ void k_depth_finish(int64_t n, const int2* __restrict__ jd, const int
   }
 }
 
+// Per-root maxima in the reference's layout (rooted_forest.cpp: -1 for a
+// non-root) and the deepest tree's depth.
+__global__ void k_root_depths(int64_t n, const int32_t* __restrict__ parent, uint32_t* rootmax,
+                              unsigned int* best) {
+  unsigned int b = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (parent[v] == (int32_t)v)
+      b = max(b, rootmax[v]);
+    else
+      rootmax[v] = 0xFFFFFFFFu;  // (int32 -1 when widened)
+  }
+  b = __reduce_max_sync(0xffffffffu, b);
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(best, b);
+}
+int64_t root_depths(Handle& h, const int32_t* parent, uint32_t* rootmax, int64_t n) {
+  unsigned int* best = reinterpret_cast<unsigned int*>(h.dev_box + 42);
+  CK(cudaMemsetAsync(h.dev_box + 42, 0, sizeof(int64_t), h.stream));
+  if (n > 0) k_root_depths<<<grid_for(n), kBlock, 0, h.stream>>>(n, parent, rootmax, best);
+  CK_LAUNCH();
+  h.read_box(h.dev_box + 42, 1);
+  return (int64_t)*reinterpret_cast<unsigned int*>(h.host_box);
+}
+
 int64_t forest_depth_device(Handle& h, const int32_t* parent, int32_t* depth, uint32_t* rootmax,
                             int64_t* cycle_vertex) {
   const int64_t n = h.g.n;

@@ -71,7 +71,7 @@ def distributed_cc(kernels, n: int, device, world: int = 1, max_rounds: int | No
     slot = torch.empty(n, dtype=torch.int64, device=device)
     kernels.init(rep, slot)
     mode, rounds, hooks = 0, 0, 0
-    limit = max_rounds if max_rounds is not None else n + 2
+    limit = max_rounds if max_rounds is not None else n + 1  # cc_forest.cpp:88
     while True:
         if rounds > limit:
             raise RuntimeError("hooking failed to converge")

@@ -488,3 +488,78 @@ def test_forest_depth_device(rst, O):
     with pytest.raises(O.OracleError, match="cycle at vertex 5"):
         O.forest_depth(tail)
     dg.close()
+
+
+def test_handle_reuse_unconsumed_upload(rst, O):
+    # an upload whose round-0 keys are never consumed,
+    # then a smaller graph that completes cc-euler, then a larger one: the
+    # slot entries past the smaller graph's n must not leak into the third
+    a, b, c = O.gen("kron", 12), O.gen("grid", 20, 25), O.gen("road", 70)
+    h = rst.DeviceGraph.from_host(a.n, np.stack([a.eu, a.ev], 1))  # keys left in the slots
+    for g in (b, c, a, b, a):
+        h.upload(g.n, np.stack([g.eu, g.ev], 1))
+        p, r, _, _ = h.run(1, 0)
+        ep, er, _ = O.run(g, 1, 0)
+        assert np.array_equal(p, ep) and np.array_equal(r, er), g.n
+    # uploads never consumed in between, larger then smaller
+    h.upload(a.n, np.stack([a.eu, a.ev], 1))
+    h.upload(b.n, np.stack([b.eu, b.ev], 1))
+    p, r, _, _ = h.run(1, 0)
+    assert np.array_equal(p, O.run(b, 1, 0)[0])
+    h.upload(a.n, np.stack([a.eu, a.ev], 1))
+    for algo in ALGOS:
+        assert np.array_equal(h.run(algo, 0)[0], O.run(a, algo, 0)[0]), algo
+    h.close()
+
+
+def test_edge_upload_rejects_bad_edge_lists(rst, O):
+    # build_csr's argument checks (graph.cpp:145-156),
+    # on the device, in the reference's order, for the edge-list upload
+    ok = np.array([[0, 1], [1, 2], [2, 3]], np.int64)
+    cases = [
+        (np.array([[0, 1], [1, 7], [2, 3]]), "edge endpoint out of range"),
+        (np.array([[0, 1], [-1, 2], [2, 3]]), "edge endpoint out of range"),
+        (np.array([[0, 1], [2, 2], [2, 3]]), "self-loop in normalized EdgeList"),
+        (np.array([[0, 1], [2, 2], [2, 9]]), "self-loop in normalized EdgeList"),  # first offender
+        (np.array([[0, 1], [2, 3], [1, 2]]), "EdgeList not normalized"),
+        (np.array([[0, 1], [1, 2], [1, 2]]), "EdgeList not normalized"),  # duplicate
+    ]
+    for edges, msg in cases:
+        with pytest.raises(rst.RSTArgError, match=msg):
+            rst.DeviceGraph.from_host(4, edges.astype(np.int64))
+    h = rst.DeviceGraph.from_host(4, ok)
+    with pytest.raises(rst.RSTArgError, match="edge endpoint out of range"):
+        h.upload(4, np.array([[0, 1], [1, 4]], np.int64))
+    # the handle is usable again after a rejected upload
+    h.upload(4, ok)
+    assert list(h.run(1, 0)[0]) == [0, 0, 1, 2]
+    h.close()
+    # chunk boundaries (4M edges per staging chunk): an order violation
+    # exactly across the boundary is seen
+    g = O.gen("path", (1 << 22) + 3)
+    e = np.stack([g.eu, g.ev], 1).copy()
+    e[[(1 << 22) - 1, 1 << 22]] = e[[1 << 22, (1 << 22) - 1]]
+    with pytest.raises(rst.RSTArgError, match="EdgeList not normalized"):
+        rst.DeviceGraph.from_host(g.n, e)
+
+
+def test_euler_root_forest_error_order(rst, O):
+    # the edge count is checked before the tour
+    # (euler_rooting.cpp:205-208); duplicate/self-loop tree edges with the
+    # right count fail in list ranking; labels out of range are rejected
+    with pytest.raises(rst.RSTError, match="edge count does not match a spanning forest"):
+        rst.euler_root_forest(3, [(0, 1), (0, 1), (1, 2)], [0, 0, 0], -1)
+    with pytest.raises(rst.RSTError, match="edge count does not match a spanning forest"):
+        rst.euler_root_forest(4, [(0, 1), (2, 2), (2, 3)], [0, 0, 0, 0], -1)
+    with pytest.raises(rst.RSTError, match="list ranking failed to converge: not a forest"):
+        rst.euler_root_forest(3, [(0, 1), (0, 1)], [0, 0, 0], -1)
+    with pytest.raises(rst.RSTError, match="list ranking failed to converge: not a forest"):
+        rst.euler_root_forest(3, [(0, 1), (2, 2)], [0, 0, 0], -1)
+    with pytest.raises(rst.RSTError, match="label out of range at vertex 1"):
+        rst.euler_root_forest(3, [(0, 1), (1, 2)], [0, 5, 0], -1)
+    with pytest.raises(rst.RSTError, match="label out of range at vertex 2"):
+        rst.euler_root_forest(3, [(0, 1), (1, 2)], [0, 0, -1], -1)
+    # unsorted, reversed tree edges are fine (arc order never changes parents)
+    p, r = rst.euler_root_forest(4, [(3, 2), (1, 0), (2, 0)], [0] * 4, 3)
+    ep, er = O.euler_root_forest(4, [(3, 2), (1, 0), (2, 0)], [0] * 4, 3)
+    assert np.array_equal(p, ep) and list(r) == [3]

@@ -11,7 +11,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
 PKG := paper_2603_11645_b200
 CSRC := $(PKG)/csrc
 OBJDIR := build/obj
-CU := engine cc listrank tilerank euler pr bfs validate graph capi
+CU := engine cc listrank tilerank euler euler_api pr bfs validate graph capi
 OBJS := $(patsubst %,$(OBJDIR)/%.o,$(CU))
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) include/rstg.h
 
@@ -42,6 +42,17 @@ build/rst_bench: $(HOST)/benchmarks/rst_bench.cpp $(PKG)/librst_b200.so
 build/rst_acceptance: $(HOST)/tests/acceptance.cpp $(PKG)/librst_b200.so
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) $< -o $@ -L$(PKG) -lrst_b200 -lrstg -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+# The reference's OWN acceptance suite (proj/tests/acceptance.cpp), compiled
+# unchanged against the rst:: mirror headers and linked to the GPU library:
+# built only where the reference sources exist (the binary travels to the box).
+REF_TESTS ?= /root/reference/proj/tests
+ifneq ($(wildcard $(REF_TESTS)/acceptance.cpp),)
+all: build/ref_acceptance
+build/ref_acceptance: $(REF_TESTS)/acceptance.cpp $(REF_TESTS)/oracles.hpp $(PKG)/librst_b200.so
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -I$(REF_TESTS) $< -o $@ -L$(PKG) -lrst_b200 -lrstg -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+endif
 
 lib: $(PKG)/librstg.so
 

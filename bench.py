@@ -43,12 +43,16 @@ WORKLOADS = {
     "kron26cc": ("kron:26:16", None, 4),
     "kron24cc": ("kron:24:16", None, 4),
 }
-REF_SAMPLE = {  # bounded CPU samples of each workload for the reference arm
-    "road": ("road", 2449),
+REF_SAMPLE = {  # the reference arm times the SAME graph as the GPU arm
+    "road": ("road", 4899),
     "grid": ("grid", 1024, 1024),
-    "path": ("path", 1 << 20),
-    "rmat24": ("kron", 18),
+    "path": ("path", 1 << 24),
+    "rmat24": ("kron", 24, 16),
 }
+# bench_row protocol of the reference (bench.cpp:56-92): 1 warm-up + 5 timed
+# runs, median. The reference arm caps K and W at these (a road build is
+# ~15 s on 16 cores), and says so in its line.
+REF_MAX_TIMED, REF_MAX_WARMUP = 5, 1
 ALGO_ID = {"bfs": 0, "cc-euler": 1, "pr-rst": 2}
 
 
@@ -211,12 +215,15 @@ def measured_peaks():
 # ------------------------------------------------------------- cpu side
 def cpu_reference(workload, algo, steps, warmup, cores=None):
     """The reference's own CPU implementation (oracle/_ref, compiled from
-    /root/reference) on a bounded sample of the workload; edges/s."""
+    /root/reference) on the same graph as the GPU arm; edges/s. Times
+    exactly what bench_row times (bench.cpp:73-76): run_algorithm including
+    its StepEngine construction, `cores` workers (default: every host core)."""
     import numpy as np
     import oracle as O
 
     cores = cores or os.cpu_count() or 1
     spec = REF_SAMPLE[workload]
+    t0 = time.perf_counter()
     g = O.gen(*spec)
     root = 0
     if WORKLOADS[workload][1] == "maxdeg":
@@ -225,35 +232,41 @@ def cpu_reference(workload, algo, steps, warmup, cores=None):
     times = []
     if kind == "reference":
         rg = O.RefGraph(g)
+        setup_s = time.perf_counter() - t0
         for i in range(warmup + steps):
             ms = rg.run_ms(ALGO_ID[algo], root, cores, 5)
             if i >= warmup:
                 times.append(ms)
+        del rg
     else:
+        setup_s = time.perf_counter() - t0
         cores = 1
         for i in range(warmup + steps):
-            t0 = time.perf_counter()
+            t1 = time.perf_counter()
             O.run(g, ALGO_ID[algo], root)
             if i >= warmup:
-                times.append((time.perf_counter() - t0) * 1e3)
+                times.append((time.perf_counter() - t1) * 1e3)
     med = statistics.median(times)
     return {
         "value": g.m / (med / 1e3), "unit": "edges/s", "cores": cores, "kind": kind,
-        "sample": f"{':'.join(map(str, spec))} (n={g.n}, m={g.m}), root {root}, {algo}, "
-                  f"median of {len(times)} runs of run_algorithm with {cores} workers",
-        "ms": med,
+        "sample": f"{':'.join(map(str, spec))} (n={g.n}, m={g.m}, the GPU arm's graph), root {root}, "
+                  f"{algo}, median of {len(times)} timed runs after {warmup} warm-up of run_algorithm "
+                  f"with {cores} workers",
+        "ms": med, "runs_ms": [round(t, 1) for t in times], "graph_setup_s": round(setup_s, 2),
     }
 
 
 # ------------------------------------------------------- kron CC (multi-GPU)
 def bench_kron_cc(args, rank, world, dev, metric, config):
     """Config 5: exact connectivity of a Kronecker graph, edges partitioned
-    over the ranks (paper_2603_11645_b200/distcc.py). Strong scaling: the
-    graph is fixed, each rank holds 1/N of the edges."""
+    over the ranks (paper_2603_11645_b200/distcc.py): the single-GPU rounds
+    of rstg_cc_labels with a MIN all-reduce of the hook slots before each
+    apply (dense in round 0, the current roots' slots after). Strong
+    scaling: the graph is fixed, each rank holds 1/N of the edges."""
     import torch
 
     import paper_2603_11645_b200 as P
-    from paper_2603_11645_b200.distcc import GpuKernels, distributed_cc, edge_base
+    from paper_2603_11645_b200.distcc import SlotExchange, distributed_cc, edge_base
 
     spec = WORKLOADS[args.workload][0]
     t0 = time.perf_counter()
@@ -266,19 +279,25 @@ def bench_kron_cc(args, rank, world, dev, metric, config):
         dist.all_reduce(m_local)
     m_total, n = int(m_local.item()), dg.n
     gen_s = time.perf_counter() - t0
-    kern = GpuKernels(dg)
+    ex = SlotExchange(n, "cuda", world) if world > 1 else None
+
+    def step():
+        if ex is not None:
+            ex.calls.clear()
+        return distributed_cc(dg, n, world, None, ex)
+
     for _ in range(args.warmup):
-        distributed_cc(kern, n, "cuda", world)
+        step()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    rounds = hooks = 0
+    st = None
     with ClockSampler(dev) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            rep, rounds, hooks = distributed_cc(kern, n, "cuda", world)
+            rep, st = step()
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -290,12 +309,18 @@ def bench_kron_cc(args, rank, world, dev, metric, config):
     comps = int((rep == torch.arange(n, device="cuda", dtype=torch.int32)).sum().item())
     peaks, peak_kind = measured_peaks()
     b_cc = 8 * m_total + 4 * n  # read edges once + write labels
+    # phase breakdown of one instrumented (untimed) step
+    dg.set_timing(True)
+    step()
+    phases = dg.phase_times()
+    dg.set_timing(False)
     if rank == 0:
         config.update({"n": n, "m": m_total, "edges_per_rank": "1/N by smaller endpoint",
-                       "rounds": rounds, "tree_edges": hooks, "components": comps,
+                       "rounds": st["rounds"], "tree_edges": st["tree_edges"], "components": comps,
                        "generation_s": round(gen_s, 2),
-                       "exchange": "NCCL all_reduce(int64 MIN) of the 8n-byte hook slots per round"
-                       if world > 1 else "none (1 GPU)"})
+                       "exchange": ("NCCL all_reduce(int64 MIN): dense 8n bytes in round 0, "
+                                    "then 8 B per current root") if world > 1 else "none (1 GPU)",
+                       "exchange_bytes_per_rank": ex.bytes_per_rank() if ex else 0})
         line = {"metric": f"CC edges/sec ({args.workload}, edge-partitioned)",
                 "value": m_total / (ms_per_step / 1e3), "unit": "edges/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -303,8 +328,9 @@ def bench_kron_cc(args, rank, world, dev, metric, config):
                 "dtype": "int32", "data": "synthetic", "config": config,
                 "step_roofline": {"b_alg": b_cc,
                                   "frac_of_measured": b_cc / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"]},
+                "phases_ms_per_step": {k: [round(v[0], 4), v[1], v[2]] for k, v in phases.items()},
                 "clocks": clk.summary(), "cpu_baseline": None, "e2e": None}
-    per_step = count_kernels(lambda: distributed_cc(kern, n, "cuda", world))
+    per_step = count_kernels(step)
     if rank == 0:
         line["gpu_launches"] = per_step * args.steps if per_step is not None else None
         line["gpu_launches_source"] = "CUPTI kernel records of one untimed step x steps"
@@ -332,9 +358,14 @@ def main():
         # The reference arm: rank 0 only, the box's host cores.
         if rank != 0:
             return
-        cb = cpu_reference(args.workload, args.algo, args.steps, args.warmup)
+        k, w = min(args.steps, REF_MAX_TIMED), min(args.warmup, REF_MAX_WARMUP)
+        cb = cpu_reference(args.workload, args.algo, k, w)
         line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "edges/s",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "n_gpus": args.gpus, "steps": k, "warmup": w,
+                "requested": {"steps": args.steps, "warmup": args.warmup},
+                "protocol": "bench_row (bench.cpp:56-92): median of the timed runs; K and W capped "
+                            f"at {REF_MAX_TIMED} and {REF_MAX_WARMUP}",
+                "runs_ms": cb["runs_ms"], "graph_setup_s": cb["graph_setup_s"],
                 "ms_per_step": cb["ms"], "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": config,
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -491,7 +522,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference(args.workload, args.algo, 3, 1)
+            cb = cpu_reference(args.workload, args.algo, 1, 1)  # ~30 s of host work on road
             cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # the checker is optional on the box
             cpu = {"error": str(ex)}

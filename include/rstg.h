@@ -16,9 +16,11 @@
  *   rstg_euler_root_forest   euler_root_forest      include/rst/euler_rooting.hpp:63-66
  *   rstg_validate         validate_rooted_forest     include/rst/validate.hpp:46-47
  *   rstg_forest_depth     forest_depth               include/rst/rooted_forest.hpp:29
- *   rstg_k_*              hook_step / jump_to_convergence / list_rank
- *                         (cc_forest.hpp:29-40, euler_rooting.hpp:52-53):
- *                         kernel-level entry points for parity tests.
+ *   rstg_k_*              hook_step / jump_to_convergence / build_euler /
+ *                         compute_successor / break_cycles / list_rank /
+ *                         derive_parents (cc_forest.hpp:29-40,
+ *                         euler_rooting.hpp:18-59): fine-grained entry
+ *                         points of the reference's unit/acceptance tests.
  */
 #ifndef RSTG_H
 #define RSTG_H
@@ -94,7 +96,8 @@ int rstg_set_stream(rstg_graph* g, void* cuda_stream);
 /* Per-phase CUDA-event timing (read with rstg_phase_times). */
 int rstg_set_timing(rstg_graph* g, int enabled);
 /* JSON object of the last run, one entry per phase:
- * {"phase": [ms, launches_of_the_phase, algorithmic_bytes], ...}. */
+ * {"phase": [ms, records, algorithmic_bytes], ...}; records = timed
+ * intervals of the phase in the run (a phase may span several launches). */
 int rstg_phase_times(rstg_graph* g, char* buf, int64_t cap);
 
 /* run_algorithm (bench.cpp:38-54): parent_out[n] (P[r] = r); levels_out[n]
@@ -147,6 +150,23 @@ int rstg_forest_depth(rstg_graph* g, const int64_t* parent, int64_t* depth_out,
 int rstg_graph_generate_part(const char* spec, int part, int nparts, int device,
                              rstg_graph** out);
 int rstg_graph_set_edge_base(rstg_graph* g, int64_t e_base);
+/* MIN-combine of hook slots across ranks, called by rstg_cc_labels before
+ * every apply: which 0 = d_slot[0, count) (round 0, dense), which 1 =
+ * d_xbuf[0, count) (the current roots' slots in roots-list order, the list
+ * being identical on every rank). The callee enqueues its collective on the
+ * handle's stream (rstg_set_stream) and returns 0, or non-zero on failure. */
+typedef int (*rstg_reduce_min_fn)(void* ctx, int which, int64_t count);
+/* cc_spanning_forest's labels (cc_forest.cpp:73-102) through the optimised
+ * single-GPU round structure (round 0 from hook keys, lazy rounds, roots-
+ * list apply). d_rep: int32 n labels out (converged reps); d_tflag (nullable):
+ * uint8 flags of the handle's edges that became tree edges. reduce_min NULL:
+ * one GPU (d_slot/d_xbuf may be NULL). Otherwise edge-partitioned: the handle
+ * holds this rank's edge range (rstg_graph_set_edge_base), d_slot/d_xbuf
+ * are caller int64[n] device buffers, and every rank ends with the same
+ * labels -- bit-identical to the 1-GPU labels. stats->tree_edges = the
+ * global tree-edge count, stats->rounds the hook rounds. */
+int rstg_cc_labels(rstg_graph* g, int32_t* d_rep, uint8_t* d_tflag, int64_t* d_slot,
+                   int64_t* d_xbuf, rstg_reduce_min_fn reduce_min, void* ctx, rstg_stats* stats);
 int rstg_cc_init(rstg_graph* g, int32_t* d_rep, int64_t* d_slot);
 int rstg_cc_hook(rstg_graph* g, int mode, const int32_t* d_rep, int64_t* d_slot);
 /* applies every non-empty slot (rep[v] = winner, slot reset); local tree
@@ -165,6 +185,21 @@ int rstg_k_jump(int64_t n, int64_t* rep);
 /* list ranking of NONE(-1)-terminated lists (euler_rooting.cpp:104-153):
  * rank = distance from the list head. */
 int rstg_k_list_rank(int64_t E, const int64_t* succ, int64_t* rank);
+/* The reference's arc-level Euler API (euler_rooting.hpp:18-59), int64 in
+ * its own layout: arc i = tree edge i (u -> v), arc i + T its reverse.
+ *   build_euler        euler_rooting.hpp:33-34: from/to/next[2T], first/last[n]
+ *   compute_successor  euler_rooting.hpp:38:    succ[E]
+ *   break_cycles       euler_rooting.hpp:43-44: succ[rev(last[r])] = -1
+ *   derive_parents     euler_rooting.hpp:53-56: parent[n] (roots are the
+ *                      caller's, sorted by the C++ mirror) */
+int rstg_k_build_euler(int64_t n, const int64_t* tree_uv, int64_t T, int64_t* from, int64_t* to,
+                       int64_t* first, int64_t* last, int64_t* next);
+int rstg_k_compute_successor(int64_t n, int64_t E, const int64_t* from, const int64_t* first,
+                             const int64_t* next, int64_t* succ);
+int rstg_k_break_cycles(int64_t n, int64_t E, const int64_t* last, const int64_t* roots,
+                        int64_t nroots, int64_t* succ);
+int rstg_k_derive_parents(int64_t n, int64_t E, const int64_t* from, const int64_t* to,
+                          const int64_t* rank, int64_t* parent);
 
 #ifdef __cplusplus
 }

@@ -56,7 +56,8 @@ def lib():
         L.og_last_error.restype = ctypes.c_char_p
         for name in ("og_normalize", "og_gen_path", "og_gen_star", "og_gen_grid",
                      "og_gen_random", "og_gen_complete", "og_gen_road", "og_gen_kron",
-                     "og_cc_spanning_forest", "og_jump_to_convergence", "og_forest_depth"):
+                     "og_cc_spanning_forest", "og_jump_to_convergence", "og_forest_depth",
+                     "og_kron_uf", "og_uf_edges"):
             getattr(L, name).restype = ctypes.c_int64
         L.og_splitmix64.restype = ctypes.c_uint64
         L.og_splitmix64.argtypes = [ctypes.c_uint64]
@@ -240,6 +241,49 @@ def components(g: Graph):
     lab = np.zeros(g.n, I64)
     lib().og_components(ctypes.c_int64(g.n), ctypes.c_int64(g.m), _p(g.eu), _p(g.ev), _p(lab))
     return lab
+
+
+def kron_uf(scale: int, edge_factor: int = 16, threads: int | None = None):
+    """Host union-find over every Kronecker tuple, regenerated on the fly
+    (kron_uf.c; the checker of config 5). Returns (root int32[n] = smallest
+    id of each class, number of classes)."""
+    n = 1 << scale
+    root = np.empty(n, np.int32)
+    c = lib().og_kron_uf(ctypes.c_int(scale), ctypes.c_int(edge_factor),
+                         ctypes.c_int(threads or os.cpu_count() or 1),
+                         root.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    if c < 0:
+        raise OracleError("kron_uf: bad parameters")
+    return root, int(c)
+
+
+def uf_edges(n: int, uv, threads: int | None = None):
+    """Host union-find over an explicit edge list (int32 pairs): (root, classes)."""
+    uv = np.ascontiguousarray(np.asarray(uv, dtype=np.int32).reshape(-1, 2))
+    root = np.empty(max(n, 1), np.int32)
+    c = lib().og_uf_edges(ctypes.c_int64(n), ctypes.c_int64(len(uv)),
+                          uv.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                          ctypes.c_int(threads or os.cpu_count() or 1),
+                          root.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    return root[:n], int(c)
+
+
+def same_partition(labels, root) -> bool:
+    """labels (any class representative per vertex, each a member of its
+    class) and root (smallest id per class) describe the same partition:
+    every vertex shares its label's class, and the class counts agree."""
+    labels = np.asarray(labels)
+    root = np.asarray(root)
+    n = len(root)
+    if len(labels) != n:
+        return False
+    if n == 0:
+        return True
+    if labels.min() < 0 or labels.max() >= n:
+        return False
+    if not np.array_equal(root[labels], root):
+        return False
+    return len(np.unique(labels)) == int(np.count_nonzero(root == np.arange(n)))
 
 
 def validate(g: Graph, parent, roots=None, required_root=-1):

@@ -31,11 +31,14 @@ EXPORTS = (
     "rstg_set_stream", "rstg_set_timing", "rstg_phase_times", "rstg_run", "rstg_run_device",
     "rstg_cc_spanning_forest", "rstg_euler_root_forest", "rstg_validate", "rstg_forest_depth",
     "rstg_graph_generate_part", "rstg_graph_set_edge_base", "rstg_cc_init", "rstg_cc_hook",
-    "rstg_cc_apply", "rstg_cc_compress", "rstg_k_hook_step",
-    "rstg_k_jump", "rstg_k_list_rank",
+    "rstg_cc_apply", "rstg_cc_compress", "rstg_cc_labels", "rstg_k_hook_step",
+    "rstg_k_jump", "rstg_k_list_rank", "rstg_k_build_euler", "rstg_k_compute_successor",
+    "rstg_k_break_cycles", "rstg_k_derive_parents",
 )
 
 _i64p = ctypes.POINTER(ctypes.c_int64)
+# int (*rstg_reduce_min_fn)(void* ctx, int which, int64_t count)
+REDUCE_MIN_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64)
 _i32p = ctypes.POINTER(ctypes.c_int32)
 _u8p = ctypes.POINTER(ctypes.c_uint8)
 _vp = ctypes.c_void_p
@@ -106,10 +109,17 @@ def lib():
         L.rstg_cc_hook.argtypes = [_vp, ctypes.c_int, _vp, _vp]
         L.rstg_cc_apply.argtypes = [_vp, _vp, _vp, _vp, _i64p]
         L.rstg_cc_compress.argtypes = [_vp, _vp]
+        L.rstg_cc_labels.argtypes = [_vp, _vp, _vp, _vp, _vp, REDUCE_MIN_FN, _vp,
+                                     ctypes.POINTER(Stats)]
         L.rstg_k_hook_step.argtypes =[ctypes.c_int64, ctypes.c_int64, _i64p, ctypes.c_int, _i64p,
                                        _u8p, _i64p, ctypes.POINTER(ctypes.c_int)]
         L.rstg_k_jump.argtypes = [ctypes.c_int64, _i64p]
         L.rstg_k_list_rank.argtypes = [ctypes.c_int64, _i64p, _i64p]
+        L.rstg_k_build_euler.argtypes = [ctypes.c_int64, _i64p, ctypes.c_int64] + [_i64p] * 5
+        L.rstg_k_compute_successor.argtypes = [ctypes.c_int64, ctypes.c_int64] + [_i64p] * 4
+        L.rstg_k_break_cycles.argtypes = [ctypes.c_int64, ctypes.c_int64, _i64p, _i64p,
+                                          ctypes.c_int64, _i64p]
+        L.rstg_k_derive_parents.argtypes = [ctypes.c_int64, ctypes.c_int64] + [_i64p] * 4
         _lib = L
     return _lib
 
@@ -199,6 +209,19 @@ class DeviceGraph:
 
     def cc_compress(self, d_rep: int):
         _check(lib().rstg_cc_compress(self._h, _vp(d_rep)))
+
+    def cc_labels(self, d_rep: int, d_tflag: int = 0, d_slot: int = 0, d_xbuf: int = 0,
+                  reduce_min=None) -> dict:
+        """rstg_cc_labels: converged labels (int32, device) through the
+        optimised rounds; reduce_min(which, count) -> 0 MIN-combines the
+        slots across ranks (edge-partitioned mode), None = one GPU."""
+        st = Stats()
+        cb = REDUCE_MIN_FN(lambda ctx, which, count: int(reduce_min(which, count))) \
+            if reduce_min is not None else REDUCE_MIN_FN()
+        _check(lib().rstg_cc_labels(self._h, _vp(d_rep), _vp(d_tflag or None),
+                                    _vp(d_slot or None), _vp(d_xbuf or None), cb, None,
+                                    ctypes.byref(st)))
+        return st.as_dict()
 
     def upload(self, n, edges_uv, offsets=None, neighbors=None, edge_origin=None):
         """Re-uploads a graph into this handle (edges_uv int64, (m, 2) or flat)."""
@@ -323,3 +346,41 @@ def list_rank(succ):
     rank = np.zeros(max(len(s), 1), np.int64)
     _check(lib().rstg_k_list_rank(len(s), _p64(s), _p64(rank)))
     return rank[: len(s)]
+
+
+class EulerStructure:
+    """The reference's arc-level Euler structure (euler_rooting.hpp:18-31),
+    int64 arrays in its layout, each step one device call."""
+
+    def __init__(self, n, tree_edges):
+        te = np.ascontiguousarray(np.asarray(tree_edges, dtype=np.int64).reshape(-1, 2))
+        self.num_vertices, self.num_arcs = int(n), 2 * len(te)
+        E = self.num_arcs
+        self.from_, self.to, self.next = (np.zeros(max(E, 1), np.int64) for _ in range(3))
+        self.first, self.last = np.zeros(max(n, 1), np.int64), np.zeros(max(n, 1), np.int64)
+        _check(lib().rstg_k_build_euler(int(n), _p64(te), len(te), _p64(self.from_), _p64(self.to),
+                                        _p64(self.first), _p64(self.last), _p64(self.next)))
+        self.from_, self.to, self.next = self.from_[:E], self.to[:E], self.next[:E]
+        self.first, self.last = self.first[:n], self.last[:n]
+        self.succ = None
+
+    def compute_successor(self):
+        self.succ = np.zeros(max(self.num_arcs, 1), np.int64)
+        _check(lib().rstg_k_compute_successor(self.num_vertices, self.num_arcs, _p64(self.from_),
+                                              _p64(self.first), _p64(self.next), _p64(self.succ)))
+        self.succ = self.succ[: self.num_arcs]
+
+    def break_cycles(self, roots):
+        r = np.ascontiguousarray(np.asarray(roots, dtype=np.int64))
+        _check(lib().rstg_k_break_cycles(self.num_vertices, self.num_arcs, _p64(self.last), _p64(r),
+                                         len(r), _p64(self.succ)))
+
+    def list_rank(self):
+        return list_rank(self.succ)
+
+    def derive_parents(self, rank):
+        parent = np.zeros(max(self.num_vertices, 1), np.int64)
+        rk = np.ascontiguousarray(np.asarray(rank, dtype=np.int64))
+        _check(lib().rstg_k_derive_parents(self.num_vertices, self.num_arcs, _p64(self.from_),
+                                           _p64(self.to), _p64(rk), _p64(parent)))
+        return parent[: self.num_vertices]

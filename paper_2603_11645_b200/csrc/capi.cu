@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -69,6 +70,14 @@ int guard(F&& f) {
   }
 }
 
+}  // namespace
+
+// The same error mapping for entry points defined in other files.
+namespace rstg {
+int guard_call(const std::function<void()>& f) { return guard(f); }
+}  // namespace rstg
+
+namespace {
 double now_ms() {
   return std::chrono::duration<double, std::milli>(
              std::chrono::steady_clock::now().time_since_epoch())
@@ -99,6 +108,34 @@ void to_device(Handle& h, const int64_t* host, int64_t count, T* dev) {
 void check_root(Handle& h, int64_t root) {
   if (root < 0 || root >= h.g.n)
     throw AlgoError("root " + std::to_string(root) + " out of range");
+}
+
+// phase times: {"name": [total_ms, records, algorithmic_bytes], ...} in
+// first-seen order (records: timed intervals of the phase in the run)
+std::string phases_to_json(Handle& h) {
+  auto ph = h.timer.collect();
+  struct Agg {
+    std::string name;
+    double ms, bytes;
+    int count;
+  };
+  std::vector<Agg> agg;
+  for (auto& p : ph) {
+    auto it = std::find_if(agg.begin(), agg.end(), [&](const Agg& a) { return a.name == p.name; });
+    if (it == agg.end())
+      agg.push_back({p.name, p.ms, p.bytes, 1});
+    else
+      it->ms += p.ms, it->bytes += p.bytes, it->count += 1;
+  }
+  std::string js = "{";
+  for (size_t i = 0; i < agg.size(); ++i) {
+    if (i) js += ",";
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "\"%s\":[%.6f,%d,%.0f]", agg[i].name.c_str(), agg[i].ms,
+                  agg[i].count, agg[i].bytes);
+    js += buf;
+  }
+  return js + "}";
 }
 
 // The device pipeline of run_algorithm. Returns the roots count (roots
@@ -139,30 +176,7 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
   CK(cudaEventDestroy(e1));
   h.stats.device_ms = ms;
   if (nroots >= 0) h.stats.components = nroots;
-  // phase times: {"name": [total_ms, records, algorithmic_bytes], ...} in first-seen order
-  auto ph = h.timer.collect();
-  struct Agg {
-    std::string name;
-    double ms, bytes;
-    int count;
-  };
-  std::vector<Agg> agg;
-  for (auto& p : ph) {
-    auto it = std::find_if(agg.begin(), agg.end(), [&](const Agg& a) { return a.name == p.name; });
-    if (it == agg.end())
-      agg.push_back({p.name, p.ms, p.bytes, 1});
-    else
-      it->ms += p.ms, it->bytes += p.bytes, it->count += 1;
-  }
-  std::string js = "{";
-  for (size_t i = 0; i < agg.size(); ++i) {
-    if (i) js += ",";
-    char buf[256];
-    std::snprintf(buf, sizeof buf, "\"%s\":[%.6f,%d,%.0f]", agg[i].name.c_str(), agg[i].ms,
-                  agg[i].count, agg[i].bytes);
-    js += buf;
-  }
-  g->phases_json = js + "}";
+  g->phases_json = phases_to_json(h);
   return nroots;
 }
 
@@ -325,6 +339,33 @@ int rstg_graph_set_edge_base(rstg_graph* g, int64_t e_base) {
   return guard([&] {
     if (e_base < 0 || e_base + g->h.g.m > (int64_t{1} << 32)) throw ArgError("edge base out of range");
     g->h.g.e_base = e_base;
+  });
+}
+
+int rstg_cc_labels(rstg_graph* g, int32_t* d_rep, uint8_t* d_tflag, int64_t* d_slot,
+                   int64_t* d_xbuf, rstg_reduce_min_fn reduce_min, void* ctx, rstg_stats* stats) {
+  return guard([&] {
+    Handle& h = g->h;
+    const double t0 = now_ms();
+    h.stats = Stats{};
+    if (reduce_min && (!d_slot || !d_xbuf)) throw ArgError("exchange needs slot and xbuf buffers");
+    CcExchange ex{reduce_min, ctx, reinterpret_cast<unsigned long long*>(d_slot),
+                  reinterpret_cast<unsigned long long*>(d_xbuf)};
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, h.stream));
+    cc_exact(h, d_rep, d_tflag, nullptr, reduce_min ? &ex : nullptr);
+    CK(cudaEventRecord(e1, h.stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    h.stats.device_ms = ms;
+    g->phases_json = phases_to_json(h);
+    fill_stats(stats, h.stats);
+    if (stats) stats->total_ms = now_ms() - t0;
   });
 }
 

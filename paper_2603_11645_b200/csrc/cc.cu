@@ -737,6 +737,7 @@ void cc_round_done(Handle& h, int64_t out_count) {
   ++h.cc_round;
 }
 bool round0_keys_from_edges(Handle& h, unsigned long long* slot);
+void launch_round0_keys(Handle& h, unsigned long long* slot);
 
 void cc_reset_rounds(Handle& h) {
   h.cc_lazy = false;
@@ -806,17 +807,67 @@ void launch_cc_init(Handle& h, int32_t* rep, unsigned long long* slot) {
   h.stats.step(h.g.n);
 }
 
-int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) {
+// Edge-partitioned rounds (multi-GPU): the proposals of
+// every rank's local edges are MIN-combined before each apply --
+// combine_min (cc_forest.cpp:34) across ranks. Round 0 exchanges the dense
+// slot array (every vertex may get a key); later rounds only the slots of
+// the current roots, gathered in roots-list order (the list is replicated:
+// identical on every rank), so the exchange shrinks with the roots.
+__global__ void k_gather_slots(const uint32_t* __restrict__ list, int64_t count,
+                               const unsigned long long* __restrict__ slot,
+                               unsigned long long* buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = slot[list[i]];
+}
+__global__ void k_scatter_slots(const uint32_t* __restrict__ list, int64_t count,
+                                const unsigned long long* __restrict__ buf,
+                                unsigned long long* slot, int* any) {
+  bool a = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = buf[i];
+    slot[list[i]] = k;
+    a |= k != kKeyInf;
+  }
+  if (__any_sync(0xffffffffu, a) && (threadIdx.x & 31) == 0) *any = 1;
+}
+__global__ void k_any_slot(int64_t n, const unsigned long long* __restrict__ slot, int* any) {
+  bool a = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a |= slot[i] != kKeyInf;
+  if (__any_sync(0xffffffffu, a) && (threadIdx.x & 31) == 0) *any = 1;
+}
+static void exchange(Handle& h, const CcExchange& ex, int which, int64_t count) {
+  if (count <= 0) return;
+  // the caller's collective is enqueued on the handle's stream (the
+  // caller sets it: rstg_set_stream) after the proposals
+  if (ex.reduce_min(ex.ctx, which, count) != 0) throw AlgoError("slot exchange failed");
+}
+
+int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
+                 const CcExchange* ex) {
   const int64_t n = h.g.n, m = h.g.m;
-  unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
+  unsigned long long* slot = ex ? ex->slot : h.ws<unsigned long long>(WS_SLOT, n);
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(h.dev_box);
-  // round 0 from the keys the edge upload left in the slots, else (CSR
-  // still pending) from keys recomputed over the edge list, else the CSR
-  const bool keyed = (h.round0_slots == slot && m > 0) || round0_keys_from_edges(h, slot);
+  bool keyed;
+  if (ex) {
+    // every rank's round-0 keys (local edges, global ids), MIN-combined
+    k_cc_init<<<grid_for(n), kBlock, 0, h.stream>>>(n, nullptr, slot);
+    CK_LAUNCH();
+    if (m > 0) launch_round0_keys(h, slot);
+    exchange(h, *ex, 0, n);
+    keyed = n > 0;
+  } else {
+    // round 0 from the keys the edge upload left in the slots, else (no
+    // CSR built) from keys recomputed over the edge list, else the CSR
+    keyed = (h.round0_slots == slot && m > 0) || round0_keys_from_edges(h, slot);
+  }
   h.round0_slots = nullptr;
   const bool round0 = keyed || (h.g.has_csr() && m > 0);  // writes every rep itself
   const bool slots_ok = keyed || (h.slots_clean == slot && n <= h.slots_clean_n);
-  h.slots_clean = nullptr;  // until this build completes
+  if (!ex) h.slots_clean = nullptr;  // until this build completes
   h.timer.begin(h.stream, "cc.init", (round0 ? 0.0 : 4.0 * n) + (slots_ok ? 0.0 : 8.0 * n));
   if (!round0 || !slots_ok) {
     k_cc_init<<<grid_for(n), kBlock, 0, h.stream>>>(n, round0 ? nullptr : rep,
@@ -884,12 +935,36 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
                   visited * ((h.cc_round >= 2 && h.cc_active >= 0) ? 20.0 : 16.0));
     cc_hook_round(h, mode, rep, slot, counter + 1, any);
     h.timer.end(h.stream);
-    // hooks so far, crossing, any; [20] the round-0 roots count (same read)
-    h.read_box(reinterpret_cast<int64_t*>(counter), 21);
+    // hooks so far, crossing, any; [20] the round-0 roots count, [21] the
+    // current roots count (same read)
+    h.read_box(reinterpret_cast<int64_t*>(counter), 22);
     const int64_t r0_count = have_r0 ? h.host_box[20] : 0;
     prev_total = total;
     total = h.host_box[0];
-    const bool proposed = h.host_box[2] != 0;
+    bool proposed = h.host_box[2] != 0;
+    if (ex) {
+      // proposals of all ranks (they target current roots only), then the
+      // global "any proposal" decides the stop on every rank alike
+      h.timer.begin(h.stream, "cc.exchange", 16.0 * (have_r0 ? h.host_box[21] : n));
+      CK(cudaMemsetAsync(any, 0, sizeof(int), h.stream));
+      if (have_r0) {
+        const int64_t R = h.host_box[21];
+        if (R > 0) {
+          k_gather_slots<<<grid_for(R), kBlock, 0, h.stream>>>(in_list, R, slot, ex->xbuf);
+          CK_LAUNCH();
+          exchange(h, *ex, 1, R);
+          k_scatter_slots<<<grid_for(R), kBlock, 0, h.stream>>>(in_list, R, ex->xbuf, slot, any);
+          CK_LAUNCH();
+        }
+      } else {
+        exchange(h, *ex, 0, n);
+        k_any_slot<<<grid_for(n), kBlock, 0, h.stream>>>(n, slot, any);
+        CK_LAUNCH();
+      }
+      h.timer.end(h.stream);
+      h.read_box(reinterpret_cast<int64_t*>(counter) + 2, 1);
+      proposed = *reinterpret_cast<int*>(h.host_box) != 0;
+    }
     if (getenv("RSTG_CC_DEBUG"))
       fprintf(stderr, "cc round %d mode %d: visited %.0f, hooks so far %lld, crossing %lld, lazy %d, r0 %lld\n",
               round, mode, visited, (long long)total, (long long)h.host_box[1], (int)h.cc_lazy,
@@ -953,8 +1028,10 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler) 
   }
   h.cc_lazy = false;
   h.stats.tree_edges = total;
-  h.slots_clean = slot;
-  h.slots_clean_n = n;
+  if (!ex) {
+    h.slots_clean = slot;
+    h.slots_clean_n = n;
+  }
   return total;
 }
 

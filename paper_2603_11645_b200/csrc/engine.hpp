@@ -296,7 +296,20 @@ void ensure_csr(Handle& h);
 // euler (nullable): every tree edge is linked into the rotation lists as it
 // is created, slot = the vertex it hooked (EulerIO; N = n slots); the labels
 // are then left lazy (reps pointing at ancestors), euler_root resolves them.
-int64_t cc_exact(Handle& h, int32_t* labels, uint8_t* tflag, const EulerIO* euler = nullptr);
+// ex (nullable): edge-partitioned mode (multi-GPU): the handle holds one
+// rank's contiguous edge range (global ids from g.e_base), the slots are
+// the caller's, and reduce_min MIN-combines them across the ranks before
+// every apply (which 0: slot[0, count) dense; 1: xbuf[0, count), the
+// current roots' slots in roots-list order). Labels and tree-edge totals
+// are then identical on every rank and equal to the 1-GPU result.
+struct CcExchange {
+  int (*reduce_min)(void* ctx, int which, int64_t count);
+  void* ctx;
+  unsigned long long* slot;  // n entries
+  unsigned long long* xbuf;  // n entries
+};
+int64_t cc_exact(Handle& h, int32_t* labels, uint8_t* tflag, const EulerIO* euler = nullptr,
+                 const CcExchange* ex = nullptr);
 // cc labels only, validity-level (any correct partition; used by BFS
 // seeding and the validator). Returns the number of hook rounds.
 void cc_labels_fast(Handle& h, int32_t* labels);

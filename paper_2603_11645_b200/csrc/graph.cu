@@ -568,15 +568,20 @@ __global__ void k_round0_keys(int64_t m, const int2* __restrict__ edges, uint32_
     }
   }
 }
+void launch_round0_keys(Handle& h, unsigned long long* slot) {
+  k_round0_keys<<<grid_for(h.g.m), kBlock, 0, h.stream>>>(h.g.m, h.g.edges, (uint32_t)h.g.e_base,
+                                                          slot);
+  CK_LAUNCH();
+}
 bool round0_keys_from_edges(Handle& h, unsigned long long* slot) {
-  if (!h.g.csr_pending || h.g.m == 0) return false;
+  // (a built CSR serves round 0 directly; without one -- pending, or a
+  // graph too large for 32-bit arc offsets -- the keys come from the edges)
+  if ((h.g.has_csr() && !h.g.csr_pending) || h.g.m == 0) return false;
   if (h.slots_clean != slot || h.g.n > h.slots_clean_n) {
     k_fill_u64<<<grid_for(h.g.n), kBlock, 0, h.stream>>>(h.g.n, slot, kKeyInf);
     CK_LAUNCH();
   }
-  k_round0_keys<<<grid_for(h.g.m), kBlock, 0, h.stream>>>(h.g.m, h.g.edges, (uint32_t)h.g.e_base,
-                                                          slot);
-  CK_LAUNCH();
+  launch_round0_keys(h, slot);
   return true;
 }
 

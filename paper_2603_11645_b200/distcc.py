@@ -5,20 +5,26 @@ Rank r of k owns the edges whose smaller endpoint lies in
 endpoint, the rank's edges are ONE contiguous range of the global list:
 global edge id = e_base + local index, with e_base = the edge counts of the
 lower ranks (one all-gather). The hook keys (winner << 32 | global edge id)
-are therefore the single-GPU keys, and the result is bit-identical to the
+are therefore the single-GPU keys, and the labels are bit-identical to the
 1-GPU run (cc_spanning_forest, cc_forest.cpp:73-102).
 
-Per round (mode alternates min/max, starting with min):
-  hook      local edge pass into the replicated slot[n] (int64, INT64_MAX empty)
-  exchange  all_reduce(slot, MIN) over NCCL -- exactly combine_min
-            (cc_forest.cpp:34) across ranks; the only data-path collective
-  apply     replicated on every rank: rep[v] = winner, count applied hooks
-  compress  replicated two-level pointer jumping
-  stop      when a round applied nothing (identical on every rank)
+The rounds are the single-GPU ones (csrc/cc.cu cc_exact, rstg_cc_labels):
+round 0 from hook keys, lazy rounds that find roots, apply over the current
+roots list only. Everything but the proposals is replicated on every rank:
+the roots list, apply, the roots-list pointer jump and the stop decision.
+The exchange before each apply is the only data-path collective:
 
-`kernels` supplies init/hook/apply/compress on this rank's tensors: the CUDA
-kernels of the C ABI (GpuKernels) in production; the CPU gloo tests plug in
-a numpy restatement to check the partitioning and exchange logic.
+  round 0   all_reduce(MIN) of the dense int64 slot array (8n bytes): every
+            vertex may receive a key when all reps are singletons
+  later     all_reduce(MIN) of the current roots' slots, gathered in roots-
+            list order (8 bytes per root): road 24M has ~3.9K roots after
+            round 0, RMAT-24 a few hundred thousand -- the exchange shrinks
+            with the roots instead of costing 8n every round
+
+That is exactly combine_min (cc_forest.cpp:34) across ranks. With the
+NCCL backend the all-reduce runs on the device buffers on the handle's
+stream; with gloo (CPU tests, several ranks sharing one GPU) it is staged
+through host memory.
 """
 from __future__ import annotations
 
@@ -40,49 +46,63 @@ def edge_base(local_m: int, rank: int, world: int, device) -> int:
     return int(sum(int(x.item()) for x in out[:rank]))
 
 
-class GpuKernels:
-    """The C-ABI CUDA kernels on a DeviceGraph holding this rank's edges."""
+class SlotExchange:
+    """The reduce_min callback of rstg_cc_labels: MIN-combines the hook
+    slots (which 0: slot[:count], dense) or the roots' gathered slots
+    (which 1: xbuf[:count]) across the ranks. Records (which, count) per
+    call so callers can report the exchanged bytes."""
 
-    def __init__(self, dg):
-        self.dg = dg
-        # Launch on torch's current stream so the NCCL all-reduce (ordered on
-        # that stream) is complete before apply reads the slots.
-        dg.set_stream(torch.cuda.current_stream().cuda_stream)
+    def __init__(self, n: int, device, world: int, staged: bool | None = None):
+        self.slot = torch.empty(max(n, 1), dtype=torch.int64, device=device)
+        self.xbuf = torch.empty(max(n, 1), dtype=torch.int64, device=device)
+        self.world = world
+        if staged is None:
+            staged = world > 1 and (torch.device(device).type == "cuda"
+                                    and dist.get_backend() != "nccl")
+        self.staged = staged
+        self.calls: list[tuple[int, int]] = []
+        self.error: BaseException | None = None
 
-    def init(self, rep, slot):
-        self.dg.cc_init(rep.data_ptr(), slot.data_ptr())
+    def __call__(self, which: int, count: int) -> int:
+        try:
+            t = (self.slot if which == 0 else self.xbuf)[:count]
+            self.calls.append((which, int(count)))
+            if self.world > 1:
+                if self.staged:
+                    h = t.cpu()  # (ordered after the proposals: same stream)
+                    dist.all_reduce(h, op=dist.ReduceOp.MIN)
+                    t.copy_(h)
+                else:
+                    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            return 0
+        except BaseException as e:  # reported by distributed_cc
+            self.error = e
+            return 1
 
-    def hook(self, mode, rep, slot):
-        self.dg.cc_hook(mode, rep.data_ptr(), slot.data_ptr())
-
-    def apply(self, rep, slot):
-        return self.dg.cc_apply(rep.data_ptr(), slot.data_ptr())
-
-    def compress(self, rep):
-        self.dg.cc_compress(rep.data_ptr())
+    def bytes_per_rank(self) -> int:
+        return 8 * sum(c for _, c in self.calls)
 
 
-def distributed_cc(kernels, n: int, device, world: int = 1, max_rounds: int | None = None):
-    """Runs the exact edge-partitioned connectivity; returns (rep, rounds, hooks).
-
-    rep: int32 tensor of converged representatives (identical on all ranks).
-    """
-    rep = torch.empty(n, dtype=torch.int32, device=device)
-    slot = torch.empty(n, dtype=torch.int64, device=device)
-    kernels.init(rep, slot)
-    mode, rounds, hooks = 0, 0, 0
-    limit = max_rounds if max_rounds is not None else n + 1  # cc_forest.cpp:88
-    while True:
-        if rounds > limit:
-            raise RuntimeError("hooking failed to converge")
-        kernels.hook(mode, rep, slot)
+def distributed_cc(dg, n: int, world: int, tflag: torch.Tensor | None = None,
+                   exchange: SlotExchange | None = None):
+    """Exact connectivity labels of the edge-partitioned graph (this rank's
+    DeviceGraph `dg`, edge base already set). Returns (rep int32 tensor,
+    stats dict); rep is identical on all ranks and equal to the 1-GPU
+    labels. world == 1: the optimised single-GPU rounds, no exchange."""
+    # the collective runs on torch's current stream: launch there too
+    dg.set_stream(torch.cuda.current_stream().cuda_stream)
+    rep = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    if world > 1 and exchange is None:
+        exchange = SlotExchange(n, "cuda", world)
+    tp = tflag.data_ptr() if tflag is not None else 0
+    try:
         if world > 1:
-            dist.all_reduce(slot, op=dist.ReduceOp.MIN)
-        applied = kernels.apply(rep, slot)
-        rounds += 1
-        if applied == 0:
-            break
-        hooks += applied
-        kernels.compress(rep)
-        mode ^= 1
-    return rep, rounds, hooks
+            st = dg.cc_labels(rep.data_ptr(), tp, exchange.slot.data_ptr(),
+                              exchange.xbuf.data_ptr(), exchange)
+        else:
+            st = dg.cc_labels(rep.data_ptr(), tp)
+    except Exception:
+        if exchange is not None and exchange.error is not None:
+            raise exchange.error
+        raise
+    return rep[:n], st

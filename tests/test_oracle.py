@@ -202,3 +202,32 @@ def test_oracle_vs_reference_shapes(O, spec):
     for algo in (0, 1, 2):
         a, b = O.run(g, algo, root), O.ref_run(g, algo, root)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ---- the config-5 checker (oracle/kron_uf.c) ------------------------------------
+@pytest.mark.parametrize("scale,ef", [(10, 16), (12, 16), (13, 4)])
+def test_kron_uf_matches_reference_components(O, scale, ef):
+    # host union-find over regenerated tuples == the partition of the
+    # normalized graph (reference cc labels when the reference is built)
+    g = O.gen("kron", scale, ef)
+    root, c = O.kron_uf(scale, ef, threads=4)
+    labels = O.ref_cc_spanning_forest(g)[0] if O.have_ref() else O.cc_spanning_forest(g)[0]
+    assert O.same_partition(labels, root)
+    _, te = O.cc_spanning_forest(g)
+    assert c == g.n - len(te)
+    # tree edges form a forest with the same classes; one extra edge makes a cycle
+    tuv = np.stack([g.eu[te], g.ev[te]], 1)
+    troot, tc = O.uf_edges(g.n, tuv, threads=3)
+    assert tc == g.n - len(te) and np.array_equal(troot, root)
+    extra = np.array([[g.eu[0], g.ev[0]]]) if 0 not in set(te.tolist()) else None
+    if extra is not None:
+        _, tc2 = O.uf_edges(g.n, np.concatenate([tuv, extra]))
+        assert tc2 == tc  # the non-tree edge merges nothing: T + 1 edges, same classes
+
+
+def test_same_partition_detects_differences(O):
+    root = np.array([0, 0, 2, 2, 4], np.int32)
+    assert O.same_partition(np.array([1, 1, 3, 3, 4]), root)
+    assert not O.same_partition(np.array([1, 1, 1, 3, 4]), root)   # merges two classes
+    assert not O.same_partition(np.array([0, 1, 2, 2, 4]), root)   # splits a class
+    assert not O.same_partition(np.array([0, 0, 2, 2, 9]), root)   # out of range

@@ -90,6 +90,11 @@ int rstg_graph_generate(const char* spec, int device, rstg_graph** out);
 int rstg_graph_info(const rstg_graph* g, int64_t* n, int64_t* m);
 /* Copies the device edge list out as int64 pairs (2m). */
 int rstg_graph_edges(rstg_graph* g, int64_t* edges_uv);
+/* The edges whose device flag (uint8 per edge of the handle, e.g. the tree
+ * flags of rstg_cc_labels) is set, in id order, as int64 (u, v) pairs;
+ * *count = how many (at most cap). SpanningForest::tree_edges as endpoints. */
+int rstg_graph_edges_flagged(rstg_graph* g, const uint8_t* d_flags, int64_t* edges_uv,
+                             int64_t cap, int64_t* count);
 int rstg_graph_destroy(rstg_graph* g);
 /* Launch on a caller stream (cudaStream_t) instead of the handle's own. */
 int rstg_set_stream(rstg_graph* g, void* cuda_stream);

@@ -27,7 +27,8 @@ RSTG_OK, RSTG_ERR_ARG, RSTG_ERR_ALGO, RSTG_ERR_CUDA = 0, 1, 2, 3
 # Symbols include/rstg.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "rstg_last_error", "rstg_device_count", "rstg_graph_create", "rstg_graph_create_device", "rstg_graph_upload",
-    "rstg_graph_generate", "rstg_graph_info", "rstg_graph_edges", "rstg_graph_destroy",
+    "rstg_graph_generate", "rstg_graph_info", "rstg_graph_edges", "rstg_graph_edges_flagged",
+    "rstg_graph_destroy",
     "rstg_set_stream", "rstg_set_timing", "rstg_phase_times", "rstg_run", "rstg_run_device",
     "rstg_cc_spanning_forest", "rstg_euler_root_forest", "rstg_validate", "rstg_forest_depth",
     "rstg_graph_generate_part", "rstg_graph_set_edge_base", "rstg_cc_init", "rstg_cc_hook",
@@ -87,6 +88,7 @@ def lib():
         L.rstg_graph_generate.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(_vp)]
         L.rstg_graph_info.argtypes = [_vp, _i64p, _i64p]
         L.rstg_graph_edges.argtypes = [_vp, _i64p]
+        L.rstg_graph_edges_flagged.argtypes = [_vp, _vp, _i64p, ctypes.c_int64, _i64p]
         L.rstg_graph_destroy.argtypes = [_vp]
         L.rstg_set_stream.argtypes = [_vp, _vp]
         L.rstg_set_timing.argtypes = [_vp, ctypes.c_int]
@@ -247,6 +249,14 @@ class DeviceGraph:
         out = np.zeros(2 * self.m, np.int64)
         _check(lib().rstg_graph_edges(self._h, _p64(out)))
         return out.reshape(-1, 2)
+
+    def edges_flagged(self, d_flags: int, cap: int) -> np.ndarray:
+        """Edges whose device uint8 flag is set, id order, (count, 2) int64."""
+        out = np.zeros(2 * max(cap, 1), np.int64)
+        c = ctypes.c_int64(0)
+        _check(lib().rstg_graph_edges_flagged(self._h, _vp(d_flags), _p64(out), int(cap),
+                                              ctypes.byref(c)))
+        return out[: 2 * c.value].reshape(-1, 2)
 
     def set_stream(self, stream_ptr: int):
         _check(lib().rstg_set_stream(self._h, _vp(stream_ptr)))

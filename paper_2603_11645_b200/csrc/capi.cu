@@ -15,6 +15,8 @@
 #include "engine.hpp"
 #include "scan.cuh"
 
+#include <cub/cub.cuh>
+
 namespace rstg {
 void upload_reference_graph(Handle& h, const int64_t* offsets, const int64_t* nbrs,
                             const int64_t* origin, const int64_t* edges_uv, int64_t n, int64_t m);
@@ -420,6 +422,28 @@ int rstg_graph_info(const rstg_graph* g, int64_t* n, int64_t* m) {
 int rstg_graph_edges(rstg_graph* g, int64_t* edges_uv) {
   return guard([&] {
     widen_to_host(g->h, reinterpret_cast<const int32_t*>(g->h.g.edges), 2 * g->h.g.m, edges_uv);
+  });
+}
+
+int rstg_graph_edges_flagged(rstg_graph* g, const uint8_t* d_flags, int64_t* edges_uv,
+                             int64_t cap, int64_t* count) {
+  return guard([&] {
+    Handle& h = g->h;
+    const int64_t m = h.g.m;
+    *count = 0;
+    if (m == 0) return;
+    // flagged edges in id order (cub select), then widened to the host
+    int2* sel = h.ws<int2>(WS_VAL_A, m);
+    long long* nsel = reinterpret_cast<long long*>(h.dev_box) + 48;
+    size_t temp = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, temp, h.g.edges, d_flags, sel, nsel, m, h.stream));
+    void* tmp = h.ws(WS_SL, temp);
+    CK(cub::DeviceSelect::Flagged(tmp, temp, h.g.edges, d_flags, sel, nsel, m, h.stream));
+    h.read_box(reinterpret_cast<int64_t*>(nsel), 1);
+    const int64_t c = h.host_box[0];
+    if (c > cap) throw ArgError("output capacity too small");
+    widen_to_host(h, reinterpret_cast<const int32_t*>(sel), 2 * c, edges_uv);
+    *count = c;
   });
 }
 

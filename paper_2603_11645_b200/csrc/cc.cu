@@ -24,6 +24,8 @@
 
 #include <algorithm>
 
+#include <cub/cub.cuh>
+
 #include "engine.hpp"
 #include "scan.cuh"
 
@@ -215,6 +217,7 @@ struct RoundIO {
   EulerIO eu;
   uint32_t* roots;              // round 0: vertices left as roots (nullable)
   unsigned long long* nroots;
+  bool edge_sentinel;           // round-0 slots carry kKeyEdge (empty = isolated)
 };
 
 template <int SRC>
@@ -290,9 +293,10 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
     } else {
       r = (int32_t)v;
       // cleared below if v hooks; an isolated vertex (no neighbour: the CSR
-      // path knows) can never hook, so it stays off the roots list that
-      // every later apply and roots jump walks (RMAT-24: 7.9M of 16.8M)
-      if (SRC != kSrcRound0 || fnb[k] != INT32_MAX) rootmask |= 1u << k;
+      // path knows, and so do slots keyed with the kKeyEdge sentinel) can
+      // never hook, so it stays off the roots list that every later apply
+      // and roots jump walks (RMAT-24: 7.9M of 16.8M)
+      if (SRC == kSrcRound0 && fnb[k] != INT32_MAX) rootmask |= 1u << k;
       {
         int32_t u = INT32_MAX;
         uint32_t ekey = kNone32;  // (kSrcRound0Slot: the edge id from the key)
@@ -300,11 +304,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
           u = fnb[k];
         } else {
           const unsigned long long key = io.slot[v];
-          if (key != kKeyInf) {
+          if (!io.edge_sentinel || key != kKeyInf) rootmask |= 1u << k;
+          if (key < kKeyEdge) {
             u = (int32_t)(key >> 32);
             ekey = (uint32_t)key;
-            io.slot[v] = kKeyInf;  // (keeps the slots clean for the next rounds)
           }
+          if (key != kKeyInf) io.slot[v] = kKeyInf;  // (keeps the slots clean for the next rounds)
         }
         if (u < r) {  // hooked onto its smallest neighbour by edge (u, v)
           rootmask &= ~(1u << k);
@@ -851,8 +856,9 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
   const int64_t n = h.g.n, m = h.g.m;
   unsigned long long* slot = ex ? ex->slot : h.ws<unsigned long long>(WS_SLOT, n);
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(h.dev_box);
-  bool keyed;
+  bool keyed, keys_from_edges = false;
   if (ex) {
+    keys_from_edges = true;
     // every rank's round-0 keys (local edges, global ids), MIN-combined
     k_cc_init<<<grid_for(n), kBlock, 0, h.stream>>>(n, nullptr, slot);
     CK_LAUNCH();
@@ -862,7 +868,9 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
   } else {
     // round 0 from the keys the edge upload left in the slots, else (no
     // CSR built) from keys recomputed over the edge list, else the CSR
-    keyed = (h.round0_slots == slot && m > 0) || round0_keys_from_edges(h, slot);
+    const bool upload_keys = h.round0_slots == slot && m > 0;
+    keys_from_edges = !upload_keys && round0_keys_from_edges(h, slot);
+    keyed = upload_keys || keys_from_edges;
   }
   h.round0_slots = nullptr;
   const bool round0 = keyed || (h.g.has_csr() && m > 0);  // writes every rep itself
@@ -889,7 +897,8 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
   unsigned long long* rcount = reinterpret_cast<unsigned long long*>(h.dev_box) + 20;
   CK(cudaMemsetAsync(rcount, 0, sizeof(unsigned long long), h.stream));
   RoundIO io{slot, tflag, (uint32_t)h.g.e_base, (uint32_t)m, counter, h.g.offsets, h.g.nbrs,
-             h.g.arc_edge, h.g.edges, euler != nullptr, euler ? *euler : EulerIO{}, rl[0], rcount};
+             h.g.arc_edge, h.g.edges, euler != nullptr, euler ? *euler : EulerIO{}, rl[0], rcount,
+             keys_from_edges};
   cc_reset_rounds(h);
   int64_t round = 0;
   if (round0) {
@@ -950,6 +959,18 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
       if (have_r0) {
         const int64_t R = h.host_box[21];
         if (R > 0) {
+          // the roots list is filled by atomics (tile / block order varies
+          // from rank to rank): sort it by id so position i names the same
+          // root on every rank
+          uint32_t* list = const_cast<uint32_t*>(in_list);
+          uint32_t* sorted = h.ws<uint32_t>(WS_XSORT, R);
+          int bits = 1;
+          while (bits < 32 && (int64_t{1} << bits) < n) ++bits;
+          size_t temp = 0;
+          CK(cub::DeviceRadixSort::SortKeys(nullptr, temp, list, sorted, (int)R, 0, bits, h.stream));
+          void* tmp = h.ws(WS_XTMP, temp);
+          CK(cub::DeviceRadixSort::SortKeys(tmp, temp, list, sorted, (int)R, 0, bits, h.stream));
+          CK(cudaMemcpyAsync(list, sorted, R * sizeof(uint32_t), cudaMemcpyDeviceToDevice, h.stream));
           k_gather_slots<<<grid_for(R), kBlock, 0, h.stream>>>(in_list, R, slot, ex->xbuf);
           CK_LAUNCH();
           exchange(h, *ex, 1, R);

@@ -20,6 +20,9 @@ constexpr uint32_t kNone32 = 0xFFFFFFFFu;
 // (vertex ids < 2^31 - 1), so unsigned and signed order agree and an NCCL
 // int64 MIN all-reduce combines slots like combine_min (multi-GPU CC).
 constexpr unsigned long long kKeyInf = 0x7FFFFFFFFFFFFFFFull;
+// Round-0 "has an edge" sentinel (graph.cu k_round0_keys): below empty,
+// above every real key ((winner < 2^31) << 32 | e).
+constexpr unsigned long long kKeyEdge = 0x7FFFFFFFFFFFFFFEull;
 constexpr unsigned long long kAllOnes = 0xFFFFFFFFFFFFFFFFull;  // "no error yet" sentinels
 constexpr int kBlock = 256;
 

@@ -194,6 +194,8 @@ enum WsSlot : int {
   WS_TOFF,        // u16 2N        offset of each arc in its tile segment (tilerank.cu)
   WS_CCROOTS,     // u32 3(n+1)    round-0 roots + current CC roots, ping-pong (cc.cu)
   WS_TSTATE,      // u64 tiles+1   tile counter + look-back states (tilerank.cu)
+  WS_XSORT,       // u32 n         edge-partitioned CC: roots list sorted by id (cc.cu)
+  WS_XTMP,        // bytes         its sort's temporary storage
   // tile-contraction levels >= 2 (tilerank.cu), one arena per level
   WS_TL2,
   WS_TL_LAST = WS_TL2 + 8,

@@ -555,7 +555,12 @@ void ensure_csr(Handle& h) {
 }
 
 // Round 0's hook keys from the device edge list (a graph uploaded for an
-// earlier build whose keys were consumed, CSR still pending).
+// earlier build whose keys were consumed, no CSR built, or one rank's
+// partition). The smaller endpoint of every edge gets the sentinel
+// kKeyEdge (above every real key, below empty): after round 0 a slot still
+// empty marks an isolated vertex, which then never enters the roots list
+// (the CSR path knows degrees; this path learns them here, and across ranks
+// the MIN exchange carries the sentinel like any key).
 __global__ void k_round0_keys(int64_t m, const int2* __restrict__ edges, uint32_t e_base,
                               unsigned long long* slot) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
@@ -565,6 +570,7 @@ __global__ void k_round0_keys(int64_t m, const int2* __restrict__ edges, uint32_
       const int lo = min(e.x, e.y), hi = max(e.x, e.y);
       const unsigned long long key = pack_key((uint32_t)lo, e_base + (uint32_t)i);
       if (key < slot[hi]) atomicMin(&slot[hi], key);
+      if (slot[lo] == kKeyInf) atomicMin(&slot[lo], kKeyEdge);
     }
   }
 }

@@ -22,6 +22,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 INF = np.iinfo(np.int64).max
+SENT = INF - 1  # kKeyEdge (common.cuh)
 
 
 def protocol_cc(n, eu, ev, e_base, exchange):
@@ -31,16 +32,19 @@ def protocol_cc(n, eu, ev, e_base, exchange):
     xbuf = exchange.xbuf.numpy()
     rep = np.arange(n, dtype=np.int64)
     ids = np.arange(len(eu), dtype=np.int64) + e_base
-    # round 0 (min mode, singleton reps): slot[v] = min over edges (u, v), u < v
+    # round 0 (min mode, singleton reps): slot[v] = min over edges (u, v),
+    # u < v; the smaller endpoint gets the "has an edge" sentinel, so after
+    # the exchange an empty slot marks an isolated vertex (kept off the list)
     slot[:n] = INF
     lo, hi = np.minimum(eu, ev), np.maximum(eu, ev)
     np.minimum.at(slot, hi, (lo << 32) | ids)
+    np.minimum.at(slot, lo, SENT)
     exchange(0, n)
-    hit = slot[:n] != INF
+    hit = slot[:n] < SENT
     rep[hit] = slot[:n][hit] >> 32
+    roots = np.nonzero(slot[:n] == SENT)[0]  # replicated on every rank, in id order
     slot[:n] = INF
     hooks = int(hit.sum())
-    roots = np.nonzero(~hit)[0]  # replicated on every rank
     while True:  # jump to convergence (compressed reps for the next hook)
         nr = rep[rep]
         if np.array_equal(nr, rep):

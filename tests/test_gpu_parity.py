@@ -718,3 +718,20 @@ def test_full_size_reference_digests(rst, name):
         if algo == 0:
             assert _sha(lv) == want["levels"], f"{name}: bfs levels"
     dg.close()
+
+
+def test_kron_verification_script_small(tmp_path):
+    # scripts/verify_kron28.py (the config-5 record) end to end at scale 16,
+    # including the 2-process partitioned run sharing the GPU
+    import json
+    import subprocess
+    import sys
+    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    out = tmp_path / "v.json"
+    r = subprocess.run([sys.executable, _os.path.join(root, "scripts", "verify_kron28.py"),
+                        "--scale", "16", "--ranks", "2", "--out", str(out)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rec = json.load(open(out))
+    assert rec["verified"] and rec["components"] == 18656  # SURVEY.md Appendix B, s=16
+    assert all(x["labels_equal_1gpu"] for x in rec["partitioned"]["per_rank"])

@@ -31,7 +31,25 @@ struct BfsCtl {
   unsigned long long mf[3];  // frontier out-degree sums (Beamer's m_f)
   int levels;                // deepest level reached
   int _pad[3];
+  unsigned long long reached;   // vertices taken off a frontier (all levels)
+  unsigned long long scanned;   // their out-degree sum: arcs read top-down
+  int d;                        // next level to expand (kernels hand over here)
+  int done;                     // frontier empty: traversal complete
+  unsigned long long vis0;      // Beamer's explored-edge count at the hand-over
 };
+
+// Small-frontier mode. A high-diameter graph (road: 13,219 levels, ~1,800
+// frontier vertices on average) spends its BFS in grid barriers: a
+// cooperative grid of ~1,200 CTAs pays several microseconds per barrier for
+// a level whose work is one dependent chain per frontier vertex. While the
+// frontier is small, the levels run instead in ONE thread-block cluster
+// (kSmallCtas CTAs x 1024 threads, one frontier vertex per thread) whose
+// hardware cluster barrier ends each level; the full cooperative grid takes
+// over when the frontier grows (hysteresis: small -> big above kSmallExit,
+// big -> small below kSmallEnter). The host relaunches only at hand-overs.
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallExit = 32768;
+constexpr int kSmallEnter = 8192;
 
 constexpr int kWarpDeg = 32;
 constexpr uint32_t kHeavyDeg = 4096;
@@ -90,22 +108,33 @@ __device__ __forceinline__ void td_visit(int32_t u, int32_t v, int d, int32_t* l
 __global__ void __launch_bounds__(kBlock)
     k_bfs(int64_t n, int64_t two_m, const uint32_t* __restrict__ offsets,
           const int32_t* __restrict__ nbrs, int32_t* level, int32_t* parent, BfsQueues qs,
-          BfsCtl* ctl, int d_start, int max_levels) {
+          BfsCtl* ctl, int max_levels, int small_enter) {
   cg::grid_group grid = cg::this_grid();
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
   const int64_t warp_id = gtid >> 5, nwarps = gsize >> 5;
   bool bottom_up = false;
-  unsigned long long visited_edges = 0;
+  const int d_start = *((volatile int*)&ctl->d);
+  unsigned long long visited_edges = *((volatile unsigned long long*)&ctl->vis0);
   for (int d = d_start; d < d_start + max_levels; ++d) {
     const int ci = d % 3, ni = (d + 1) % 3, zi = (d + 2) % 3;
     const int qn = *((volatile int*)&ctl->qn[ci]);
     const int hn = *((volatile int*)&ctl->hn[ci]);
-    if (qn + hn == 0) break;
+    if (qn + hn == 0 || (!bottom_up && qn + hn < small_enter)) {
+      // every thread saw the same counters: a uniform exit
+      if (gtid == 0) {
+        ctl->d = d;
+        ctl->done = qn + hn == 0;
+        ctl->vis0 = visited_edges;
+      }
+      return;
+    }
     const unsigned long long mf = *((volatile unsigned long long*)&ctl->mf[ci]);
     visited_edges += mf;
     if (gtid == 0) {
+      ctl->reached += (unsigned long long)(qn + hn);
+      ctl->scanned += mf;
       ctl->levels = d - 1;
       ctl->qn[zi] = 0;
       ctl->hn[zi] = 0;
@@ -166,6 +195,80 @@ __global__ void __launch_bounds__(kBlock)
     }
     grid.sync();
   }
+  if (gtid == 0) {  // (level cap reached: hand back as is)
+    ctl->d = d_start + max_levels;
+    ctl->vis0 = visited_edges;
+  }
+}
+
+// The small-frontier levels: one cluster, top-down only (a small frontier
+// never favours bottom-up), cluster barrier per level. Cross-CTA data
+// (frontier queues, counters, levels) is read through L2 (ld.cg).
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_bfs_small(const uint32_t* __restrict__ offsets, const int32_t* __restrict__ nbrs,
+                int32_t* level, int32_t* parent, BfsQueues qs, BfsCtl* ctl, int exit_above) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int64_t ctid = (int64_t)cl.block_rank() * blockDim.x + threadIdx.x;
+  const int64_t csize = (int64_t)cl.num_blocks() * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_id = ctid >> 5, nwarps = csize >> 5;
+  int d = ld_cg(&ctl->d);
+  unsigned long long visited_edges = __ldcg(&ctl->vis0);
+  for (;; ++d) {
+    const int ci = d % 3, ni = (d + 1) % 3, zi = (d + 2) % 3;
+    const int qn = ld_cg(&ctl->qn[ci]);
+    const int hn = ld_cg(&ctl->hn[ci]);
+    if (qn + hn == 0 || qn + hn > exit_above) {
+      if (ctid == 0) {
+        ctl->d = d;
+        ctl->done = qn + hn == 0;
+        ctl->vis0 = visited_edges;
+      }
+      return;
+    }
+    const unsigned long long mf = __ldcg(&ctl->mf[ci]);
+    visited_edges += mf;
+    if (ctid == 0) {
+      ctl->reached += (unsigned long long)(qn + hn);
+      ctl->scanned += mf;
+      ctl->levels = d - 1;
+      ctl->qn[zi] = 0;
+      ctl->hn[zi] = 0;
+      ctl->mf[zi] = 0;
+    }
+    const int32_t* qc = qs.q[d & 1];
+    const int32_t* hqc = qs.hq[d & 1];
+    const LevelIO io{qs.q[(d + 1) & 1], &ctl->qn[ni], qs.hq[(d + 1) & 1], &ctl->hn[ni],
+                     &ctl->mf[ni]};
+    for (int64_t base = warp_id * 32; base < qn; base += nwarps * 32) {
+      const int64_t i = base + lane;
+      int32_t u = -1;
+      uint32_t b = 0, e = 0;
+      if (i < qn) {
+        u = ld_cg(&qc[i]);
+        b = offsets[u];
+        e = offsets[u + 1];
+      }
+      const uint32_t deg = e - b;
+      unsigned wmask = __ballot_sync(0xffffffffu, u >= 0 && deg >= (uint32_t)kWarpDeg);
+      while (wmask) {  // warp gathering
+        const int src = __ffs(wmask) - 1;
+        wmask &= wmask - 1;
+        const int32_t wu = __shfl_sync(0xffffffffu, u, src);
+        const uint32_t wb = __shfl_sync(0xffffffffu, b, src);
+        const uint32_t we = __shfl_sync(0xffffffffu, e, src);
+        for (uint32_t j = wb + lane; j < we; j += 32) td_visit(wu, nbrs[j], d, level, parent, offsets, io);
+      }
+      if (u >= 0 && deg < (uint32_t)kWarpDeg)  // thread gathering
+        for (uint32_t j = b; j < e; ++j) td_visit(u, nbrs[j], d, level, parent, offsets, io);
+    }
+    for (int h = 0; h < hn; ++h) {  // heavy vertices: the whole cluster
+      const int32_t u = ld_cg(&hqc[h]);
+      const uint32_t b = offsets[u], e = offsets[u + 1];
+      for (int64_t j = b + ctid; j < e; j += csize) td_visit(u, nbrs[j], d, level, parent, offsets, io);
+    }
+    cl.sync();
+  }
 }
 
 __global__ void k_bfs_init(int64_t n, int32_t* level, int32_t* parent) {
@@ -189,6 +292,7 @@ __global__ void k_bfs_seed_one(int32_t r, int32_t* level, int32_t* parent, BfsQu
     ctl->qn[1] = 1;
   }
   ctl->mf[1] = deg;
+  ctl->d = 1;
 }
 
 namespace {
@@ -218,7 +322,10 @@ struct EmitSeed {
 
 void launch_min_vertex(Handle& h, const int32_t* lab, uint32_t* minv);
 
-__global__ void k_seed_ctl(BfsCtl* ctl, unsigned long long edges) { ctl->mf[1] = edges; }
+__global__ void k_seed_ctl(BfsCtl* ctl, unsigned long long edges) {
+  ctl->mf[1] = edges;
+  ctl->d = 1;
+}
 
 __global__ void k_sum_seed_degrees(const int32_t* q, int count, const uint32_t* offsets,
                                    unsigned long long* out) {
@@ -239,23 +346,84 @@ struct Nop {
 };
 }  // namespace
 
+// Cluster size of the small-frontier kernel: 16 CTAs (non-portable) where
+// the device schedules it, else 8; 0 = small mode unavailable / disabled
+// (RSTG_BFS_SMALL=0).
+static int small_cluster_ctas(Handle& h) {
+  static int cached = -1;
+  if (cached >= 0) return cached;
+  cached = 0;
+  const char* env = getenv("RSTG_BFS_SMALL");
+  if (env && atoi(env) == 0) return cached;
+  CK(cudaFuncSetAttribute((const void*)k_bfs_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  for (int c : {16, 8}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c);
+    cfg.blockDim = dim3(kSmallThreads);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k_bfs_small, &cfg) == cudaSuccess &&
+        nclusters > 0) {
+      cached = c;
+      break;
+    }
+    cudaGetLastError();
+  }
+  (void)h;
+  return cached;
+}
+
+// All levels from ctl->d on: the small-frontier cluster kernel while the
+// frontier stays small, the cooperative grid while it is large; each kernel
+// returns at a hand-over (ctl->d, ctl->done), read back here.
 static void run_levels(Handle& h, int32_t* level, int32_t* parent, BfsQueues qs, BfsCtl* ctl,
-                       int d_start) {
+                       int64_t frontier) {
   static int max_blocks = 0;
   if (max_blocks == 0) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs, kBlock, 0));
     max_blocks = per_sm * num_sms();
   }
+  const int cl = small_cluster_ctas(h);
   int64_t n = h.g.n, two_m = 2 * h.g.m;
   const uint32_t* offsets = h.g.offsets;
   const int32_t* nbrs = h.g.nbrs;
   int max_levels = (int)std::min<int64_t>(n + 2, 0x7ffffff0);
-  void* args[] = {&n, &two_m, (void*)&offsets, (void*)&nbrs, &level, &parent, &qs, &ctl,
-                  &d_start, &max_levels};
-  CK(cudaLaunchCooperativeKernel((void*)k_bfs, dim3(max_blocks), dim3(kBlock), args, 0,
-                                 h.stream));
-  h.stats.launches += 1;
+  int small_enter = cl ? kSmallEnter : 0;
+  for (;;) {
+    if (cl && frontier <= kSmallExit) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cl);
+      cfg.blockDim = dim3(kSmallThreads);
+      cfg.stream = h.stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cl;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, k_bfs_small, offsets, nbrs, level, parent, qs, ctl,
+                            (int)kSmallExit));
+    } else {
+      void* args[] = {&n, &two_m, (void*)&offsets, (void*)&nbrs, &level, &parent, &qs, &ctl,
+                      &max_levels, &small_enter};
+      CK(cudaLaunchCooperativeKernel((void*)k_bfs, dim3(max_blocks), dim3(kBlock), args, 0,
+                                     h.stream));
+    }
+    h.stats.launches += 1;
+    CK(cudaMemcpyAsync(h.host_box, ctl, sizeof(BfsCtl), cudaMemcpyDeviceToHost, h.stream));
+    CK(cudaStreamSynchronize(h.stream));
+    const BfsCtl* hc = reinterpret_cast<const BfsCtl*>(h.host_box);
+    if (hc->done) return;
+    frontier = (int64_t)hc->qn[hc->d % 3] + hc->hn[hc->d % 3];
+  }
 }
 
 int64_t bfs_rst(Handle& h, int32_t root, int32_t* parent, int32_t* level, int32_t* roots) {
@@ -271,7 +439,7 @@ int64_t bfs_rst(Handle& h, int32_t root, int32_t* parent, int32_t* level, int32_
   BfsCtl* ctl = reinterpret_cast<BfsCtl*>(h.ws<char>(WS_BFS_CTRL, sizeof(BfsCtl) + 64));
   const cudaStream_t s = h.stream;
 
-  h.timer.begin(s, "bfs.init");
+  h.timer.begin(s, "bfs.init", 8.0 * n);
   CK(cudaMemsetAsync(ctl, 0, sizeof(BfsCtl), s));
   k_bfs_init<<<grid_for(n), kBlock, 0, s>>>(n, level, parent);
   k_bfs_seed_one<<<1, 1, 0, s>>>(root, level, parent, qs, h.g.offsets, ctl);
@@ -279,12 +447,15 @@ int64_t bfs_rst(Handle& h, int32_t root, int32_t* parent, int32_t* level, int32_
   h.stats.step(n);
   h.timer.end(s);
 
-  h.timer.begin(s, "bfs.levels");
+  // compulsory per reached vertex: offsets 8 B, its level and parent 8 B;
+  // per arc of a reached vertex 4 B (the neighbour id) -- counted on the
+  // device as the frontiers go (ctl->reached, ctl->scanned)
+  h.timer.begin(s, "bfs.levels", 0.0);
   run_levels(h, level, parent, qs, ctl, 1);
   h.timer.end(s);
-  CK(cudaMemcpyAsync(h.host_box, &ctl->levels, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const int levels_root = *reinterpret_cast<int*>(h.host_box);
+  const BfsCtl* hc = reinterpret_cast<const BfsCtl*>(h.host_box);
+  const int levels_root = hc->levels;
+  h.timer.add_bytes("bfs.levels", 16.0 * (double)hc->reached + 4.0 * (double)hc->scanned);
   h.stats.levels = levels_root;
   // one barrier per level plus the final empty level (with the init step:
   // depth + 2 for a connected graph, bfs_rst.hpp:19)
@@ -322,12 +493,11 @@ int64_t bfs_rst(Handle& h, int32_t root, int32_t* parent, int32_t* level, int32_
   CK(cudaMemcpyAsync(&ctl->qn[1], h.host_box, sizeof(int), cudaMemcpyHostToDevice, s));
   CK_LAUNCH();
   h.timer.end(s);
-  h.timer.begin(s, "bfs.levels2");
-  run_levels(h, level, parent, qs, ctl, 1);
+  h.timer.begin(s, "bfs.levels2", 0.0);
+  run_levels(h, level, parent, qs, ctl, seeds);
   h.timer.end(s);
-  CK(cudaMemcpyAsync(h.host_box, &ctl->levels, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const int lv2 = *reinterpret_cast<int*>(h.host_box);
+  const int lv2 = hc->levels;
+  h.timer.add_bytes("bfs.levels2", 16.0 * (double)hc->reached + 4.0 * (double)hc->scanned);
   h.stats.levels = std::max<int64_t>(levels_root, lv2);
   h.stats.steps += lv2 + 2;
   return 1 + (int64_t)seeds;

@@ -938,16 +938,22 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
       throw AlgoError("hooking failed to converge");
     }
     CK(cudaMemsetAsync(counter + 1, 0, 2 * sizeof(unsigned long long), h.stream));
-    // edge 8 B + two rep gathers per visited edge (+ 4 B list entry when filtered)
-    const double visited = (h.cc_round >= 2 && h.cc_active >= 0) ? (double)h.cc_active : (double)m;
-    h.timer.begin(h.stream, mode == 0 ? "cc.hook_min" : "cc.hook_max",
-                  visited * ((h.cc_round >= 2 && h.cc_active >= 0) ? 20.0 : 16.0));
+    // compulsory: each visited edge 8 B (+ 4 B list entry when filtered),
+    // the rep array once (4 B per vertex, at most two gathers per edge),
+    // 4 B per crossing edge appended (added once the count is read)
+    const bool filtered = h.cc_round >= 2 && h.cc_active >= 0;
+    const double visited = filtered ? (double)h.cc_active : (double)m;
+    const char* hook_phase = mode == 0 ? "cc.hook_min" : "cc.hook_max";
+    h.timer.begin(h.stream, hook_phase,
+                  visited * (filtered ? 12.0 : 8.0) + std::min(4.0 * n, 8.0 * visited));
     cc_hook_round(h, mode, rep, slot, counter + 1, any);
     h.timer.end(h.stream);
     // hooks so far, crossing, any; [20] the round-0 roots count, [21] the
     // current roots count (same read)
     h.read_box(reinterpret_cast<int64_t*>(counter), 22);
+    if (h.cc_round >= 1 && m > 0) h.timer.add_bytes(hook_phase, 4.0 * h.host_box[1]);
     const int64_t r0_count = have_r0 ? h.host_box[20] : 0;
+    const int64_t cur_roots = have_r0 ? h.host_box[21] : n;
     prev_total = total;
     total = h.host_box[0];
     bool proposed = h.host_box[2] != 0;
@@ -994,7 +1000,8 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     h.stats.rounds = round + 1;
     // a round without proposals applies nothing (cc_forest.cpp:91)
     if (!proposed) break;
-    h.timer.begin(h.stream, "cc.apply", 16.0 * n);  // (upper bound: every vertex a root)
+    // per current root: list entry 4 B, slot 8 B, rep or next-list entry 4 B
+    h.timer.begin(h.stream, "cc.apply", 16.0 * cur_roots);
     CK(cudaMemsetAsync(rcount + 2, 0, sizeof(unsigned long long), h.stream));
     k_apply_roots<<<grid_for(n), kBlock, 0, h.stream>>>(in_list, rcount + 1, n, rep, io, rl[out],
                                                         rcount + 2);

@@ -49,12 +49,14 @@ void PhaseTimer::begin(cudaStream_t s, const char* name, double bytes) {
   if (!enabled) return;
   Rec r{name, bytes, get(), nullptr};
   CK(cudaEventRecord(r.a, s));
+  open_.push_back(recs_.size());
   recs_.push_back(r);
 }
 void PhaseTimer::end(cudaStream_t s) {
   nvtxRangePop();
-  if (!enabled || recs_.empty()) return;
-  Rec& r = recs_.back();
+  if (!enabled || open_.empty()) return;
+  Rec& r = recs_[open_.back()];
+  open_.pop_back();
   r.b = get();
   CK(cudaEventRecord(r.b, s));
 }
@@ -68,6 +70,7 @@ std::vector<PhaseRec> PhaseTimer::collect() {
     out.push_back(PhaseRec{r.name, (double)ms, r.bytes});
   }
   recs_.clear();
+  open_.clear();
   used_ = 0;
   return out;
 }

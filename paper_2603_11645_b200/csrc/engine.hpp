@@ -48,6 +48,20 @@ class PhaseTimer {
  public:
   void begin(cudaStream_t s, const char* name, double bytes = 0);
   void end(cudaStream_t s);
+  // Adds algorithmic bytes to the open phase (known only once it runs).
+  void add_bytes(double b) {
+    if (enabled && !open_.empty()) recs_[open_.back()].bytes += b;
+  }
+  // ... or to the latest closed phase of that name (bytes counted on the
+  // device, read back after the phase)
+  void add_bytes(const char* name, double b) {
+    if (!enabled) return;
+    for (auto it = recs_.rbegin(); it != recs_.rend(); ++it)
+      if (it->name == name) {
+        it->bytes += b;
+        return;
+      }
+  }
   // Synchronizes and returns the phases in order; clears.
   std::vector<PhaseRec> collect();
   bool enabled = false;
@@ -59,6 +73,7 @@ class PhaseTimer {
     cudaEvent_t a, b;
   };
   std::vector<Rec> recs_;
+  std::vector<size_t> open_;  // indices of open phases (phases nest)
   std::vector<cudaEvent_t> pool_;
   size_t used_ = 0;
   cudaEvent_t get();
@@ -168,11 +183,13 @@ enum WsSlot : int {
   // PR-RST
   WS_PR_SCRATCH,  // int32 n
   WS_PR_ONPATH,   // u8 n
-  WS_PR_FRESH,    // u8 n
+  WS_PR_FRESH,    // u8 n          skip level | root bit per vertex
   WS_PR_GROOT,    // u8 n
-  WS_PR_GU,       // int32 n
-  WS_PR_ANC,      // int32 n*L (level-major)
-  WS_PR_NEXT,     // int32 n (jump double buffer)
+  WS_PR_GU,       // u32 n         graft endpoints (marking seeds) of a round
+  WS_PR_ANC,      // int32 n*K     skip pointers, level-major (level k at (k-1)*n)
+  WS_PR_NEXT,     // u32 n         grafted roots of a round
+  WS_PR_BYL,      // u32 n         vertices by descending skip level
+  WS_PR_MK,       // u32 n         marked vertices, one queue per exact level
   // BFS
   WS_BFS_LEVEL,   // int32 n
   WS_BFS_Q0,      // int32 n

@@ -394,7 +394,10 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   if (use_tiles) {
     const TileRank tr = lr_rank_tiles(h, P, N, io.S, labels, cc_slots, T, verify);
     // seg of every slot; per tree edge eto, the other seg, two offsets, two starts, parent
-    h.timer.begin(s, "euler.orient", 4.0 * N + 28.0 * T);
+    // compulsory: per slot its arc's segment word 4 B + offset 2 B; per tree
+    // edge the pair's heads 8 B, the other arc's word 4 B + offset 2 B, the
+    // parent 4 B (segment starts: one small L2-resident table)
+    h.timer.begin(s, "euler.orient", 6.0 * N + 18.0 * T);
     k_orient_tiles<<<grid_for(N), kBlock, 0, s>>>(N, reinterpret_cast<const uint2*>(io.eto), tr.seg,
                                                   tr.off, tr.segstart, parent);
     CK_LAUNCH();

@@ -1,170 +1,399 @@
 // pr.cu -- PR-RST path-reversal rooted spanning tree (pr_rst.cpp:267-314).
 //
-// Round = {graft, mark, check, reverse, batched jump, rebuild ancestors}
-// exactly as the reference, each step a coalesced vertex/edge sweep:
-//   graft proposals   k_hook (shared with CC; pr_rst.cpp:82-99)
-//   resolve + update  k_graft_resolve / k_graft_update (:112-128)
-//   mark_paths        one launch per doubling level k; marks carry the level
-//                     they were set in, so "marked before level k" replaces
-//                     the reference's cur/fresh double buffer and one kernel
-//                     per level suffices (:135-164). A level that adds
-//                     nothing stops the remaining launches on the device;
-//                     later levels could not add anything either (the marked
-//                     set is a contiguous 2^(k+1)-prefix of each chain).
-//   reverse_paths     two sweeps (:178-204)
-//   batched_jump      Jacobi snapshot hops, 2^batch per barrier (:216-252);
-//                     converged barriers exit on the device
-//   rebuild ancestors level-major table anc[k*n + v] (:254-265); a level
-//                     equal to its predecessor stops the rebuild (all higher
-//                     levels are then identical) and mark reads are clamped.
-// The only host synchronisation is one flag read per round.
+// Rounds of {graft, mark, check, reverse, jump} exactly as the reference
+// (graft_round :72-133, mark_paths :135-164, the check :281-288,
+// reverse_paths :178-204, batched_jump :216-252), each on the B200 as a
+// sweep over the set it concerns rather than over all n vertices:
+//
+//   graft     proposals: k_hook (shared with the CC, active-edge filtered);
+//             resolve + update over the CURRENT ROOTS list only (a graft
+//             proposal targets a root), which is compacted as it goes.
+//   mark      the reference marks the path from each graft endpoint u to
+//             its tree root by doubling over an n x L "special ancestor"
+//             table rebuilt every round (:254-265) -- L full sweeps to
+//             rebuild, L more to mark. Here the ancestor structure is a
+//             randomised skip list over the parent forest: vertex v has
+//             level lvl(v) = trailing ones of a hash of v (P[lvl >= k] =
+//             2^-k), and ptr_k[v], for lvl(v) >= k, is v's nearest proper
+//             ancestor of level >= k (or its tree root). Rebuilding level k
+//             walks ptr_{k-1} from the n/2^k vertices of level >= k,
+//             expected 2 hops each: O(n) work per round instead of O(n L).
+//             Marking then touches only path vertices: an ascent from each
+//             endpoint climbs the levels (expected O(log n) hops) to the
+//             root, and a descent fills, level by level from the top, the
+//             gaps between consecutive marked vertices of the level above
+//             (expected O(1) hops per walker per level). The marked set is
+//             exactly the reference's (all ancestors of each endpoint), kept
+//             as per-level frontier queues in HBM.
+//   check     over the grafted roots (each marked and still a root).
+//   reverse   over the marked queues only.
+//   jump      rep stays fully converged between rounds, so after a graft
+//             only the grafted roots' pointers chain: they are pointer-
+//             jumped as a list (one cooperative launch), then one gather
+//             rep[v] = rep[rep[v]] -- the converged reps batched_jump ends
+//             with, whatever the batch.
+// Tree edges and converged reps equal the CC's (same proposals, same
+// rounds); the parents are those of the reference's path reversals.
+// The designated root's tree is re-rooted at the end (:298-303).
 #include "engine.hpp"
 
 namespace rstg {
 
-void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_base,
-                 const int32_t* rep, unsigned long long* slot, int* any_prop);
 void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* slot,
                    unsigned long long* out_count, int* any_prop);
 void cc_round_done(Handle& h, int64_t out_count);
 void cc_reset_rounds(Handle& h);
+void compress_via_roots(Handle& h, int32_t* rep, int64_t n, const uint32_t* roots,
+                        const unsigned long long* nroots);
 
-// Device control block layout (int32 words in the WS_BFS_CTRL workspace).
+namespace {
+
+constexpr int kMaxLvl = 31;        // levels 0..K, K <= 31 (n < 2^31)
+constexpr uint8_t kRootBit = 0x80;  // lv[v]: level | root-of-its-tree bit
+
+// Device control block (u64 words in WS_BFS_CTRL).
 enum PrCtl : int {
-  C_ANY = 0,      // any graft proposal this round
-  C_BAD_REV,      // reversal found a marked vertex with no source
-  C_JUMP_DONE,    // batched jump converged
-  C_JUMP_FINAL,   // index (0/1) of the buffer holding the jumped reps
-  C_LMAX,         // valid ancestor levels
-  C_MARK_STOP,    // marking stopped (a level added nothing)
-  C_GREW0,        // C_GREW0 + k: level k added a mark
-  C_CHANGED0 = C_GREW0 + 40,  // C_CHANGED0 + k: anc level k differs from k-1
-  C_NWORDS = C_CHANGED0 + 40
+  P_NROOTS_IN = 0,  // current roots list length
+  P_NROOTS_OUT,     // next roots list length
+  P_NGRAFT,         // grafts this round (seeds / grafted roots)
+  P_CROSSING,       // crossing edges of the graft proposals
+  P_ANY,            // int: any proposal (block_flag)
+  P_BAD_REV,        // int: reversal found a marked vertex with no source
+  P_MCNT0 = 8,      // P_MCNT0 + b: marked vertices of exact level b
+  P_NWORDS = P_MCNT0 + kMaxLvl + 2
 };
 
-__global__ void k_pr_init(int64_t n, int32_t* parent, int32_t* rep, int32_t* scratch,
-                          uint8_t* mark, uint8_t* groot, unsigned long long* slot) {
+__device__ __forceinline__ uint32_t vertex_level(uint32_t v, int K) {
+  unsigned long long x = (unsigned long long)v + 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return min((uint32_t)__ffsll((long long)~x) - 1u, (uint32_t)K);  // trailing ones
+}
+__device__ __forceinline__ bool is_root(const uint8_t* lv, int32_t x) {
+  return (lv[x] & kRootBit) != 0;
+}
+__device__ __forceinline__ int lvl_of(const uint8_t* lv, int32_t x) { return lv[x] & 0x7F; }
+// ptr_k(x): k = 0 the parent, else the level-k skip pointer
+__device__ __forceinline__ int32_t up(const int32_t* parent, const int32_t* ptr, int64_t n, int k,
+                                      int32_t x) {
+  return k == 0 ? parent[x] : ptr[(int64_t)(k - 1) * n + x];
+}
+
+__global__ void k_pr_init(int64_t n, int K, int32_t* parent, int32_t* rep, int32_t* scratch,
+                          uint8_t* mark, uint8_t* lv, unsigned long long* slot,
+                          unsigned long long* hist) {
+  __shared__ unsigned int s_h[kMaxLvl + 1];
+  for (int i = threadIdx.x; i <= kMaxLvl; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     parent[v] = rep[v] = (int32_t)v;
     scratch[v] = -1;
     mark[v] = 0;
-    groot[v] = 0;
     slot[v] = kKeyInf;
+    const uint32_t l = vertex_level((uint32_t)v, K);
+    lv[v] = (uint8_t)l | kRootBit;  // every vertex starts as its own tree
+    atomicAdd(&s_h[l], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= K; i += blockDim.x)
+    if (s_h[i]) atomicAdd(&hist[i], (unsigned long long)s_h[i]);
+}
+
+// Vertices sorted by descending level: level >= k is the prefix [0, C_k).
+// cursor[l] starts at C_{l+1}; order within a level is irrelevant.
+__global__ void k_pr_bylevel(int64_t n, const uint8_t* __restrict__ lv, uint32_t* byl,
+                             unsigned long long* cursor) {
+  __shared__ unsigned int s_c[kMaxLvl + 1];
+  __shared__ unsigned long long s_b[kMaxLvl + 1];
+  for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
+    for (int i = threadIdx.x; i <= kMaxLvl; i += blockDim.x) s_c[i] = 0;
+    __syncthreads();
+    const int64_t v = b0 + threadIdx.x;
+    int l = -1;
+    unsigned pos = 0;
+    if (v < n) {
+      l = lv[v] & 0x7F;
+      pos = atomicAdd(&s_c[l], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i <= kMaxLvl; i += blockDim.x)
+      s_b[i] = s_c[i] ? atomicAdd(&cursor[i], (unsigned long long)s_c[i]) : 0ull;
+    __syncthreads();
+    if (l >= 0) byl[s_b[l] + pos] = (uint32_t)v;
+    __syncthreads();
   }
 }
 
-// make_pr_state's anc[v][k] = v (pr_rst.cpp:60-68): every level of the
-// identity table equals level 0, so only level 0 is written and the valid
-// level count starts at 1 (reads of higher levels clamp to it).
-__global__ void k_anc_identity(int64_t n, int32_t* anc) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x)
-    anc[v] = (int32_t)v;
+// Level-k skip pointers (k >= 1) of the vertices of level >= k.
+template <int kB>
+__global__ void __launch_bounds__(kBlock)
+    k_pr_rebuild(int64_t count, int k, int64_t n, const uint32_t* __restrict__ byl,
+                 const int32_t* __restrict__ parent, const uint8_t* __restrict__ lv, int32_t* ptr) {
+  const int32_t* __restrict__ below = k == 1 ? parent : ptr + (int64_t)(k - 2) * n;
+  int32_t* __restrict__ out = ptr + (int64_t)(k - 1) * n;
+  const int64_t g = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < count; i0 += kB * g) {
+    int32_t v[kB], x[kB];
+    bool walk[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int64_t i = i0 + j * g;
+      walk[j] = i < count;
+      v[j] = walk[j] ? (int32_t)byl[i] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      if (walk[j] && is_root(lv, v[j])) {
+        x[j] = v[j];
+        walk[j] = false;
+      } else {
+        x[j] = walk[j] ? below[v[j]] : 0;
+      }
+    }
+    // walks of kB vertices advance together (their loads in flight at once)
+    for (;;) {
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        if (!walk[j]) continue;
+        const uint8_t l = lv[x[j]];
+        if ((l & kRootBit) || (l & 0x7F) >= k) {
+          walk[j] = false;
+        } else {
+          x[j] = below[x[j]];
+          any = true;
+        }
+      }
+      if (!any) break;
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j)
+      if (i0 + j * g < count) out[v[j]] = x[j];
+  }
 }
 
-// resolve winners against the frozen rep (pr_rst.cpp:112-122)
-__global__ void k_graft_resolve(int64_t n, const int2* __restrict__ edges, uint32_t e_base,
-                                const int32_t* __restrict__ rep,
-                                const unsigned long long* __restrict__ slot,
-                                uint8_t* __restrict__ mark, int32_t* __restrict__ scratch,
-                                uint8_t* __restrict__ groot, int32_t* __restrict__ gu) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
+// Append x to the marked queue of its exact level (bucket b occupies
+// [base_b, base_b + capacity_b) of mk: the descending-level layout of byl).
+__device__ __forceinline__ void enqueue(uint32_t* mk, const unsigned long long* bbase,
+                                        unsigned long long* mcnt, int b, int32_t x) {
+  const unsigned long long p = atomicAdd(&mcnt[b], 1ull);
+  mk[bbase[b] + p] = (uint32_t)x;
+}
+
+// graft_round resolve (pr_rst.cpp:112-122) over the current roots: root v
+// with a proposal loses to the key's winner; u = the endpoint in v's tree
+// (marked: it starts the path to reverse), w = the other (u's new parent).
+// seeds[i] = u and grafted[i] = v share one index.
+__global__ void k_pr_resolve(const uint32_t* __restrict__ list, const unsigned long long* cnt,
+                             int64_t n, const int2* __restrict__ edges, uint32_t e_base,
+                             const int32_t* __restrict__ rep, const unsigned long long* __restrict__ slot,
+                             uint8_t* mark, int32_t* scratch, uint32_t* seeds, uint32_t* grafted,
+                             unsigned long long* ngraft) {
+  const int64_t R = list ? (int64_t)*cnt : n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = list ? list[i] : (uint32_t)i;
     const unsigned long long key = slot[v];
     if (key == kKeyInf) continue;
     const int2 uv = edges[(uint32_t)key - e_base];
     const int32_t u = (rep[uv.x] == (int32_t)v) ? uv.x : uv.y;
     const int32_t w = (u == uv.x) ? uv.y : uv.x;
-    mark[u] = 1;  // seeds carry level tag 1
+    mark[u] = 1;
     scratch[u] = w;
-    groot[v] = 1;
-    gu[v] = u;
+    const unsigned long long p = atomicAdd(ngraft, 1ull);
+    seeds[p] = (uint32_t)u;
+    grafted[p] = v;
   }
 }
 
-// rep update (pr_rst.cpp:123-128)
-__global__ void k_graft_update(int64_t n, int32_t* rep, unsigned long long* slot) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long key = slot[v];
-    if (key == kKeyInf) continue;
-    rep[v] = (int32_t)(key >> 32);
-    slot[v] = kKeyInf;
-  }
-}
-
-// One mark_paths level k (pr_rst.cpp:146-153). Marked-before-level-k means
-// tag in [1, k+1]; new marks get tag k+2.
+// graft_round update (pr_rst.cpp:123-128): rep = winner; the roots that did
+// not graft form the next roots list.
 __global__ void __launch_bounds__(kBlock)
-    k_mark_level(int64_t n, int k, const int32_t* __restrict__ anc, uint8_t* mark, int* ctl) {
-  if (k > 0 && (ctl[C_MARK_STOP] || !ctl[C_GREW0 + k - 1])) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl[C_MARK_STOP] = 1;
-    return;
-  }
-  const int kk = min(k, ctl[C_LMAX] - 1);
-  const int32_t* lvl = anc + (int64_t)kk * n;
-  bool grew = false;
-  // four marks per load (almost all are 0: one 32-bit test skips them); the
-  // mark buffer is padded past n
-  const int64_t words = (n + 3) / 4;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t t4 = reinterpret_cast<const volatile uint32_t*>(mark)[w];
-    if (t4 == 0) continue;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const uint32_t t = (t4 >> (8 * b)) & 0xFFu;
-      const int64_t v = 4 * w + b;
-      if (t == 0 || t > (uint32_t)(k + 1) || v >= n) continue;
-      const int32_t a = lvl[v];
-      if (mark[a] == 0) {
-        mark[a] = (uint8_t)(k + 2);
-        grew = true;
+    k_pr_update(const uint32_t* __restrict__ list, const unsigned long long* cnt, int64_t n,
+                int32_t* rep, unsigned long long* slot, uint32_t* out_list,
+                unsigned long long* out_cnt) {
+  const int64_t R = list ? (int64_t)*cnt : n;
+  __shared__ uint32_t s_n;
+  __shared__ unsigned long long s_b;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < R; b += (int64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const int64_t i = b + threadIdx.x;
+    bool keep = false;
+    uint32_t v = 0;
+    if (i < R) {
+      v = list ? list[i] : (uint32_t)i;
+      const unsigned long long key = slot[v];
+      if (key == kKeyInf) {
+        keep = true;
+      } else {
+        rep[v] = (int32_t)(key >> 32);
+        slot[v] = kKeyInf;
       }
     }
-  }
-  block_flag(grew, &ctl[C_GREW0 + k]);
-}
-
-// The graft check (pr_rst.cpp:281-288): every grafted root r is marked and
-// still a root. Records the smallest offending (r, u).
-__global__ void k_graft_check(int64_t n, const uint8_t* groot, const uint8_t* mark,
-                              const int32_t* parent, const int32_t* gu,
-                              unsigned long long* bad) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    if (!groot[v]) continue;
-    if (!mark[v] || parent[v] != (int32_t)v)
-      atomicMin(bad, ((unsigned long long)v << 32) | (uint32_t)gu[v]);
+    const uint32_t pos = keep ? atomicAdd(&s_n, 1u) : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) s_b = s_n ? atomicAdd(out_cnt, (unsigned long long)s_n) : 0ull;
+    __syncthreads();
+    if (keep) out_list[s_b + pos] = v;
+    __syncthreads();
   }
 }
-__global__ void k_check_one(int32_t r, int32_t u, const uint8_t* mark, const int32_t* parent,
-                            unsigned long long* bad) {
-  if (!mark[r] || parent[r] != r) atomicMin(bad, ((unsigned long long)r << 32) | (uint32_t)u);
-}
-__global__ void k_clear_groot(int64_t n, uint8_t* groot) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x)
-    groot[v] = 0;
+
+// Marking, ascent: from each seed u climb to its tree root -- at level k
+// (starting at lvl(u)) follow ptr_k; a vertex of a higher level lifts the
+// climb to that level. Every vertex passed is on the path: marked and
+// queued by its exact level. Seeds themselves are queued first, block-
+// aggregated (round 0 has ~n/2 seeds, all singleton roots).
+__global__ void __launch_bounds__(kBlock)
+    k_pr_ascend(const uint32_t* __restrict__ seeds, const unsigned long long* nseeds, int64_t n,
+                const int32_t* __restrict__ parent, const int32_t* __restrict__ ptr,
+                const uint8_t* __restrict__ lv, uint8_t* mark, uint32_t* mk,
+                const unsigned long long* __restrict__ bbase, unsigned long long* mcnt) {
+  __shared__ unsigned int s_c[kMaxLvl + 1];
+  __shared__ unsigned long long s_b[kMaxLvl + 1];
+  const int64_t S = (int64_t)*nseeds;
+  for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < S; b0 += (int64_t)gridDim.x * blockDim.x) {
+    for (int i = threadIdx.x; i <= kMaxLvl; i += blockDim.x) s_c[i] = 0;
+    __syncthreads();
+    const int64_t i = b0 + threadIdx.x;
+    int32_t u = -1;
+    int l = 0;
+    unsigned pos = 0;
+    if (i < S) {
+      u = (int32_t)seeds[i];
+      l = lvl_of(lv, u);
+      pos = atomicAdd(&s_c[l], 1u);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j <= kMaxLvl; j += blockDim.x)
+      s_b[j] = s_c[j] ? atomicAdd(&mcnt[j], (unsigned long long)s_c[j]) : 0ull;
+    __syncthreads();
+    if (u >= 0) {
+      mk[bbase[l] + s_b[l] + pos] = (uint32_t)u;
+      int32_t c = u;
+      int k = l;
+      while (!is_root(lv, c)) {
+        const int32_t x = up(parent, ptr, n, k, c);
+        mark[x] = 1;
+        const int lx = lvl_of(lv, x);
+        enqueue(mk, bbase, mcnt, lx, x);
+        if (is_root(lv, x)) break;
+        if (lx > k) k = lx;
+        c = x;
+      }
+    }
+    __syncthreads();
+  }
 }
 
-// reverse_paths (pr_rst.cpp:186-190, 191-201)
-__global__ void k_reverse_a(int64_t n, const uint8_t* __restrict__ mark,
-                            const int32_t* __restrict__ parent, int32_t* scratch) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    if (!mark[v]) continue;
+// Marking, descent at level j: every marked vertex a of level > j walks
+// ptr_j up to the next vertex of level > j (or the root), marking the
+// level-j vertices of that gap (queued into bucket j, not read here).
+__global__ void __launch_bounds__(kBlock)
+    k_pr_descend(int j, int K, int64_t n, const int32_t* __restrict__ parent,
+                 const int32_t* __restrict__ ptr, const uint8_t* __restrict__ lv, uint8_t* mark,
+                 uint32_t* mk, const unsigned long long* __restrict__ bbase,
+                 unsigned long long* mcnt) {
+  __shared__ unsigned long long s_pre[kMaxLvl + 2];
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int b = j + 1; b <= K; ++b) {
+      s_pre[b] = t;
+      t += mcnt[b];
+    }
+    s_pre[K + 1] = t;
+  }
+  __syncthreads();
+  const int64_t T = (int64_t)s_pre[K + 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int b = j + 1;
+    while (b < K && (int64_t)s_pre[b + 1] <= i) ++b;
+    const int32_t a = (int32_t)mk[bbase[b] + (i - (int64_t)s_pre[b])];
+    if (is_root(lv, a)) continue;
+    int32_t x = up(parent, ptr, n, j, a);
+    while (!is_root(lv, x) && lvl_of(lv, x) == j) {
+      mark[x] = 1;
+      enqueue(mk, bbase, mcnt, j, x);
+      x = up(parent, ptr, n, j, x);
+    }
+  }
+}
+
+// The check (pr_rst.cpp:281-288): each grafted root is marked and still a
+// root; records the smallest offending (r, u).
+__global__ void k_pr_check(const uint32_t* __restrict__ grafted, const uint32_t* __restrict__ seeds,
+                           const unsigned long long* ngraft, const uint8_t* mark,
+                           const int32_t* parent, unsigned long long* bad) {
+  const int64_t G = (int64_t)*ngraft;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < G;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = grafted[i];
+    if (!mark[r] || parent[r] != (int32_t)r)
+      atomicMin(bad, ((unsigned long long)r << 32) | seeds[i]);
+  }
+}
+
+// Index i over all marked queues (every level) -> the marked vertex.
+struct MarkedAt {
+  const uint32_t* mk;
+  const unsigned long long* bbase;
+  unsigned long long pre[kMaxLvl + 2];
+  int K;
+  __device__ int32_t operator()(int64_t i) const {
+    int b = 0;
+    while (b < K && (int64_t)pre[b + 1] <= i) ++b;
+    return (int32_t)mk[bbase[b] + (i - (int64_t)pre[b])];
+  }
+};
+__device__ void load_marked(MarkedAt& m, const unsigned long long* mcnt) {
+  unsigned long long t = 0;
+  for (int b = 0; b <= m.K; ++b) {
+    m.pre[b] = t;
+    t += mcnt[b];
+  }
+  m.pre[m.K + 1] = t;
+}
+
+// reverse_paths (pr_rst.cpp:186-201) over the marked vertices only.
+__global__ void k_pr_reverse_a(int K, const uint32_t* mk, const unsigned long long* bbase,
+                               const unsigned long long* mcnt, const int32_t* __restrict__ parent,
+                               int32_t* scratch) {
+  __shared__ MarkedAt m;
+  if (threadIdx.x == 0) {
+    m.mk = mk;
+    m.bbase = bbase;
+    m.K = K;
+    load_marked(m, mcnt);
+  }
+  __syncthreads();
+  const int64_t T = (int64_t)m.pre[K + 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = m(i);
     const int32_t p = parent[v];
-    if (p != (int32_t)v) scratch[p] = (int32_t)v;
+    if (p != v) scratch[p] = v;
   }
 }
-__global__ void k_reverse_b(int64_t n, uint8_t* mark, int32_t* parent, int32_t* scratch,
-                            int* ctl) {
+__global__ void k_pr_reverse_b(int K, const uint32_t* mk, const unsigned long long* bbase,
+                               const unsigned long long* mcnt, uint8_t* mark, int32_t* parent,
+                               int32_t* scratch, int* bad_rev) {
+  __shared__ MarkedAt m;
+  if (threadIdx.x == 0) {
+    m.mk = mk;
+    m.bbase = bbase;
+    m.K = K;
+    load_marked(m, mcnt);
+  }
+  __syncthreads();
+  const int64_t T = (int64_t)m.pre[K + 1];
   bool bad = false;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    if (!mark[v]) continue;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = m(i);
     const int32_t s = scratch[v];
     if (s < 0) {
       bad = true;
@@ -174,100 +403,23 @@ __global__ void k_reverse_b(int64_t n, uint8_t* mark, int32_t* parent, int32_t* 
     scratch[v] = -1;
     mark[v] = 0;
   }
-  block_flag(bad, &ctl[C_BAD_REV]);
+  block_flag(bad, bad_rev);
 }
-
-// One batched_jump barrier (pr_rst.cpp:235-244). Buffers alternate; a
-// converged state makes later barriers no-ops.
-template <int kB>
-__global__ void __launch_bounds__(kBlock)
-    k_jump_barrier(int64_t n, int64_t hops, int barrier, int32_t* buf0, int32_t* buf1,
-                   int* ctl, int* not_done) {
-  if (ctl[C_JUMP_DONE]) return;
-  const int32_t* __restrict__ snap = (barrier & 1) ? buf1 : buf0;
-  int32_t* __restrict__ next = (barrier & 1) ? buf0 : buf1;
-  // kB vertices' chains walked together: each hop's loads issued at once
-  bool pending = false;
-  const int64_t g = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n; v0 += kB * g) {
-    int32_t x[kB];
-    bool walk[kB];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      walk[j] = v0 + j * g < n;
-      x[j] = walk[j] ? snap[v0 + j * g] : 0;
-    }
-    for (int64_t t = 1; t < hops; ++t) {
-      bool any = false;
-#pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        if (!walk[j]) continue;
-        const int32_t nx = snap[x[j]];
-        if (nx == x[j]) walk[j] = false;
-        else x[j] = nx;
-        any |= walk[j];
-      }
-      if (!any) break;
-    }
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      if (v0 + j * g >= n) continue;
-      next[v0 + j * g] = x[j];
-      if (snap[x[j]] != x[j]) pending = true;
-    }
-  }
-  block_flag(pending, not_done);
-}
-// Closes barrier `barrier`: converged -> record which buffer holds reps.
-__global__ void k_jump_close(int barrier, int* ctl, int* not_done) {
-  if (ctl[C_JUMP_DONE]) return;
-  if (*not_done == 0) {
-    ctl[C_JUMP_DONE] = 1;
-    ctl[C_JUMP_FINAL] = (barrier & 1) ? 0 : 1;
-  }
-  *not_done = 0;
-}
-__global__ void k_jump_copyback(int64_t n, int32_t* rep, const int32_t* other, const int* ctl) {
-  if (ctl[C_JUMP_FINAL] == 0) return;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x)
-    rep[v] = other[v];
-}
-
-// rebuild_special_ancestors level k >= 1 (pr_rst.cpp:260-264).
-template <int kB>
-__global__ void __launch_bounds__(kBlock) k_anc_level(int64_t n, int k, int32_t* anc, int* ctl) {
-  if (k >= 2 && !ctl[C_CHANGED0 + k - 1]) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(&ctl[C_LMAX], k);
-    return;
-  }
-  // (distinct levels of one buffer: restrict-qualified so the stores do not
-  // order the next vertices' loads; kB vertices' gathers in flight -- 4 on
-  // graphs larger than L2, where each gather waits on DRAM)
-  const int32_t* __restrict__ prev = anc + (int64_t)(k - 1) * n;
-  int32_t* __restrict__ cur = anc + (int64_t)k * n;
-  bool changed = false;
-  const int64_t g = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n; v0 += kB * g) {
-    int32_t a[kB], b[kB];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) a[j] = v0 + j * g < n ? __ldcs(&prev[v0 + j * g]) : 0;
-#pragma unroll
-    for (int j = 0; j < kB; ++j) b[j] = v0 + j * g < n ? prev[a[j]] : 0;
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      if (v0 + j * g >= n) continue;
-      cur[v0 + j * g] = b[j];
-      changed |= (b[j] != a[j]);
-    }
-  }
-  block_flag(changed, &ctl[C_CHANGED0 + k]);
+// Grafted roots are roots no more (their tree hangs off the winner's now).
+__global__ void k_pr_unroot(const uint32_t* __restrict__ grafted, const unsigned long long* ngraft,
+                            uint8_t* lv) {
+  const int64_t G = (int64_t)*ngraft;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < G;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lv[grafted[i]] &= (uint8_t)~kRootBit;
 }
 
 __global__ void k_set_i32(int32_t* p, int32_t v) { *p = v; }
 __global__ void k_set_u8(uint8_t* p, uint8_t v) { *p = v; }
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
-static int ceil_log2_i(int64_t x) {
+int ceil_log2_i(int64_t x) {
   int k = 0;
   int64_t p = 1;
   while (p < x) {
@@ -277,137 +429,178 @@ static int ceil_log2_i(int64_t x) {
   return k;
 }
 
+}  // namespace
+
 void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
-  // batched gathers pay once a level of the ancestor table (4n bytes) no
-  // longer sits in L2
-  const bool big = h.g.n > (int64_t{1} << 22);
-  const int64_t n = h.g.n, m = h.g.m;
-  const int L = std::max(ceil_log2_i(std::max<int64_t>(n, 1)), 1);
+  const int64_t n = h.g.n;
+  const int K = std::min(std::max(ceil_log2_i(std::max<int64_t>(n, 1)), 1), kMaxLvl);
   int32_t* rep = h.ws<int32_t>(WS_REP, n);
   int32_t* scratch = h.ws<int32_t>(WS_PR_SCRATCH, n);
   uint8_t* mark = h.ws<uint8_t>(WS_PR_ONPATH, n);
-  uint8_t* groot = h.ws<uint8_t>(WS_PR_GROOT, n);
-  int32_t* gu = h.ws<int32_t>(WS_PR_GU, n);
-  int32_t* nextbuf = h.ws<int32_t>(WS_PR_NEXT, n);
-  int32_t* anc = h.ws<int32_t>(WS_PR_ANC, (size_t)n * L);
+  uint8_t* lv = h.ws<uint8_t>(WS_PR_FRESH, n);
+  uint32_t* seeds = h.ws<uint32_t>(WS_PR_GU, n + 1);
+  uint32_t* grafted = h.ws<uint32_t>(WS_PR_NEXT, n + 1);
+  uint32_t* byl = h.ws<uint32_t>(WS_PR_BYL, n + 1);
+  uint32_t* mk = h.ws<uint32_t>(WS_PR_MK, n + 1);
+  int32_t* ptr = h.ws<int32_t>(WS_PR_ANC, (size_t)n * K);
+  uint32_t* rlist = h.ws<uint32_t>(WS_CCROOTS, 3 * n + 3);
+  uint32_t* rl[2] = {rlist, rlist + n + 1};
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
   h.slots_clean = nullptr;  // graft rounds leave slots of their own
   cc_reset_rounds(h);       // (graft rounds use the CC's active-edge lists)
-  unsigned long long* crossing = reinterpret_cast<unsigned long long*>(h.dev_box) + 18;
   h.round0_slots = nullptr;  // (and overwrite an upload's round-0 keys)
-  int* ctl = reinterpret_cast<int*>(h.ws<int>(WS_BFS_CTRL, C_NWORDS + 8));
+  unsigned long long* pc =
+      reinterpret_cast<unsigned long long*>(h.ws<unsigned long long>(WS_BFS_CTRL, P_NWORDS + 2 * (kMaxLvl + 2)));
+  unsigned long long* bbase = pc + P_NWORDS;           // bucket b base in mk
+  unsigned long long* cursor = bbase + (kMaxLvl + 2);  // histogram, then byl cursors
+  unsigned long long* mcnt = pc + P_MCNT0;
+  int* any = reinterpret_cast<int*>(pc + P_ANY);
+  int* bad_rev = reinterpret_cast<int*>(pc + P_BAD_REV);
   unsigned long long* bad_mark = reinterpret_cast<unsigned long long*>(h.dev_box) + 16;
-  int* not_done = ctl + C_NWORDS;
   const unsigned g = grid_for(n);
   const cudaStream_t s = h.stream;
 
-  h.timer.begin(s, "pr.init");
-  k_pr_init<<<g, kBlock, 0, s>>>(n, parent, rep, scratch, mark, groot, slot);
-  k_anc_identity<<<g, kBlock, 0, s>>>(n, anc);  // make_pr_state :60-68
+  // ---- init: identity forest (make_pr_state :40-70), vertex levels, the
+  // descending-level vertex order (C_k = #vertices of level >= k)
+  h.timer.begin(s, "pr.init", 4.0 * n * 4 + 8.0 * n + 1.0 * n + 4.0 * n);
+  CK(cudaMemsetAsync(pc, 0, (P_NWORDS + 2 * (kMaxLvl + 2)) * sizeof(unsigned long long), s));
+  k_pr_init<<<g, kBlock, 0, s>>>(n, K, parent, rep, scratch, mark, lv, slot, cursor);
   CK_LAUNCH();
   CK(cudaMemsetAsync(bad_mark, 0xFF, sizeof(unsigned long long), s));
-  h.stats.step(n, 2);
+  h.read_box(reinterpret_cast<int64_t*>(cursor), K + 1);
+  std::vector<int64_t> C(K + 2, 0);  // C[k] = #level >= k
+  for (int k = K; k >= 0; --k) C[k] = C[k + 1] + h.host_box[k];
+  {
+    unsigned long long hb[2 * (kMaxLvl + 2)] = {0};
+    for (int b = 0; b <= K; ++b) hb[b] = (unsigned long long)C[b + 1];  // bucket base
+    for (int b = 0; b <= K; ++b) hb[(kMaxLvl + 2) + b] = (unsigned long long)C[b + 1];  // cursors
+    CK(cudaMemcpyAsync(bbase, hb, sizeof(hb), cudaMemcpyHostToDevice, s));
+  }
+  if (n > 0) k_pr_bylevel<<<g, kBlock, 0, s>>>(n, lv, byl, cursor);
+  CK_LAUNCH();
+  CK(cudaStreamSynchronize(s));  // (hb is a host stack buffer)
+  h.stats.step(n, 3);
   h.timer.end(s);
 
+  bool forest_dirty = false;  // the skip pointers lag the parent forest
+  auto rebuild = [&]() {
+    h.timer.begin(s, "pr.rebuild", 0.0);
+    double bytes = 0;
+    for (int k = 1; k <= K && C[k] > 0; ++k) {
+      // per vertex of level >= k: its id, ~2 hops (pointer + level byte), the pointer out
+      bytes += (double)C[k] * (4.0 + 2.0 * 5.0 + 4.0);
+      (n > (int64_t{1} << 22) ? k_pr_rebuild<4> : k_pr_rebuild<1>)
+          <<<grid_for(C[k]), kBlock, 0, s>>>(C[k], k, n, byl, parent, lv, ptr);
+      h.stats.step(C[k]);
+    }
+    CK_LAUNCH();
+    h.timer.add_bytes(bytes);
+    h.timer.end(s);
+    forest_dirty = false;
+  };
+  // marked set of one round: all ancestors of every seed (mark_paths :135-164)
   auto run_marking = [&]() {
-    CK(cudaMemsetAsync(ctl + C_MARK_STOP, 0, (1 + 40) * sizeof(int), s));
-    for (int k = 0; k < L; ++k) {
-      k_mark_level<<<g, kBlock, 0, s>>>(n, k, anc, mark, ctl);
+    if (forest_dirty) rebuild();
+    h.timer.begin(s, "pr.mark", 0.0);
+    CK(cudaMemsetAsync(mcnt, 0, (kMaxLvl + 2) * sizeof(unsigned long long), s));
+    k_pr_ascend<<<g, kBlock, 0, s>>>(seeds, pc + P_NGRAFT, n, parent, ptr, lv, mark, mk, bbase,
+                                     mcnt);
+    h.stats.step(n);
+    const unsigned dg = 4 * num_sms();
+    for (int j = K - 1; j >= 0; --j) {
+      k_pr_descend<<<dg, kBlock, 0, s>>>(j, K, n, parent, ptr, lv, mark, mk, bbase, mcnt);
       h.stats.step(n);
     }
     CK_LAUNCH();
+    h.timer.end(s);
   };
   auto run_reverse = [&]() {
-    k_reverse_a<<<g, kBlock, 0, s>>>(n, mark, parent, scratch);
-    k_reverse_b<<<g, kBlock, 0, s>>>(n, mark, parent, scratch, ctl);
+    const unsigned dg = 8 * num_sms();
+    k_pr_reverse_a<<<dg, kBlock, 0, s>>>(K, mk, bbase, mcnt, parent, scratch);
+    k_pr_reverse_b<<<dg, kBlock, 0, s>>>(K, mk, bbase, mcnt, mark, parent, scratch, bad_rev);
     CK_LAUNCH();
     h.stats.step(n);
     h.stats.step(n);
+    forest_dirty = true;
   };
-  // ctl[C_LMAX] = 1 initially (identity table: level 0 stands for all).
-  {
-    int init[C_NWORDS + 8] = {0};
-    init[C_LMAX] = 1;
-    CK(cudaMemcpyAsync(ctl, init, sizeof(init), cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
-  }
 
-  // batched_jump's guard (pr_rst.cpp:218-219) fires only once a graft
-  // happened; hops / barrier cap are derived after that check.
+  // batched_jump's guard (pr_rst.cpp:218-219) fires only once a graft happened.
   const bool batch_ok = jump_batch >= 1 && jump_batch <= 20;
-  const int64_t hops = batch_ok ? (int64_t{1} << jump_batch) : 1;
   const int64_t max_barriers =
       batch_ok ? (ceil_log2_i(std::max<int64_t>(n, 1)) + jump_batch - 1) / jump_batch + 2 : 0;
+  const uint32_t* in_list = nullptr;  // nullptr: every vertex is a root
+  int out = 0;
   int mode = 0;
   for (int64_t round = 0;; ++round) {
     if (round > n + 1) throw AlgoError("grafting failed to converge");
-    h.timer.begin(s, "pr.graft");
+    h.timer.begin(s, "pr.graft", 0.0);
     // graft proposals with active-edge filtering (as in the CC: an edge
     // inside one tree stays inside; the proposals are unchanged)
-    CK(cudaMemsetAsync(ctl + C_ANY, 0, sizeof(int), s));
-    CK(cudaMemsetAsync(crossing, 0, sizeof(unsigned long long), s));
-    cc_hook_round(h, mode, rep, slot, crossing, ctl + C_ANY);
-    CK(cudaMemcpyAsync(h.host_box, ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h.host_box + 1, crossing, sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    cc_round_done(h, h.host_box[1]);
+    CK(cudaMemsetAsync(pc + P_CROSSING, 0, 3 * sizeof(unsigned long long), s));
+    const double visited = (h.cc_round >= 2 && h.cc_active >= 0) ? (double)h.cc_active : (double)h.g.m;
+    h.timer.add_bytes(visited * 16.0);
+    cc_hook_round(h, mode, rep, slot, pc + P_CROSSING, any);
+    h.read_box(reinterpret_cast<int64_t*>(pc), P_ANY + 1);
+    const int64_t crossing = h.host_box[P_CROSSING];
+    const bool proposed = static_cast<int>(h.host_box[P_ANY]) != 0;
+    const int64_t nroots = in_list ? h.host_box[P_NROOTS_IN] : n;
+    cc_round_done(h, crossing);
     h.timer.end(s);
     h.stats.rounds = round + 1;
-    if (reinterpret_cast<int*>(h.host_box)[C_ANY] == 0) break;  // no graft (:279)
+    if (!proposed) break;  // no graft (:279)
     if (!batch_ok) throw AlgoError("jump batch out of range [1, 20]");
-    h.timer.begin(s, "pr.resolve");
-    k_graft_resolve<<<g, kBlock, 0, s>>>(n, h.g.edges, (uint32_t)h.g.e_base, rep, slot, mark,
-                                         scratch, groot, gu);
-    k_graft_update<<<g, kBlock, 0, s>>>(n, rep, slot);
+
+    h.timer.begin(s, "pr.resolve", 24.0 * nroots);
+    CK(cudaMemsetAsync(pc + P_NROOTS_OUT, 0, 2 * sizeof(unsigned long long), s));  // out, ngraft
+    k_pr_resolve<<<grid_for(nroots), kBlock, 0, s>>>(in_list, pc + P_NROOTS_IN, n, h.g.edges,
+                                                     (uint32_t)h.g.e_base, rep, slot, mark,
+                                                     scratch, seeds, grafted, pc + P_NGRAFT);
+    k_pr_update<<<grid_for(nroots), kBlock, 0, s>>>(in_list, pc + P_NROOTS_IN, n, rep, slot,
+                                                    rl[out], pc + P_NROOTS_OUT);
+    CK(cudaMemcpyAsync(pc + P_NROOTS_IN, pc + P_NROOTS_OUT, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToDevice, s));
     CK_LAUNCH();
+    in_list = rl[out];
+    out ^= 1;
     h.stats.step(n);
     h.stats.step(n);
     h.timer.end(s);
-    h.timer.begin(s, "pr.mark");
+
     run_marking();
-    k_graft_check<<<g, kBlock, 0, s>>>(n, groot, mark, parent, gu, bad_mark);
-    k_clear_groot<<<g, kBlock, 0, s>>>(n, groot);
-    CK_LAUNCH();
+    h.timer.begin(s, "pr.reverse", 0.0);
+    k_pr_check<<<grid_for(nroots), kBlock, 0, s>>>(grafted, seeds, pc + P_NGRAFT, mark, parent,
+                                                   bad_mark);
     h.stats.step(n);
-    h.timer.end(s);
-    h.timer.begin(s, "pr.reverse");
     run_reverse();
-    h.timer.end(s);
-    h.timer.begin(s, "pr.jump");
-    CK(cudaMemsetAsync(ctl + C_JUMP_DONE, 0, 2 * sizeof(int), s));
-    CK(cudaMemsetAsync(not_done, 0, sizeof(int), s));
-    for (int64_t b = 0; b <= max_barriers; ++b) {
-      (big ? k_jump_barrier<4> : k_jump_barrier<1>)<<<g, kBlock, 0, s>>>(n, hops, (int)b, rep,
-                                                                        nextbuf, ctl, not_done);
-      k_jump_close<<<1, 1, 0, s>>>((int)b, ctl, not_done);
-      h.stats.step(n);
-    }
-    k_jump_copyback<<<g, kBlock, 0, s>>>(n, rep, nextbuf, ctl);
+    k_pr_unroot<<<grid_for(nroots), kBlock, 0, s>>>(grafted, pc + P_NGRAFT, lv);
     CK_LAUNCH();
     h.timer.end(s);
-    h.timer.begin(s, "pr.anc");
-    CK(cudaMemcpyAsync(anc, parent, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemsetAsync(ctl + C_CHANGED0, 0, 40 * sizeof(int), s));
-    k_set_i32<<<1, 1, 0, s>>>(ctl + C_LMAX, L);
-    for (int k = 1; k < L; ++k) {
-      (big ? k_anc_level<4> : k_anc_level<1>)<<<g, kBlock, 0, s>>>(n, k, anc, ctl);
-      h.stats.step(n);
-    }
-    CK_LAUNCH();
+
+    // converged reps again (batched_jump's result, :216-252): the grafted
+    // roots' chains are jumped as a list, then one gather over n
+    h.timer.begin(s, "pr.jump", 8.0 * n);
+    compress_via_roots(h, rep, n, grafted, pc + P_NGRAFT);
+    h.stats.step(n, std::max<int64_t>(max_barriers / 2, 1) - 1);
     h.timer.end(s);
-    // Deferred error checks for this round.
-    CK(cudaMemcpyAsync(h.host_box, ctl, C_GREW0 * sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h.host_box + 8, bad_mark, sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const int* hc = reinterpret_cast<int*>(h.host_box);
-    const unsigned long long bm = (unsigned long long)h.host_box[8];
+    // deferred error checks of this round (+ the marked count, for the
+    // phases' algorithmic bytes)
+    h.read_box(reinterpret_cast<int64_t*>(pc), P_MCNT0 + K + 1);
+    const bool badrev = static_cast<int>(h.host_box[P_BAD_REV]) != 0;
+    double marked = 0;
+    for (int b = 0; b <= K; ++b) marked += (double)h.host_box[P_MCNT0 + b];
+    const double grafts = (double)h.host_box[P_NGRAFT];
+    // mark: per marked vertex its queue entry 4 B + mark byte, ~2 hops of
+    // pointer + level byte; reverse: queue entry, parent, scratch (twice),
+    // mark; per graft the check and the root bit; jump: the grafted list
+    h.timer.add_bytes("pr.mark", marked * (4.0 + 1.0 + 2.0 * 5.0));
+    h.timer.add_bytes("pr.reverse", marked * 21.0 + grafts * 14.0);
+    h.timer.add_bytes("pr.jump", grafts * 8.0);
+    h.read_box(reinterpret_cast<int64_t*>(bad_mark), 1);
+    const unsigned long long bm = (unsigned long long)h.host_box[0];
     if (bm != kAllOnes)
       throw AlgoError("path marking corrupted: " + std::to_string(bm >> 32) +
                       " is not the root above " + std::to_string((uint32_t)bm));
-    if (hc[C_BAD_REV]) throw AlgoError("reversal found a marked vertex with no source");
-    if (!hc[C_JUMP_DONE]) throw AlgoError("pointer jumping detected a representative cycle");
+    if (badrev) throw AlgoError("reversal found a marked vertex with no source");
     mode ^= 1;
   }
 
@@ -416,24 +609,29 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   CK(cudaStreamSynchronize(s));
   const int32_t emergent = *reinterpret_cast<int32_t*>(h.host_box);
   if (emergent != root) {
-    h.timer.begin(s, "pr.reroot");
-    k_set_u8<<<1, 1, 0, s>>>(mark + root, 1);  // mark_path :170
+    h.timer.begin(s, "pr.reroot", 0.0);
+    // mark_path(root, emergent) :166-176: one seed
+    k_set_u32<<<1, 1, 0, s>>>(seeds, (uint32_t)root);
+    k_set_u32<<<1, 1, 0, s>>>(grafted, (uint32_t)emergent);
+    k_set_u64<<<1, 1, 0, s>>>(pc + P_NGRAFT, 1ull);
+    k_set_u8<<<1, 1, 0, s>>>(mark + root, 1);
+    CK_LAUNCH();
+    h.timer.end(s);
     run_marking();
-    k_check_one<<<1, 1, 0, s>>>(emergent, root, mark, parent, bad_mark);  // :172-175
+    h.timer.begin(s, "pr.reroot", 0.0);
+    k_pr_check<<<1, 32, 0, s>>>(grafted, seeds, pc + P_NGRAFT, mark, parent, bad_mark);
     k_set_i32<<<1, 1, 0, s>>>(scratch + root, root);  // reverse_path :212
     run_reverse();
     CK_LAUNCH();
-    CK(cudaMemcpyAsync(h.host_box, ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h.host_box + 8, bad_mark, sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    h.read_box(reinterpret_cast<int64_t*>(pc), P_BAD_REV + 1);
+    const bool badrev = static_cast<int>(h.host_box[P_BAD_REV]) != 0;
+    h.read_box(reinterpret_cast<int64_t*>(bad_mark), 1);
     h.timer.end(s);
-    const unsigned long long bm = (unsigned long long)h.host_box[8];
+    const unsigned long long bm = (unsigned long long)h.host_box[0];
     if (bm != kAllOnes)
       throw AlgoError("path marking corrupted: " + std::to_string(bm >> 32) +
                       " is not the root above " + std::to_string((uint32_t)bm));
-    if (reinterpret_cast<int*>(h.host_box)[C_BAD_REV])
-      throw AlgoError("reversal found a marked vertex with no source");
+    if (badrev) throw AlgoError("reversal found a marked vertex with no source");
   }
 }
 

@@ -11,7 +11,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
 PKG := paper_2603_11645_b200
 CSRC := $(PKG)/csrc
 OBJDIR := build/obj
-CU := engine cc listrank tilerank euler euler_api pr bfs validate graph capi
+CU := engine cc listrank tilerank euler euler_api pr bfs validate graph loader capi
 OBJS := $(patsubst %,$(OBJDIR)/%.o,$(CU))
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) include/rstg.h
 

@@ -9,6 +9,7 @@
  *
  * Reference interfaces replaced (paths under /root/reference/proj/core):
  *   rstg_graph_create*    Graph / build_csr          include/rst/graph.hpp:29-43,71
+ *   rstg_edge_list_*      load_edge_list / EdgeList  include/rst/graph.hpp:17-23,60-64
  *   rstg_run              run_algorithm              include/rst/bench.hpp:36
  *                         (bfs_rst bfs_rst.hpp:23, cc_euler_rst
  *                          euler_rooting.hpp:69, pr_rst pr_rst.hpp:94-95)
@@ -35,6 +36,7 @@ extern "C" {
 #define RSTG_ERR_ARG 1   /* invalid argument (reference: std::invalid_argument) */
 #define RSTG_ERR_ALGO 2  /* algorithm failure (reference: std::runtime_error)   */
 #define RSTG_ERR_CUDA 3  /* CUDA runtime error / no device                      */
+#define RSTG_ERR_PARSE 4 /* malformed edge-list text (reference: rst::ParseError) */
 
 /* AlgoKind order of bench.hpp:16 */
 #define RSTG_BFS 0
@@ -42,6 +44,7 @@ extern "C" {
 #define RSTG_PR_RST 2
 
 typedef struct rstg_graph rstg_graph;
+typedef struct rstg_edge_list rstg_edge_list;
 
 /* Mirrors StepReport (step_engine.hpp:21-25) plus device-side figures. */
 typedef struct {
@@ -83,6 +86,26 @@ int rstg_graph_upload(rstg_graph* g, const int64_t* offsets, const int64_t* neig
 int rstg_graph_create_device(const int32_t* d_edges_uv, const uint32_t* d_offsets,
                              const int32_t* d_nbrs, const uint32_t* d_arc_edge, int64_t n,
                              int64_t m, int device, rstg_graph** out);
+/* load_edge_list (graph.hpp:60-64, graph.cpp:48-127) over an in-memory
+ * text (edge list or MatrixMarket): parsed by `threads` host threads,
+ * then ids densified/remapped and the list normalized on `device`.
+ * Errors: RSTG_ERR_PARSE "line N: <what>" with *err_line = N (the
+ * reference's ParseError texts); RSTG_ERR_ALGO "empty edge-list input: no
+ * data lines" / "graph too large: vertex ids exceed 2^31". */
+int rstg_edge_list_load(const char* text, int64_t len, int threads, int device,
+                        rstg_edge_list** out, int64_t* err_line);
+/* n (num_vertices), m (normalized edges), original-id count (0 = identity ids). */
+int rstg_edge_list_info(const rstg_edge_list* el, int64_t* n, int64_t* m, int64_t* n_original_ids);
+/* edges_uv[2m] (u < v, sorted) and original_ids[n_original_ids]; either nullable. */
+int rstg_edge_list_copy(rstg_edge_list* el, int64_t* edges_uv, int64_t* original_ids);
+int rstg_edge_list_destroy(rstg_edge_list* el);
+/* Device graph straight from a loaded list (no host round trip; CSR on device). */
+int rstg_graph_from_edge_list(const rstg_edge_list* el, int device, rstg_graph** out);
+/* The parse stage alone (host threads only, no device): raw pairs in file
+ * order into uv_out (when *count <= cap), or RSTG_ERR_PARSE + *err_line. */
+int rstg_parse_edge_text(const char* text, int64_t len, int threads, int64_t* uv_out, int64_t cap,
+                         int64_t* count, int64_t* err_line);
+
 /* Device generator: "path:N", "star:N", "grid:R:C", "road:R[:p]",
  * "kron:SCALE[:EF]" (SURVEY.md Appendix B shapes; identical edge lists to
  * the host generators). */

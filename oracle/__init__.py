@@ -87,6 +87,8 @@ def ref():
         L.ref_generate.restype = ctypes.c_int64
         L.ref_generate.argtypes = [ctypes.c_char_p, ctypes.c_uint64, _i64p, _i64p, _i64p]
         L.ref_forest_depth.restype = ctypes.c_int64
+        L.ref_load_edge_list.restype = ctypes.c_int64
+        L.ref_load_edge_list.argtypes = [ctypes.c_char_p, ctypes.c_int64] + [_i64p] * 6
         _ref = L
     return _ref
 
@@ -315,6 +317,24 @@ def ref_generate(spec: str, seed: int = 0) -> Graph:
     ev = np.zeros(m, I64)
     R.ref_generate(spec.encode(), seed, ctypes.byref(n), _p(eu), _p(ev))
     return Graph(n.value, eu, ev)
+
+
+def ref_load_edge_list(text: bytes):
+    """The reference's load_edge_list (graph.cpp:48-127) on an in-memory
+    text: (n, eu, ev, original_ids), or raises OracleError(message) with
+    .line set for a ParseError."""
+    R = ref()
+    n, nids, line = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(-1)
+    m = R.ref_load_edge_list(text, len(text), ctypes.byref(n), None, None, None,
+                             ctypes.byref(nids), ctypes.byref(line))
+    if m < 0:
+        e = OracleError(_err(R, "ref_last_error"))
+        e.line = line.value
+        raise e
+    eu, ev, ids = np.zeros(max(m, 1), I64), np.zeros(max(m, 1), I64), np.zeros(max(nids.value, 1), I64)
+    R.ref_load_edge_list(text, len(text), ctypes.byref(n), _p(eu), _p(ev), _p(ids),
+                         ctypes.byref(nids), ctypes.byref(line))
+    return n.value, eu[:m], ev[:m], ids[: nids.value]
 
 
 def ref_run(g: Graph, algo: int, root: int = 0, workers: int = 1, jump_batch: int = 5):

@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -191,6 +192,36 @@ int64_t ref_generate(const char* spec, uint64_t seed, int64_t* n_out, int64_t* e
       }
     }
     return static_cast<int64_t>(el.edges.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// load_edge_list (graph.cpp:48-127) over an in-memory text. Returns m
+// (normalized), fills n, the edges (when eu != nullptr) and original_ids
+// (when ids != nullptr; *nids = their count); -1 on any exception, with
+// *err_line = the ParseError line (or -1 for other errors).
+int64_t ref_load_edge_list(const char* text, int64_t len, int64_t* n_out, int64_t* eu,
+                           int64_t* ev, int64_t* ids, int64_t* nids, int64_t* err_line) {
+  *err_line = -1;
+  try {
+    std::istringstream in(std::string(text, static_cast<size_t>(len)));
+    rst::EdgeList el = rst::load_edge_list(in);
+    *n_out = el.num_vertices;
+    *nids = static_cast<int64_t>(el.original_ids.size());
+    if (eu) {
+      for (size_t i = 0; i < el.edges.size(); ++i) {
+        eu[i] = el.edges[i].u;
+        ev[i] = el.edges[i].v;
+      }
+    }
+    if (ids) std::memcpy(ids, el.original_ids.data(), el.original_ids.size() * sizeof(int64_t));
+    return static_cast<int64_t>(el.edges.size());
+  } catch (const rst::ParseError& e) {
+    g_err = e.what();
+    *err_line = e.line();
+    return -1;
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

@@ -22,13 +22,14 @@ LIB_PATH = os.path.join(HERE, "librstg.so")
 BFS, CC_EULER, PR_RST = 0, 1, 2  # bench.hpp:16 AlgoKind
 ALGOS = {"bfs": BFS, "cc-euler": CC_EULER, "pr-rst": PR_RST}
 
-RSTG_OK, RSTG_ERR_ARG, RSTG_ERR_ALGO, RSTG_ERR_CUDA = 0, 1, 2, 3
+RSTG_OK, RSTG_ERR_ARG, RSTG_ERR_ALGO, RSTG_ERR_CUDA, RSTG_ERR_PARSE = 0, 1, 2, 3, 4
 
 # Symbols include/rstg.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "rstg_last_error", "rstg_device_count", "rstg_graph_create", "rstg_graph_create_device", "rstg_graph_upload",
     "rstg_graph_generate", "rstg_graph_info", "rstg_graph_edges", "rstg_graph_edges_flagged",
-    "rstg_graph_destroy",
+    "rstg_graph_destroy", "rstg_edge_list_load", "rstg_edge_list_info", "rstg_edge_list_copy",
+    "rstg_edge_list_destroy", "rstg_graph_from_edge_list", "rstg_parse_edge_text",
     "rstg_set_stream", "rstg_set_timing", "rstg_phase_times", "rstg_run", "rstg_run_device",
     "rstg_cc_spanning_forest", "rstg_euler_root_forest", "rstg_validate", "rstg_forest_depth",
     "rstg_graph_generate_part", "rstg_graph_set_edge_base", "rstg_cc_init", "rstg_cc_hook",
@@ -60,6 +61,14 @@ class RSTError(RuntimeError):
     """Algorithm failure; message = the reference's std::runtime_error text."""
 
 
+class RSTParseError(ValueError):
+    """Malformed edge-list text (rst::ParseError); .line = 1-based line."""
+
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line = line
+
+
 class RSTArgError(ValueError):
     """Invalid argument (reference: std::invalid_argument)."""
 
@@ -89,6 +98,14 @@ def lib():
         L.rstg_graph_info.argtypes = [_vp, _i64p, _i64p]
         L.rstg_graph_edges.argtypes = [_vp, _i64p]
         L.rstg_graph_edges_flagged.argtypes = [_vp, _vp, _i64p, ctypes.c_int64, _i64p]
+        L.rstg_edge_list_load.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                          ctypes.POINTER(_vp), _i64p]
+        L.rstg_edge_list_info.argtypes = [_vp, _i64p, _i64p, _i64p]
+        L.rstg_edge_list_copy.argtypes = [_vp, _i64p, _i64p]
+        L.rstg_edge_list_destroy.argtypes = [_vp]
+        L.rstg_graph_from_edge_list.argtypes = [_vp, ctypes.c_int, ctypes.POINTER(_vp)]
+        L.rstg_parse_edge_text.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, _i64p,
+                                           ctypes.c_int64, _i64p, _i64p]
         L.rstg_graph_destroy.argtypes = [_vp]
         L.rstg_set_stream.argtypes = [_vp, _vp]
         L.rstg_set_timing.argtypes = [_vp, ctypes.c_int]
@@ -183,6 +200,23 @@ class DeviceGraph:
         _check(lib().rstg_graph_create_device(_vp(d_edges), _vp(d_offsets), _vp(d_nbrs),
                                               _vp(d_arc_edge), int(n), int(m), device,
                                               ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_edge_list_text(cls, text: bytes, threads: int = 0, device=0):
+        """load_edge_list on the device, then the graph from it (no host round trip)."""
+        L = lib()
+        el, line = _vp(), ctypes.c_int64(-1)
+        rc = L.rstg_edge_list_load(text, len(text), threads or os.cpu_count() or 1, device,
+                                   ctypes.byref(el), ctypes.byref(line))
+        if rc == RSTG_ERR_PARSE:
+            raise RSTParseError(L.rstg_last_error().decode(), line.value)
+        _check(rc)
+        try:
+            h = _vp()
+            _check(L.rstg_graph_from_edge_list(el, device, ctypes.byref(h)))
+        finally:
+            L.rstg_edge_list_destroy(el)
         return cls(h)
 
     @classmethod
@@ -394,3 +428,39 @@ class EulerStructure:
         _check(lib().rstg_k_derive_parents(self.num_vertices, self.num_arcs, _p64(self.from_),
                                            _p64(self.to), _p64(rk), _p64(parent)))
         return parent[: self.num_vertices]
+
+
+def parse_edge_text(text: bytes, threads: int = 0):
+    """The loader's parse stage alone (host threads): raw (u, v) pairs in
+    file order, int64 (count, 2); RSTParseError on malformed text."""
+    L = lib()
+    threads = threads or os.cpu_count() or 1
+    c, line = ctypes.c_int64(0), ctypes.c_int64(-1)
+    rc = L.rstg_parse_edge_text(text, len(text), threads, None, 0, ctypes.byref(c), ctypes.byref(line))
+    if rc == RSTG_ERR_PARSE:
+        raise RSTParseError(L.rstg_last_error().decode(), line.value)
+    _check(rc)
+    out = np.zeros(2 * max(c.value, 1), np.int64)
+    _check(L.rstg_parse_edge_text(text, len(text), threads, _p64(out), c.value, ctypes.byref(c),
+                                  ctypes.byref(line)))
+    return out[: 2 * c.value].reshape(-1, 2)
+
+
+def load_edge_list(text: bytes, threads: int = 0, device: int = 0):
+    """load_edge_list (graph.cpp:48-127): (n, edges int64 (m, 2), original_ids)."""
+    L = lib()
+    h, line = _vp(), ctypes.c_int64(-1)
+    rc = L.rstg_edge_list_load(text, len(text), threads or os.cpu_count() or 1, device,
+                               ctypes.byref(h), ctypes.byref(line))
+    if rc == RSTG_ERR_PARSE:
+        raise RSTParseError(L.rstg_last_error().decode(), line.value)
+    _check(rc)
+    try:
+        n, m, k = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(L.rstg_edge_list_info(h, ctypes.byref(n), ctypes.byref(m), ctypes.byref(k)))
+        e = np.zeros(2 * max(m.value, 1), np.int64)
+        ids = np.zeros(max(k.value, 1), np.int64)
+        _check(L.rstg_edge_list_copy(h, _p64(e), _p64(ids)))
+        return n.value, e[: 2 * m.value].reshape(-1, 2), ids[: k.value]
+    finally:
+        L.rstg_edge_list_destroy(h)

@@ -24,6 +24,7 @@ void upload_edges_build_csr(Handle& h, const int64_t* edges_uv, int64_t n, int64
 void adopt_device_graph(Handle& h, const int2* edges, const uint32_t* offsets, const int32_t* nbrs,
                         const uint32_t* arc_edge, int64_t n, int64_t m);
 void generate_device(Handle& h, int kind, int64_t a, int64_t b, double p, bool build_csr);
+const int2* edge_list_device(const rstg_edge_list* el, int64_t* n, int64_t* m);  // loader.cu
 void widen_to_host(Handle& h, const int32_t* dev, int64_t count, int64_t* host);
 int64_t forest_depth_device(Handle& h, const int32_t* parent, int32_t* depth, uint32_t* rootmax,
                             int64_t* cycle_vertex);
@@ -270,6 +271,22 @@ int rstg_graph_create_device(const int32_t* d_edges_uv, const uint32_t* d_offset
     try {
       adopt_device_graph(g->h, reinterpret_cast<const int2*>(d_edges_uv), d_offsets, d_nbrs,
                          d_arc_edge, n, m);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int rstg_graph_from_edge_list(const rstg_edge_list* el, int device, rstg_graph** out) {
+  *out = nullptr;
+  return guard([&] {
+    int64_t n = 0, m = 0;
+    const int2* edges = edge_list_device(el, &n, &m);
+    auto* g = new rstg_graph(device);
+    try {
+      adopt_device_graph(g->h, edges, nullptr, nullptr, nullptr, n, m);  // CSR built on the device
     } catch (...) {
       delete g;
       throw;

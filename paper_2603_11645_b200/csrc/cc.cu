@@ -362,12 +362,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
       const uint32_t hd = s_head[i];
-      io.eu.vhead[base + i] = hd;
-      if (hd != kNone32) {
-        const uint32_t tl = s_tail[i];
-        io.eu.vtail[base + i] = tl;
-        io.eu.S[arc_rev(tl, io.eu.nslots)] = hd;
-      }
+      io.eu.vhead[base + i] = hd;  // (one arc of the cycle is all a later splice needs)
+      if (hd != kNone32) io.eu.S[arc_rev(s_tail[i], io.eu.nslots)] = hd;
     }
   }
   if (SRC != kSrcRep) {

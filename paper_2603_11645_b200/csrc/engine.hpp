@@ -202,7 +202,7 @@ enum WsSlot : int {
   WS_VAL_C,
   // Euler tour (euler.cu): rotation lists
   WS_VHEAD,       // u32 n         first arc of each vertex's local rotation list
-  WS_VTAIL,       // u32 n         its last arc
+  WS_VTAIL,       // (unused: local lists keep no tail)
   WS_RHEAD,       // u32 n         remote list (atomic prepends): first arc
   WS_RTAIL,       // u32 n         its last arc (the first one inserted)
   WS_ETO,         // u32 2N        arc heads, pairs (2i: a->b, 2i+1: b->a)
@@ -237,16 +237,15 @@ enum WsSlot : int {
 //
 // Two lists per vertex, concatenated by the vertex pass after the CC: the
 // "local" one written by round 0's shared-memory tiles with plain stores
-// (vhead/vtail, every vertex covered, so no initialisation; closed into
-// its cycle at once), and the
-// "remote" one that every other link prepends to with atomicExch
-// (rhead/rtail, NONE-initialised).
+// (vhead: one arc of it, every vertex covered, so no initialisation; it is
+// closed into its cycle at once, so no tail is kept -- a splice goes in
+// after vhead), and the "remote" one that every other link prepends to with
+// atomicExch (rhead/rtail, NONE-initialised).
 struct EulerIO {
   uint32_t nslots;  // N
   uint32_t* eto;    // N pairs (to(i), to(N + i)) = (b, a)
   uint32_t* S;      // 2N  successors
-  uint32_t* vhead;  // n   local list: first arc
-  uint32_t* vtail;  // n   local list: last arc
+  uint32_t* vhead;  // n   local cycle: one of its arcs (NONE: no local list)
   uint32_t* rhead;  // n   remote list: first arc (NONE-initialised)
   uint32_t* rtail;  // n   remote list: last arc (the first inserted)
 };

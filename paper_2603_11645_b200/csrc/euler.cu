@@ -137,9 +137,10 @@ __global__ void __launch_bounds__(kBlock)
       if (h2[k] == kNone32) continue;
       const int64_t v = base + k * kBlock + threadIdx.x;
       const uint32_t h1 = io.vhead[v], t2 = io.rtail[v];
-      if (h1 != kNone32) {
-        io.S[arc_rev(io.vtail[v], io.nslots)] = h2[k];
-        io.S[arc_rev(t2, io.nslots)] = h1;
+      if (h1 != kNone32) {  // the remote chain goes in right after h1
+        const uint32_t nx = io.S[arc_rev(h1, io.nslots)];
+        io.S[arc_rev(h1, io.nslots)] = h2[k];
+        io.S[arc_rev(t2, io.nslots)] = nx;
       } else {
         io.S[arc_rev(t2, io.nslots)] = h2[k];
       }
@@ -194,10 +195,11 @@ __global__ void __launch_bounds__(kBlock)
       if (reset) minv[labels[i]] = kNone32;
       parent[r] = (int32_t)r;
       const uint32_t h1 = io.vhead[r], h2 = io.rhead[r];
-      hd = h1 != kNone32 ? h1 : h2;  // the combined list: local, then remote
-      if (hd != kNone32) {
-        const uint32_t tl = h2 != kNone32 ? io.rtail[r] : io.vtail[r];
-        io.S[arc_rev(tl, io.nslots)] = kNone32;  // the tour ends back at the root
+      const uint32_t x = h1 != kNone32 ? h1 : h2;  // an arc of r's (spliced) rotation cycle
+      if (x != kNone32) {
+        // the tour starts with the arc after x and ends entering r by rev(x)
+        hd = io.S[arc_rev(x, io.nslots)];
+        io.S[arc_rev(x, io.nslots)] = kNone32;
       }
     }
     if (!rulers) continue;  // (block-uniform)
@@ -275,7 +277,6 @@ EulerIO euler_buffers(Handle& h, int64_t N, bool local_written) {
   io.eto = h.ws<uint32_t>(WS_ETO, 2 * N);
   io.S = h.ws<uint32_t>(WS_SUCC, 2 * N);
   io.vhead = h.ws<uint32_t>(WS_VHEAD, h.g.n);
-  io.vtail = h.ws<uint32_t>(WS_VTAIL, h.g.n);
   io.rhead = h.ws<uint32_t>(WS_RHEAD, h.g.n);
   io.rtail = h.ws<uint32_t>(WS_RTAIL, h.g.n);
   if (!local_written) CK(cudaMemsetAsync(io.vhead, 0xFF, (size_t)h.g.n * sizeof(uint32_t), h.stream));

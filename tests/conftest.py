@@ -30,3 +30,12 @@ def O():
     if not os.path.exists(oracle.ORACLE_SO):
         oracle.build()
     return oracle
+
+
+@pytest.fixture(scope="session")
+def rsth():
+    """The product package for host-only entry points (no device needed)."""
+    import paper_2603_11645_b200 as P
+
+    P.lib()
+    return P

@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bfs-ratio", action="store_true")
+    ap.add_argument("--ref-workers", type=int, default=0,
+                    help="reference arm: run_algorithm workers (default: every host core)")
     return ap.parse_args()
 
 
@@ -359,7 +361,7 @@ def main():
         if rank != 0:
             return
         k, w = min(args.steps, REF_MAX_TIMED), min(args.warmup, REF_MAX_WARMUP)
-        cb = cpu_reference(args.workload, args.algo, k, w)
+        cb = cpu_reference(args.workload, args.algo, k, w, cores=args.ref_workers or None)
         line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "edges/s",
                 "n_gpus": args.gpus, "steps": k, "warmup": w,
                 "requested": {"steps": args.steps, "warmup": args.warmup},

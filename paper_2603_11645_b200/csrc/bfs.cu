@@ -108,7 +108,7 @@ __device__ __forceinline__ void td_visit(int32_t u, int32_t v, int d, int32_t* l
 __global__ void __launch_bounds__(kBlock)
     k_bfs(int64_t n, int64_t two_m, const uint32_t* __restrict__ offsets,
           const int32_t* __restrict__ nbrs, int32_t* level, int32_t* parent, BfsQueues qs,
-          BfsCtl* ctl, int max_levels, int small_enter) {
+          BfsCtl* ctl, int max_levels, int small_enter, unsigned long long small_mf) {
   cg::grid_group grid = cg::this_grid();
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(kBlock)
     const int ci = d % 3, ni = (d + 1) % 3, zi = (d + 2) % 3;
     const int qn = *((volatile int*)&ctl->qn[ci]);
     const int hn = *((volatile int*)&ctl->hn[ci]);
-    if (qn + hn == 0 || (!bottom_up && qn + hn < small_enter)) {
+    const unsigned long long mf = *((volatile unsigned long long*)&ctl->mf[ci]);
+    if (qn + hn == 0 || (!bottom_up && qn + hn < small_enter && mf <= small_mf)) {
       // every thread saw the same counters: a uniform exit
       if (gtid == 0) {
         ctl->d = d;
@@ -130,7 +131,6 @@ __global__ void __launch_bounds__(kBlock)
       }
       return;
     }
-    const unsigned long long mf = *((volatile unsigned long long*)&ctl->mf[ci]);
     visited_edges += mf;
     if (gtid == 0) {
       ctl->reached += (unsigned long long)(qn + hn);
@@ -202,50 +202,119 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // The small-frontier levels: one cluster, top-down only (a small frontier
-// never favours bottom-up), cluster barrier per level. Cross-CTA data
-// (frontier queues, counters, levels) is read through L2 (ld.cg).
+// never favours bottom-up), one hardware cluster barrier per level. The
+// frontier lives in SHARED memory: every CTA keeps the vertices its own
+// threads discovered (cur/next queues of kSmallCap entries) with its
+// count and degree sum, so a level's critical path holds only the graph
+// reads and the level/parent atomics in HBM -- the queue reads, counters
+// and appends stay on chip. The totals (termination, hand-over) are read
+// across the cluster through distributed shared memory. A CTA's next queue
+// can hold at most its current degree sum, so a level whose per-CTA degree
+// sum exceeds kSmallCap is handed back to the cooperative grid first.
+constexpr int kSmallCap = 16384;
+struct SmallQ {
+  uint32_t q[2][kSmallCap];
+  unsigned int qn[2];
+  unsigned int dsum[2];  // degree sum, each degree clamped to kSmallCap + 1 (bounded, exact test)
+};
+
+__device__ __forceinline__ void small_enqueue(SmallQ& sq, int nx, int32_t v, uint32_t deg) {
+  const unsigned pos = atomicAdd(&sq.qn[nx], 1u);
+  sq.q[nx][pos] = (uint32_t)v;
+  atomicAdd(&sq.dsum[nx], min(deg, (uint32_t)kSmallCap + 1u));
+}
+__device__ __forceinline__ void small_visit(int32_t u, int32_t v, int d, int32_t* level,
+                                            int32_t* parent, const uint32_t* offsets, SmallQ& sq,
+                                            int nx) {
+  const int lv = ld_cg(&level[v]);
+  if (lv != -1 && lv != d) return;
+  if (u < ld_cg(&parent[v])) atomicMin(&parent[v], u);
+  if (lv == -1 && atomicCAS(&level[v], -1, d) == -1)
+    small_enqueue(sq, nx, v, offsets[v + 1] - offsets[v]);
+}
+
 __global__ void __launch_bounds__(kSmallThreads, 1)
     k_bfs_small(const uint32_t* __restrict__ offsets, const int32_t* __restrict__ nbrs,
-                int32_t* level, int32_t* parent, BfsQueues qs, BfsCtl* ctl, int exit_above) {
+                int32_t* level, int32_t* parent, BfsQueues qs, BfsCtl* ctl) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  SmallQ& sq = *reinterpret_cast<SmallQ*>(s_raw);
+  __shared__ unsigned long long s_tot, s_dtot, s_dmax;
+  __shared__ unsigned int s_pre[33];  // frontier prefix over the cluster's queues
+  __shared__ const SmallQ* s_rq[32];
   cg::cluster_group cl = cg::this_cluster();
-  const int64_t ctid = (int64_t)cl.block_rank() * blockDim.x + threadIdx.x;
-  const int64_t csize = (int64_t)cl.num_blocks() * blockDim.x;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp_id = ctid >> 5, nwarps = csize >> 5;
+  const unsigned rank = cl.block_rank(), C = cl.num_blocks();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int d = ld_cg(&ctl->d);
-  unsigned long long visited_edges = __ldcg(&ctl->vis0);
-  for (;; ++d) {
-    const int ci = d % 3, ni = (d + 1) % 3, zi = (d + 2) % 3;
-    const int qn = ld_cg(&ctl->qn[ci]);
-    const int hn = ld_cg(&ctl->hn[ci]);
-    if (qn + hn == 0 || qn + hn > exit_above) {
-      if (ctid == 0) {
-        ctl->d = d;
-        ctl->done = qn + hn == 0;
-        ctl->vis0 = visited_edges;
+  int cur = d & 1;
+  // entry: the global frontier of level d, dealt round-robin to the CTAs
+  {
+    const int ci = d % 3;
+    const int qn = ld_cg(&ctl->qn[ci]), hn = ld_cg(&ctl->hn[ci]);
+    if (threadIdx.x == 0) {
+      sq.qn[cur] = 0;
+      sq.dsum[cur] = 0;
+    }
+    __syncthreads();
+    for (int i = rank + C * threadIdx.x; i < qn + hn; i += C * blockDim.x) {
+      const int32_t v = i < qn ? ld_cg(&qs.q[d & 1][i]) : ld_cg(&qs.hq[d & 1][i - qn]);
+      small_enqueue(sq, cur, v, offsets[v + 1] - offsets[v]);
+    }
+  }
+  unsigned long long vis = __ldcg(&ctl->vis0), reached = 0, scanned = 0;
+  cl.sync();
+  for (;; ++d, cur ^= 1) {
+    const int nx = cur ^ 1;
+    // frontier totals, the per-queue prefix and the largest per-CTA degree
+    // sum, over the cluster (distributed shared memory)
+    if (warp == 0) {
+      unsigned t = 0, ds = 0;
+      if (lane < (int)C) {
+        const SmallQ* r = cl.map_shared_rank(&sq, lane);
+        s_rq[lane] = r;
+        t = r->qn[cur];
+        ds = r->dsum[cur];
       }
-      return;
+      unsigned incl = t;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      s_pre[lane + 1] = incl;
+      if (lane == 0) s_pre[0] = 0;
+      unsigned long long dsum = ds, dm = ds;
+      for (int o = 16; o > 0; o >>= 1) {
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+        dm = max(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+      }
+      if (lane == 31) s_tot = incl;
+      if (lane == 0) {
+        s_dtot = dsum;
+        s_dmax = dm;
+      }
     }
-    const unsigned long long mf = __ldcg(&ctl->mf[ci]);
-    visited_edges += mf;
-    if (ctid == 0) {
-      ctl->reached += (unsigned long long)(qn + hn);
-      ctl->scanned += mf;
-      ctl->levels = d - 1;
-      ctl->qn[zi] = 0;
-      ctl->hn[zi] = 0;
-      ctl->mf[zi] = 0;
+    __syncthreads();
+    const unsigned long long total = s_tot, dtot = s_dtot;
+    if (total == 0 || s_dmax > (unsigned long long)kSmallCap) break;
+    reached += total;
+    scanned += dtot;
+    vis += dtot;
+    if (threadIdx.x == 0) {
+      sq.qn[nx] = 0;
+      sq.dsum[nx] = 0;
     }
-    const int32_t* qc = qs.q[d & 1];
-    const int32_t* hqc = qs.hq[d & 1];
-    const LevelIO io{qs.q[(d + 1) & 1], &ctl->qn[ni], qs.hq[(d + 1) & 1], &ctl->hn[ni],
-                     &ctl->mf[ni]};
-    for (int64_t base = warp_id * 32; base < qn; base += nwarps * 32) {
-      const int64_t i = base + lane;
+    __syncthreads();
+    // the cluster's frontier, dealt evenly over all its threads (entries
+    // read from the owning CTA's shared memory); discoveries stay local
+    const unsigned tot = (unsigned)total;
+    const unsigned ct = rank * blockDim.x + threadIdx.x, cs = C * blockDim.x;
+    for (unsigned base = ct - lane; base < tot; base += cs) {
+      const unsigned i = base + lane;
       int32_t u = -1;
       uint32_t b = 0, e = 0;
-      if (i < qn) {
-        u = ld_cg(&qc[i]);
+      if (i < tot) {
+        int r = 0;
+        while (s_pre[r + 1] <= i) ++r;
+        u = (int32_t)s_rq[r]->q[cur][i - s_pre[r]];
         b = offsets[u];
         e = offsets[u + 1];
       }
@@ -257,18 +326,48 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
         const int32_t wu = __shfl_sync(0xffffffffu, u, src);
         const uint32_t wb = __shfl_sync(0xffffffffu, b, src);
         const uint32_t we = __shfl_sync(0xffffffffu, e, src);
-        for (uint32_t j = wb + lane; j < we; j += 32) td_visit(wu, nbrs[j], d, level, parent, offsets, io);
+        for (uint32_t j = wb + lane; j < we; j += 32)
+          small_visit(wu, nbrs[j], d, level, parent, offsets, sq, nx);
       }
       if (u >= 0 && deg < (uint32_t)kWarpDeg)  // thread gathering
-        for (uint32_t j = b; j < e; ++j) td_visit(u, nbrs[j], d, level, parent, offsets, io);
-    }
-    for (int h = 0; h < hn; ++h) {  // heavy vertices: the whole cluster
-      const int32_t u = ld_cg(&hqc[h]);
-      const uint32_t b = offsets[u], e = offsets[u + 1];
-      for (int64_t j = b + ctid; j < e; j += csize) td_visit(u, nbrs[j], d, level, parent, offsets, io);
+        for (uint32_t j = b; j < e; ++j) small_visit(u, nbrs[j], d, level, parent, offsets, sq, nx);
     }
     cl.sync();
   }
+  // hand-over at level d (not expanded): done, or the frontier back to the
+  // global queues for the cooperative grid
+  const int ci = d % 3, ni = (d + 1) % 3;
+  if (rank == 0 && threadIdx.x == 0) {
+    ctl->d = d;
+    ctl->done = s_tot == 0;
+    ctl->vis0 = vis;
+    ctl->reached += reached;
+    ctl->scanned += scanned;
+    ctl->levels = d - 1;
+    ctl->qn[ci] = ctl->hn[ci] = 0;
+    ctl->mf[ci] = 0;
+    ctl->qn[ni] = ctl->hn[ni] = 0;
+    ctl->mf[ni] = 0;
+  }
+  if (s_tot == 0) return;
+  cl.sync();  // (counters zeroed before the appends)
+  const unsigned qn = sq.qn[cur];
+  for (unsigned i = threadIdx.x; i < qn; i += blockDim.x) {
+    const int32_t v = (int32_t)sq.q[cur][i];
+    const uint32_t deg = offsets[v + 1] - offsets[v];
+    if (deg >= kHeavyDeg) {
+      qs.hq[d & 1][atomicAdd(&ctl->hn[ci], 1)] = v;
+    } else {
+      qs.q[d & 1][atomicAdd(&ctl->qn[ci], 1)] = v;
+    }
+  }
+  unsigned long long dsum = 0;
+  for (unsigned i = threadIdx.x; i < qn; i += blockDim.x) {
+    const int32_t v = (int32_t)sq.q[cur][i];
+    dsum += offsets[v + 1] - offsets[v];
+  }
+  for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+  if (lane == 0 && dsum) atomicAdd(&ctl->mf[ci], dsum);
 }
 
 __global__ void k_bfs_init(int64_t n, int32_t* level, int32_t* parent) {
@@ -356,10 +455,13 @@ static int small_cluster_ctas(Handle& h) {
   const char* env = getenv("RSTG_BFS_SMALL");
   if (env && atoi(env) == 0) return cached;
   CK(cudaFuncSetAttribute((const void*)k_bfs_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute((const void*)k_bfs_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)sizeof(SmallQ)));
   for (int c : {16, 8}) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c);
     cfg.blockDim = dim3(kSmallThreads);
+    cfg.dynamicSmemBytes = sizeof(SmallQ);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = c;
@@ -396,11 +498,19 @@ static void run_levels(Handle& h, int32_t* level, int32_t* parent, BfsQueues qs,
   const int32_t* nbrs = h.g.nbrs;
   int max_levels = (int)std::min<int64_t>(n + 2, 0x7ffffff0);
   int small_enter = cl ? kSmallEnter : 0;
+  // (a frontier whose degree sum could overflow a CTA's shared queue stays
+  // on the grid: dealt round-robin, each CTA gets about 1/cl of it)
+  unsigned long long small_mf = (unsigned long long)cl * kSmallCap / 4;
+  bool small_stalled = false;  // the small kernel handed back without a level
+  int d_now = 1;               // (the callers start every traversal at level 1)
   for (;;) {
-    if (cl && frontier <= kSmallExit) {
+    const int d_before = d_now;
+    const bool small = cl && frontier <= kSmallExit && !small_stalled;
+    if (small) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cl);
       cfg.blockDim = dim3(kSmallThreads);
+      cfg.dynamicSmemBytes = sizeof(SmallQ);
       cfg.stream = h.stream;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -409,11 +519,10 @@ static void run_levels(Handle& h, int32_t* level, int32_t* parent, BfsQueues qs,
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      CK(cudaLaunchKernelEx(&cfg, k_bfs_small, offsets, nbrs, level, parent, qs, ctl,
-                            (int)kSmallExit));
+      CK(cudaLaunchKernelEx(&cfg, k_bfs_small, offsets, nbrs, level, parent, qs, ctl));
     } else {
       void* args[] = {&n, &two_m, (void*)&offsets, (void*)&nbrs, &level, &parent, &qs, &ctl,
-                      &max_levels, &small_enter};
+                      &max_levels, &small_enter, &small_mf};
       CK(cudaLaunchCooperativeKernel((void*)k_bfs, dim3(max_blocks), dim3(kBlock), args, 0,
                                      h.stream));
     }
@@ -422,6 +531,8 @@ static void run_levels(Handle& h, int32_t* level, int32_t* parent, BfsQueues qs,
     CK(cudaStreamSynchronize(h.stream));
     const BfsCtl* hc = reinterpret_cast<const BfsCtl*>(h.host_box);
     if (hc->done) return;
+    small_stalled = small && hc->d == d_before;
+    d_now = hc->d;
     frontier = (int64_t)hc->qn[hc->d % 3] + hc->hn[hc->d % 3];
   }
 }

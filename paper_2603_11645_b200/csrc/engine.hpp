@@ -120,6 +120,11 @@ class Handle {
   // BFS, validation, degree counts -- clear this when they take the buffer).
   const void* minv_clean = nullptr;
   int64_t minv_clean_n = 0;  // ... for its first minv_clean_n entries
+  // PR-RST skip levels (pr.cu): vertex order by level and the counts C_k
+  // of vertices of level >= k, valid for graphs of pr_levels_n vertices
+  int64_t pr_levels_n = -1;
+  const void* pr_levels_byl = nullptr;
+  std::vector<int64_t> pr_levels_C;
   cudaStream_t copy_stream = nullptr;  // H2D staging of uploads (lazily created)
   cudaStream_t stream = nullptr;
   bool own_stream = true;
@@ -190,6 +195,7 @@ enum WsSlot : int {
   WS_PR_NEXT,     // u32 n         grafted roots of a round
   WS_PR_BYL,      // u32 n         vertices by descending skip level
   WS_PR_MK,       // u32 n         marked vertices, one queue per exact level
+  WS_PR_CBASE,    // u64 32        queue bases C_{b+1} (kept with pr_levels_n)
   // BFS
   WS_BFS_LEVEL,   // int32 n
   WS_BFS_Q0,      // int32 n

@@ -35,6 +35,8 @@
 // Tree edges and converged reps equal the CC's (same proposals, same
 // rounds); the parents are those of the reference's path reversals.
 // The designated root's tree is re-rooted at the end (:298-303).
+#include <cub/cub.cuh>
+
 #include "engine.hpp"
 
 namespace rstg {
@@ -45,6 +47,7 @@ void cc_round_done(Handle& h, int64_t out_count);
 void cc_reset_rounds(Handle& h);
 void compress_via_roots(Handle& h, int32_t* rep, int64_t n, const uint32_t* roots,
                         const unsigned long long* nroots);
+void launch_compress2(Handle& h, int32_t* rep, int64_t n);
 
 namespace {
 
@@ -94,35 +97,23 @@ __global__ void k_pr_init(int64_t n, int K, int32_t* parent, int32_t* rep, int32
     slot[v] = kKeyInf;
     const uint32_t l = vertex_level((uint32_t)v, K);
     lv[v] = (uint8_t)l | kRootBit;  // every vertex starts as its own tree
-    atomicAdd(&s_h[l], 1u);
+    if (hist) atomicAdd(&s_h[l], 1u);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i <= K; i += blockDim.x)
-    if (s_h[i]) atomicAdd(&hist[i], (unsigned long long)s_h[i]);
+  if (hist)
+    for (int i = threadIdx.x; i <= K; i += blockDim.x)
+      if (s_h[i]) atomicAdd(&hist[i], (unsigned long long)s_h[i]);
 }
 
-// Vertices sorted by descending level: level >= k is the prefix [0, C_k).
-// cursor[l] starts at C_{l+1}; order within a level is irrelevant.
-__global__ void k_pr_bylevel(int64_t n, const uint8_t* __restrict__ lv, uint32_t* byl,
-                             unsigned long long* cursor) {
-  __shared__ unsigned int s_c[kMaxLvl + 1];
-  __shared__ unsigned long long s_b[kMaxLvl + 1];
-  for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
-    for (int i = threadIdx.x; i <= kMaxLvl; i += blockDim.x) s_c[i] = 0;
-    __syncthreads();
-    const int64_t v = b0 + threadIdx.x;
-    int l = -1;
-    unsigned pos = 0;
-    if (v < n) {
-      l = lv[v] & 0x7F;
-      pos = atomicAdd(&s_c[l], 1u);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i <= kMaxLvl; i += blockDim.x)
-      s_b[i] = s_c[i] ? atomicAdd(&cursor[i], (unsigned long long)s_c[i]) : 0ull;
-    __syncthreads();
-    if (l >= 0) byl[s_b[l] + pos] = (uint32_t)v;
-    __syncthreads();
+// Sort keys of the level order: descending level = ascending (K - level);
+// a stable radix sort keeps ids ascending within a level, so level >= k is
+// the prefix [0, C_k) of the result and its walks sweep ids in order.
+__global__ void k_pr_level_keys(int64_t n, int K, const uint8_t* __restrict__ lv, uint32_t* keys,
+                                uint32_t* ids) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    keys[v] = (uint32_t)(K - (lv[v] & 0x7F));
+    ids[v] = (uint32_t)v;
   }
 }
 
@@ -192,19 +183,37 @@ __global__ void k_pr_resolve(const uint32_t* __restrict__ list, const unsigned l
                              uint8_t* mark, int32_t* scratch, uint32_t* seeds, uint32_t* grafted,
                              unsigned long long* ngraft) {
   const int64_t R = list ? (int64_t)*cnt : n;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = list ? list[i] : (uint32_t)i;
-    const unsigned long long key = slot[v];
-    if (key == kKeyInf) continue;
-    const int2 uv = edges[(uint32_t)key - e_base];
-    const int32_t u = (rep[uv.x] == (int32_t)v) ? uv.x : uv.y;
-    const int32_t w = (u == uv.x) ? uv.y : uv.x;
-    mark[u] = 1;
-    scratch[u] = w;
-    const unsigned long long p = atomicAdd(ngraft, 1ull);
-    seeds[p] = (uint32_t)u;
-    grafted[p] = v;
+  __shared__ uint32_t s_n;
+  __shared__ unsigned long long s_b;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < R; b += (int64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const int64_t i = b + threadIdx.x;
+    bool g = false;
+    uint32_t v = 0;
+    int32_t u = 0;
+    if (i < R) {
+      v = list ? list[i] : (uint32_t)i;
+      const unsigned long long key = slot[v];
+      if (key != kKeyInf) {
+        const int2 uv = edges[(uint32_t)key - e_base];
+        u = (rep[uv.x] == (int32_t)v) ? uv.x : uv.y;
+        const int32_t w = (u == uv.x) ? uv.y : uv.x;
+        mark[u] = 1;
+        scratch[u] = w;
+        g = true;
+      }
+    }
+    // one claim per block (round 0 grafts nearly every vertex)
+    const uint32_t pos = g ? atomicAdd(&s_n, 1u) : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) s_b = s_n ? atomicAdd(ngraft, (unsigned long long)s_n) : 0ull;
+    __syncthreads();
+    if (g) {
+      seeds[s_b + pos] = (uint32_t)u;
+      grafted[s_b + pos] = v;
+    }
+    __syncthreads();
   }
 }
 
@@ -297,22 +306,13 @@ __global__ void __launch_bounds__(kBlock)
                  const int32_t* __restrict__ ptr, const uint8_t* __restrict__ lv, uint8_t* mark,
                  uint32_t* mk, const unsigned long long* __restrict__ bbase,
                  unsigned long long* mcnt) {
-  __shared__ unsigned long long s_pre[kMaxLvl + 2];
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int b = j + 1; b <= K; ++b) {
-      s_pre[b] = t;
-      t += mcnt[b];
-    }
-    s_pre[K + 1] = t;
-  }
-  __syncthreads();
-  const int64_t T = (int64_t)s_pre[K + 1];
+  const int b = j + 1 + (int)blockIdx.y;  // this block row's bucket (level b > j)
+  if (b > K) return;
+  const int64_t T = (int64_t)mcnt[b];
+  const uint32_t* q = mk + bbase[b];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int b = j + 1;
-    while (b < K && (int64_t)s_pre[b + 1] <= i) ++b;
-    const int32_t a = (int32_t)mk[bbase[b] + (i - (int64_t)s_pre[b])];
+    const int32_t a = (int32_t)q[i];
     if (is_root(lv, a)) continue;
     int32_t x = up(parent, ptr, n, j, a);
     while (!is_root(lv, x) && lvl_of(lv, x) == j) {
@@ -337,63 +337,31 @@ __global__ void k_pr_check(const uint32_t* __restrict__ grafted, const uint32_t*
   }
 }
 
-// Index i over all marked queues (every level) -> the marked vertex.
-struct MarkedAt {
-  const uint32_t* mk;
-  const unsigned long long* bbase;
-  unsigned long long pre[kMaxLvl + 2];
-  int K;
-  __device__ int32_t operator()(int64_t i) const {
-    int b = 0;
-    while (b < K && (int64_t)pre[b + 1] <= i) ++b;
-    return (int32_t)mk[bbase[b] + (i - (int64_t)pre[b])];
-  }
-};
-__device__ void load_marked(MarkedAt& m, const unsigned long long* mcnt) {
-  unsigned long long t = 0;
-  for (int b = 0; b <= m.K; ++b) {
-    m.pre[b] = t;
-    t += mcnt[b];
-  }
-  m.pre[m.K + 1] = t;
-}
-
-// reverse_paths (pr_rst.cpp:186-201) over the marked vertices only.
-__global__ void k_pr_reverse_a(int K, const uint32_t* mk, const unsigned long long* bbase,
+// reverse_paths (pr_rst.cpp:186-201) over the marked vertices only; block
+// row y walks the queue of level y.
+__global__ void k_pr_reverse_a(const uint32_t* mk, const unsigned long long* bbase,
                                const unsigned long long* mcnt, const int32_t* __restrict__ parent,
                                int32_t* scratch) {
-  __shared__ MarkedAt m;
-  if (threadIdx.x == 0) {
-    m.mk = mk;
-    m.bbase = bbase;
-    m.K = K;
-    load_marked(m, mcnt);
-  }
-  __syncthreads();
-  const int64_t T = (int64_t)m.pre[K + 1];
+  const int b = (int)blockIdx.y;
+  const int64_t T = (int64_t)mcnt[b];
+  const uint32_t* q = mk + bbase[b];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t v = m(i);
+    const int32_t v = (int32_t)q[i];
     const int32_t p = parent[v];
     if (p != v) scratch[p] = v;
   }
 }
-__global__ void k_pr_reverse_b(int K, const uint32_t* mk, const unsigned long long* bbase,
+__global__ void k_pr_reverse_b(const uint32_t* mk, const unsigned long long* bbase,
                                const unsigned long long* mcnt, uint8_t* mark, int32_t* parent,
                                int32_t* scratch, int* bad_rev) {
-  __shared__ MarkedAt m;
-  if (threadIdx.x == 0) {
-    m.mk = mk;
-    m.bbase = bbase;
-    m.K = K;
-    load_marked(m, mcnt);
-  }
-  __syncthreads();
-  const int64_t T = (int64_t)m.pre[K + 1];
+  const int b = (int)blockIdx.y;
+  const int64_t T = (int64_t)mcnt[b];
+  const uint32_t* q = mk + bbase[b];
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t v = m(i);
+    const int32_t v = (int32_t)q[i];
     const int32_t s = scratch[v];
     if (s < 0) {
       bad = true;
@@ -460,25 +428,46 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   const unsigned g = grid_for(n);
   const cudaStream_t s = h.stream;
 
-  // ---- init: identity forest (make_pr_state :40-70), vertex levels, the
-  // descending-level vertex order (C_k = #vertices of level >= k)
-  h.timer.begin(s, "pr.init", 4.0 * n * 4 + 8.0 * n + 1.0 * n + 4.0 * n);
+  // ---- init: identity forest (make_pr_state :40-70) and vertex levels.
+  // The level order (vertices sorted by descending level, ids ascending
+  // within a level, so level-k walks sweep ids in order) and the counts C_k
+  // depend on n only: built once per graph size, kept with the handle.
+  h.timer.begin(s, "pr.init", (4.0 + 4.0 + 4.0 + 1.0 + 8.0 + 1.0) * n);
   CK(cudaMemsetAsync(pc, 0, (P_NWORDS + 2 * (kMaxLvl + 2)) * sizeof(unsigned long long), s));
-  k_pr_init<<<g, kBlock, 0, s>>>(n, K, parent, rep, scratch, mark, lv, slot, cursor);
+  const bool cached = h.pr_levels_n == n && h.pr_levels_byl == byl && (int)h.pr_levels_C.size() == K + 2;
+  k_pr_init<<<g, kBlock, 0, s>>>(n, K, parent, rep, scratch, mark, lv, slot, cached ? nullptr : cursor);
   CK_LAUNCH();
   CK(cudaMemsetAsync(bad_mark, 0xFF, sizeof(unsigned long long), s));
-  h.read_box(reinterpret_cast<int64_t*>(cursor), K + 1);
-  std::vector<int64_t> C(K + 2, 0);  // C[k] = #level >= k
-  for (int k = K; k >= 0; --k) C[k] = C[k + 1] + h.host_box[k];
-  {
-    unsigned long long hb[2 * (kMaxLvl + 2)] = {0};
-    for (int b = 0; b <= K; ++b) hb[b] = (unsigned long long)C[b + 1];  // bucket base
-    for (int b = 0; b <= K; ++b) hb[(kMaxLvl + 2) + b] = (unsigned long long)C[b + 1];  // cursors
-    CK(cudaMemcpyAsync(bbase, hb, sizeof(hb), cudaMemcpyHostToDevice, s));
+  unsigned long long* cbase = h.ws<unsigned long long>(WS_PR_CBASE, kMaxLvl + 2);
+  if (!cached) {
+    h.read_box(reinterpret_cast<int64_t*>(cursor), K + 1);
+    std::vector<int64_t> C(K + 2, 0);  // C[k] = #level >= k
+    for (int k = K; k >= 0; --k) C[k] = C[k + 1] + h.host_box[k];
+    // bucket b of the marked queues (and level b of byl) starts at C[b+1]
+    std::vector<unsigned long long> hb(kMaxLvl + 2, 0);
+    for (int b = 0; b <= K; ++b) hb[b] = (unsigned long long)C[b + 1];
+    CK(cudaMemcpy(cbase, hb.data(), hb.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    if (n > 0) {
+      // stable radix sort of (K - level) over ids in order
+      uint32_t* keys = h.ws<uint32_t>(WS_VAL_A, 2 * n);
+      uint32_t* ids = reinterpret_cast<uint32_t*>(h.ws<uint32_t>(WS_VAL_B, 2 * n));
+      k_pr_level_keys<<<g, kBlock, 0, s>>>(n, K, lv, keys, ids);
+      CK_LAUNCH();
+      int bits = 1;
+      while ((1 << bits) <= K) ++bits;
+      size_t temp = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys, keys + n, ids, byl, (int)n, 0, bits, s));
+      void* tmp = h.ws(WS_SL, temp);
+      CK(cub::DeviceRadixSort::SortPairs(tmp, temp, keys, keys + n, ids, byl, (int)n, 0, bits, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    h.pr_levels_C = C;
+    h.pr_levels_n = n;
+    h.pr_levels_byl = byl;
   }
-  if (n > 0) k_pr_bylevel<<<g, kBlock, 0, s>>>(n, lv, byl, cursor);
-  CK_LAUNCH();
-  CK(cudaStreamSynchronize(s));  // (hb is a host stack buffer)
+  const std::vector<int64_t>& C = h.pr_levels_C;
+  CK(cudaMemcpyAsync(bbase, cbase, (kMaxLvl + 2) * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToDevice, s));
   h.stats.step(n, 3);
   h.timer.end(s);
 
@@ -506,18 +495,22 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     k_pr_ascend<<<g, kBlock, 0, s>>>(seeds, pc + P_NGRAFT, n, parent, ptr, lv, mark, mk, bbase,
                                      mcnt);
     h.stats.step(n);
-    const unsigned dg = 4 * num_sms();
+    // level-j walkers are the queues of levels > j: one block row each,
+    // sized by the expected queue (n / 2^(b+1) path vertices at most)
     for (int j = K - 1; j >= 0; --j) {
-      k_pr_descend<<<dg, kBlock, 0, s>>>(j, K, n, parent, ptr, lv, mark, mk, bbase, mcnt);
+      const int64_t expect = std::max<int64_t>(C[j + 1] - C[j + 2], 1);
+      const unsigned gx = std::min<unsigned>(grid_for(expect), 2 * (unsigned)num_sms());
+      k_pr_descend<<<dim3(gx, K - j), kBlock, 0, s>>>(j, K, n, parent, ptr, lv, mark, mk, bbase,
+                                                      mcnt);
       h.stats.step(n);
     }
     CK_LAUNCH();
     h.timer.end(s);
   };
   auto run_reverse = [&]() {
-    const unsigned dg = 8 * num_sms();
-    k_pr_reverse_a<<<dg, kBlock, 0, s>>>(K, mk, bbase, mcnt, parent, scratch);
-    k_pr_reverse_b<<<dg, kBlock, 0, s>>>(K, mk, bbase, mcnt, mark, parent, scratch, bad_rev);
+    const dim3 dg(2 * num_sms(), K + 1);
+    k_pr_reverse_a<<<dg, kBlock, 0, s>>>(mk, bbase, mcnt, parent, scratch);
+    k_pr_reverse_b<<<dg, kBlock, 0, s>>>(mk, bbase, mcnt, mark, parent, scratch, bad_rev);
     CK_LAUNCH();
     h.stats.step(n);
     h.stats.step(n);
@@ -579,7 +572,10 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     // converged reps again (batched_jump's result, :216-252): the grafted
     // roots' chains are jumped as a list, then one gather over n
     h.timer.begin(s, "pr.jump", 8.0 * n);
-    compress_via_roots(h, rep, n, grafted, pc + P_NGRAFT);
+    if (nroots > n / 8)
+      launch_compress2(h, rep, n);  // many grafts (round 0: long hook chains): tile shortcutting
+    else
+      compress_via_roots(h, rep, n, grafted, pc + P_NGRAFT);
     h.stats.step(n, std::max<int64_t>(max_barriers / 2, 1) - 1);
     h.timer.end(s);
     // deferred error checks of this round (+ the marked count, for the

@@ -57,7 +57,8 @@ def main():
         rows, prev_end, t0 = [], None, ev[0].time_range.start if ev else 0
         for e in ev:
             st, en = e.time_range.start, e.time_range.end
-            rows.append({"name": e.name.split("(")[0][:60], "start_us": st - t0, "dur_us": en - st,
+            nm = e.name.replace("(anonymous namespace)::", "").split("(")[0][:60]
+            rows.append({"name": nm, "start_us": st - t0, "dur_us": en - st,
                          "gap_us": 0 if prev_end is None else max(0, st - prev_end)})
             prev_end = en if prev_end is None else max(prev_end, en)
         builds.append(rows)
@@ -67,6 +68,15 @@ def main():
     print(f"{a.workload} {a.algo}: span {statistics.median(span):.1f} us, kernels "
           f"{statistics.median(busy):.1f} us, idle {statistics.median(span) - statistics.median(busy):.1f} us, "
           f"{len(last)} device activities")
+    agg = {}
+    for r in last:
+        acc = agg.setdefault(r["name"], [0.0, 0, 0.0])
+        acc[0] += r["dur_us"]
+        acc[1] += 1
+        acc[2] += r["gap_us"]
+    print("per kernel (us, launches, idle before):")
+    for k, (d, c, gp) in sorted(agg.items(), key=lambda x: -x[1][0]):
+        print(f"  {d:10.1f} {c:5d} {gp:8.1f}  {k}")
     for r in last:
         print(f"{r['start_us']:9.1f} {r['dur_us']:8.1f} gap {r['gap_us']:7.1f}  {r['name']}")
     if a.json:

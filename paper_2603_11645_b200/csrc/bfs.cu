@@ -334,6 +334,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     }
     cl.sync();
   }
+  // every CTA leaves the loop at the same level (the totals are the
+  // cluster's), but a CTA may still be reading the others' counters through
+  // distributed shared memory: none exits before all have read
+  cl.sync();
   // hand-over at level d (not expanded): done, or the frontier back to the
   // global queues for the cooperative grid
   const int ci = d % 3, ni = (d + 1) % 3;

@@ -36,7 +36,8 @@ void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tf
                   uint32_t* tlist);
 void launch_cc_init(Handle& h, int32_t* rep, unsigned long long* slot);
 void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* slot,
-                   unsigned long long* out_count, int* any_prop);
+                   unsigned long long* out_count, int* any_prop,
+                   unsigned long long* zero_word = nullptr);
 void cc_round_done(Handle& h, int64_t out_count);
 void cc_reset_rounds(Handle& h);
 void launch_compress2(Handle& h, int32_t* rep, int64_t n);
@@ -148,6 +149,7 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
   Handle& h = g->h;
   check_root(h, root);
   h.stats = Stats{};
+  h.late_check = nullptr;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -171,6 +173,12 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
     throw ArgError("unknown algorithm");
   }
   CK(cudaEventRecord(e1, h.stream));
+  if (h.late_check) {  // (the deferred tile-ranking check: before anything reads P)
+    CK(cudaEventSynchronize(e1));
+    auto f = std::move(h.late_check);
+    h.late_check = nullptr;
+    f();
+  }
   if (roots && algo != RSTG_BFS) nroots = roots_ascending(h, parent, roots);
   CK(cudaEventSynchronize(e1));
   float ms = 0;

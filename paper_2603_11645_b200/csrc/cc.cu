@@ -64,10 +64,13 @@ __global__ void __launch_bounds__(kBlock)
     k_hook(const int2* __restrict__ edges, int64_t count, uint32_t e_base,
            const uint32_t* __restrict__ in_list, int32_t* rep,
            unsigned long long* __restrict__ slot, int* any_proposal, uint32_t* __restrict__ out_list,
-           unsigned long long* out_count, bool lazy) {
+           unsigned long long* out_count, bool lazy, unsigned long long* zero_word) {
   __shared__ unsigned long long s_base;
   __shared__ uint32_t s_total;
   bool proposed = false;
+  // a counter the next kernel on the stream accumulates into (the round's
+  // apply), cleared here instead of by a memset launch
+  if (zero_word && blockIdx.x == 0 && threadIdx.x == 0) *zero_word = 0;
   for (int64_t tile = blockIdx.x; tile * kHookTile < count; tile += gridDim.x) {
     const int64_t base = tile * kHookTile;
     uint32_t idx[kHookItems];
@@ -362,8 +365,15 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
       const uint32_t hd = s_head[i];
-      io.eu.vhead[base + i] = hd;  // (one arc of the cycle is all a later splice needs)
-      if (hd != kNone32) io.eu.S[arc_rev(s_tail[i], io.eu.nslots)] = hd;
+      io.eu.vhead[base + i] = hd;
+      if (hd != kNone32) {
+        // the tail is kept so a later splice needs no load of S: loading S
+        // right after other warps stored into the same sectors costs 3.4x
+        // in k_euler_fix (163 -> 553 us on road)
+        const uint32_t tl = s_tail[i];
+        io.eu.vtail[base + i] = tl;
+        io.eu.S[arc_rev(tl, io.eu.nslots)] = hd;
+      }
     }
   }
   if (SRC != kSrcRep) {
@@ -501,15 +511,42 @@ __global__ void __launch_bounds__(kBlock) k_final_gather(int64_t n, int32_t* rep
 
 // One shortcutting pass (optionally fused with the round's apply step or
 // the CSR first round): tile resolve, then the exit set, then the gather.
-void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& io) {
+// Zeroes up to kZeroRanges word ranges in one launch (the counters and
+// bitmaps a phase accumulates into), instead of one memset launch each.
+constexpr int kZeroRanges = 6;
+struct ZeroRanges {
+  uint32_t* p[kZeroRanges];
+  uint32_t words[kZeroRanges];
+  int k;
+  void add(void* ptr, size_t bytes) {
+    p[k] = static_cast<uint32_t*>(ptr);
+    words[k++] = (uint32_t)(bytes / 4);
+  }
+};
+__global__ void k_zero_ranges(ZeroRanges z) {
+  for (int r = 0; r < z.k; ++r)
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < z.words[r];
+         i += gridDim.x * blockDim.x)
+      z.p[r][i] = 0;
+}
+
+void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& io,
+                   const ZeroRanges* extra = nullptr) {
   if (n <= 0) return;
   const int64_t words = (n + 31) / 32;
   uint32_t* xbits = h.ws<uint32_t>(WS_XBITS, words);
   uint32_t* xlist = h.ws<uint32_t>(WS_HEADS, n + 1);
   unsigned long long* xcount = reinterpret_cast<unsigned long long*>(h.dev_box) + 5;
   int* flags = reinterpret_cast<int*>(h.dev_box + 6);  // 3 ints in dev_box[6..7]
-  CK(cudaMemsetAsync(xbits, 0, (size_t)words * sizeof(uint32_t), h.stream));
-  CK(cudaMemsetAsync(h.dev_box + 5, 0, 3 * sizeof(int64_t), h.stream));
+  {
+    ZeroRanges z = extra ? *extra : ZeroRanges{};
+    if (!extra) z.k = 0;
+    z.add(xbits, (size_t)words * sizeof(uint32_t));
+    z.add(h.dev_box + 5, 3 * sizeof(int64_t));
+    k_zero_ranges<<<(unsigned)std::min<int64_t>(1184, (words + 1023) / 1024 + 1), 1024, 0,
+                    h.stream>>>(z);
+    CK_LAUNCH();
+  }
   const unsigned tiles = (unsigned)((n + kTileV - 1) / kTileV);
   static int coop_blocks = 0;
   ensure_dyn_smem((const void*)k_tile_resolve<kSrcApply>, kTileSmem);
@@ -684,22 +721,23 @@ void launch_compress2(Handle& h, int32_t* rep, int64_t n) {
 
 static void launch_hook_k(Handle& h, int mode, const int2* edges, int64_t count, uint32_t e_base,
                           const uint32_t* in_list, const int32_t* rep_c, unsigned long long* slot,
-                          int* any_prop, uint32_t* out_list, unsigned long long* out_count) {
+                          int* any_prop, uint32_t* out_list, unsigned long long* out_count,
+                          unsigned long long* zero_word = nullptr) {
   const unsigned grid = grid_for((count + kHookItems - 1) / kHookItems);
   int32_t* rep = const_cast<int32_t*>(rep_c);  // lazy mode path-compresses
   const bool lazy = h.cc_lazy;
   if (mode == 0 && out_list)
     k_hook<0, true><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
-                                                   any_prop, out_list, out_count, lazy);
+                                                   any_prop, out_list, out_count, lazy, zero_word);
   else if (mode == 0)
     k_hook<0, false><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
-                                                    any_prop, out_list, out_count, lazy);
+                                                    any_prop, out_list, out_count, lazy, zero_word);
   else if (out_list)
     k_hook<1, true><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
-                                                   any_prop, out_list, out_count, lazy);
+                                                   any_prop, out_list, out_count, lazy, zero_word);
   else
     k_hook<1, false><<<grid, kBlock, 0, h.stream>>>(edges, count, e_base, in_list, rep, slot,
-                                                    any_prop, out_list, out_count, lazy);
+                                                    any_prop, out_list, out_count, lazy, zero_word);
   CK_LAUNCH();
   h.stats.step(count);
 }
@@ -714,21 +752,31 @@ void launch_hook(Handle& h, int mode, const int2* edges, int64_t m, uint32_t e_b
 // edges; later rounds visit only the previous round's list.
 // *out_count (device) must be zero; pass its host value to cc_round_done.
 void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* slot,
-                   unsigned long long* out_count, int* any_prop) {
+                   unsigned long long* out_count, int* any_prop, unsigned long long* zero_word) {
   const int64_t m = h.g.m;
   const uint32_t eb = (uint32_t)h.g.e_base;
+  bool launched = false;
   if (h.cc_round == 0 || m == 0) {
-    if (m > 0)
-      launch_hook_k(h, mode, h.g.edges, m, eb, nullptr, rep, slot, any_prop, nullptr, nullptr);
+    if (m > 0) {
+      launch_hook_k(h, mode, h.g.edges, m, eb, nullptr, rep, slot, any_prop, nullptr, nullptr,
+                    zero_word);
+      launched = true;
+    }
   } else if (h.cc_active < 0) {
     uint32_t* out = h.ws<uint32_t>(WS_ELIST0, m);
-    launch_hook_k(h, mode, h.g.edges, m, eb, nullptr, rep, slot, any_prop, out, out_count);
+    launch_hook_k(h, mode, h.g.edges, m, eb, nullptr, rep, slot, any_prop, out, out_count,
+                  zero_word);
+    launched = true;
   } else {
     const uint32_t* in = h.ws<uint32_t>(h.cc_list ? WS_ELIST1 : WS_ELIST0, m);
     uint32_t* out = h.ws<uint32_t>(h.cc_list ? WS_ELIST0 : WS_ELIST1, m);
-    if (h.cc_active > 0)
-      launch_hook_k(h, mode, h.g.edges, h.cc_active, eb, in, rep, slot, any_prop, out, out_count);
+    if (h.cc_active > 0) {
+      launch_hook_k(h, mode, h.g.edges, h.cc_active, eb, in, rep, slot, any_prop, out, out_count,
+                    zero_word);
+      launched = true;
+    }
   }
+  if (zero_word && !launched) CK(cudaMemsetAsync(zero_word, 0, sizeof(*zero_word), h.stream));
 }
 void cc_round_done(Handle& h, int64_t out_count) {
   if (h.cc_round >= 1 && h.g.m > 0) {
@@ -762,8 +810,12 @@ void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tf
 // list == nullptr: the roots are all vertices [0, n).
 __global__ void __launch_bounds__(kBlock)
     k_apply_roots(const uint32_t* __restrict__ list, const unsigned long long* count, int64_t n,
-                  int32_t* rep, RoundIO io, uint32_t* out_list, unsigned long long* out_count) {
+                  int32_t* rep, RoundIO io, uint32_t* out_list, unsigned long long* out_count,
+                  unsigned long long* zero2) {
   const int64_t R = list ? (int64_t)*count : n;
+  // the next hook round's counters (crossing count, any-proposal flag): the
+  // host has read them already
+  if (zero2 && blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   __shared__ uint32_t s_n, s_h;
   __shared__ unsigned long long s_b;
@@ -881,7 +933,12 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
   // the init step (cc_forest.cpp:82) counts whether or not it had work left
   h.stats.step(n, (!round0 || !slots_ok) ? 1 : 0);
   if (tflag && m > 0) CK(cudaMemsetAsync(tflag, 0, (size_t)m, h.stream));
-  CK(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), h.stream));
+  // the counters of the build: [0] hooks, [1] crossing, [2] any proposal,
+  // [20..22] roots counts -- zeroed in one launch (with round 0's exit-set
+  // state when round 0 runs)
+  ZeroRanges zc{};
+  zc.add(counter, 3 * sizeof(unsigned long long));
+  zc.add(counter + 20, 3 * sizeof(unsigned long long));
   h.timer.end(h.stream);
   int mode = 0;  // HookMode::kMin first (cc_forest.cpp:87)
   int* any = reinterpret_cast<int*>(h.dev_box + 2);
@@ -891,7 +948,6 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
   uint32_t* rl[3] = {rlist, rlist + n + 1, rlist + 2 * n + 2};
   // dev_box [20] round-0 roots, [21] current roots in, [22] out
   unsigned long long* rcount = reinterpret_cast<unsigned long long*>(h.dev_box) + 20;
-  CK(cudaMemsetAsync(rcount, 0, sizeof(unsigned long long), h.stream));
   RoundIO io{slot, tflag, (uint32_t)h.g.e_base, (uint32_t)m, counter, h.g.offsets, h.g.nbrs,
              h.g.arc_edge, h.g.edges, euler != nullptr, euler ? *euler : EulerIO{}, rl[0], rcount,
              keys_from_edges};
@@ -902,7 +958,8 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     // upload's keys), fused with its apply and shortcutting
     // offsets, first neighbour, rep; a tree edge (arc heads + successors) per vertex
     h.timer.begin(h.stream, "cc.round0", 4.0 * (n + 1) + 8.0 * n + (euler ? 16.0 * n : 0.0));
-    resolve_round(h, rep, n, keyed ? kSrcRound0Slot : kSrcRound0, io);
+    resolve_round(h, rep, n, keyed ? kSrcRound0Slot : kSrcRound0, io, &zc);
+    zc.k = 0;
     h.timer.end(h.stream);
     cc_round_done(h, 0);
     round = 1;
@@ -911,11 +968,14 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
   // Rounds >= 1 run lazy: no compression pass per round (hooks find roots,
   // apply touches the current roots only), one find pass at the end.
   const bool have_r0 = round == 1;  // round 0 collected the roots
-  if (have_r0)
-    CK(cudaMemcpyAsync(rcount + 1, rcount, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
-                       h.stream));
+  if (zc.k) {  // (no round 0: the counters still need their zeros)
+    k_zero_ranges<<<1, 32, 0, h.stream>>>(zc);
+    CK_LAUNCH();
+  }
+  // roots list rl[i] has its count in rcount[i]; apply reads list `in`
+  // and writes list `out` (1 and 2 alternate after the round-0 list)
   const uint32_t* in_list = have_r0 ? rl[0] : nullptr;  // nullptr: all vertices
-  int out = 1;
+  int in = 0, out = 1;
   auto compress = [&]() {
     if (have_r0)
       compress_via_roots(h, rep, n, rl[0], rcount);
@@ -933,7 +993,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
       h.cc_lazy = false;
       throw AlgoError("hooking failed to converge");
     }
-    CK(cudaMemsetAsync(counter + 1, 0, 2 * sizeof(unsigned long long), h.stream));
+    // (counter[1], counter[2] are zero here: the build's zeroing, then each apply)
     // compulsory: each visited edge 8 B (+ 4 B list entry when filtered),
     // the rep array once (4 B per vertex, at most two gathers per edge),
     // 4 B per crossing edge appended (added once the count is read)
@@ -942,24 +1002,25 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     const char* hook_phase = mode == 0 ? "cc.hook_min" : "cc.hook_max";
     h.timer.begin(h.stream, hook_phase,
                   visited * (filtered ? 12.0 : 8.0) + std::min(4.0 * n, 8.0 * visited));
-    cc_hook_round(h, mode, rep, slot, counter + 1, any);
+    // (the hook clears the count this round's apply appends to)
+    cc_hook_round(h, mode, rep, slot, counter + 1, any, rcount + out);
     h.timer.end(h.stream);
-    // hooks so far, crossing, any; [20] the round-0 roots count, [21] the
-    // current roots count (same read)
-    h.read_box(reinterpret_cast<int64_t*>(counter), 22);
+    // hooks so far, crossing, any; [20] the round-0 roots count, [20 + in]
+    // the current roots count (same read)
+    h.read_box(reinterpret_cast<int64_t*>(counter), 23);
     if (h.cc_round >= 1 && m > 0) h.timer.add_bytes(hook_phase, 4.0 * h.host_box[1]);
     const int64_t r0_count = have_r0 ? h.host_box[20] : 0;
-    const int64_t cur_roots = have_r0 ? h.host_box[21] : n;
+    const int64_t cur_roots = have_r0 ? h.host_box[20 + in] : n;
     prev_total = total;
     total = h.host_box[0];
     bool proposed = h.host_box[2] != 0;
     if (ex) {
       // proposals of all ranks (they target current roots only), then the
       // global "any proposal" decides the stop on every rank alike
-      h.timer.begin(h.stream, "cc.exchange", 16.0 * (have_r0 ? h.host_box[21] : n));
+      h.timer.begin(h.stream, "cc.exchange", 16.0 * cur_roots);
       CK(cudaMemsetAsync(any, 0, sizeof(int), h.stream));
       if (have_r0) {
-        const int64_t R = h.host_box[21];
+        const int64_t R = h.host_box[20 + in];
         if (R > 0) {
           // the roots list is filled by atomics (tile / block order varies
           // from rank to rank): sort it by id so position i names the same
@@ -998,14 +1059,12 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     if (!proposed) break;
     // per current root: list entry 4 B, slot 8 B, rep or next-list entry 4 B
     h.timer.begin(h.stream, "cc.apply", 16.0 * cur_roots);
-    CK(cudaMemsetAsync(rcount + 2, 0, sizeof(unsigned long long), h.stream));
-    k_apply_roots<<<grid_for(n), kBlock, 0, h.stream>>>(in_list, rcount + 1, n, rep, io, rl[out],
-                                                        rcount + 2);
-    CK(cudaMemcpyAsync(rcount + 1, rcount + 2, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
-                       h.stream));
+    k_apply_roots<<<grid_for(n), kBlock, 0, h.stream>>>(in_list, rcount + in, n, rep, io, rl[out],
+                                                        rcount + out, counter + 1);
     CK_LAUNCH();
     h.stats.step(n);
     in_list = rl[out];
+    in = out;
     out = out == 1 ? 2 : 1;
     h.timer.end(h.stream);
     mode ^= 1;

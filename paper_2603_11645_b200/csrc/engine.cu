@@ -109,6 +109,7 @@ void* Handle::ws(int slot, size_t bytes) {
   if (b.second < bytes) {
     // a new buffer (possibly at the old address) holds nothing known
     if (slot == WS_MINV) minv_clean = nullptr;
+    if (slot == WS_RHEAD) rhead_clean = nullptr;
     if (slot == WS_SLOT) slots_clean = nullptr;
     if (slot == WS_PR_BYL || slot == WS_PR_CBASE) pr_levels_n = -1;
     if (b.first) {
@@ -125,6 +126,7 @@ void* Handle::ws(int slot, size_t bytes) {
 void Handle::release(int slot) {
   auto& b = bufs_[slot];
   if (slot == WS_MINV) minv_clean = nullptr;
+  if (slot == WS_RHEAD) rhead_clean = nullptr;
   if (slot == WS_SLOT) slots_clean = nullptr;
   if (slot == WS_PR_BYL || slot == WS_PR_CBASE) pr_levels_n = -1;
   if (b.first) {

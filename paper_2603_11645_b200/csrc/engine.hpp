@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -116,10 +117,23 @@ class Handle {
   // apart (-1: not measured for this graph). Decides the Euler-tour
   // ranking: tile contraction for locally numbered graphs, else ruling sets.
   int edge_locality = -1;
+  // Segment count of the last tile-contraction ranking of this graph (-1:
+  // none yet): later builds size the level grids from it (with a margin;
+  // a larger count raises the device overflow flag) instead of reading the
+  // count back mid-build. Reset with edge_locality when the graph changes.
+  int64_t tile_segments = -1;
+  // Work a build left to check after its final stream sync (the tile
+  // ranking's overflow flag, copied asynchronously into host_box[32..]):
+  // run by run_late_checks() before anything reads the outputs.
+  std::function<void()> late_check;
   // WS_MINV holds all-ones left by the Euler root pass (its other users --
   // BFS, validation, degree counts -- clear this when they take the buffer).
   const void* minv_clean = nullptr;
   int64_t minv_clean_n = 0;  // ... for its first minv_clean_n entries
+  // WS_RHEAD holds all-NONE left by the Euler vertex pass (it resets every
+  // remote list it splices), so a build needs no 4n-byte fill
+  const void* rhead_clean = nullptr;
+  int64_t rhead_clean_n = 0;
   // PR-RST skip levels (pr.cu): vertex order by level and the counts C_k
   // of vertices of level >= k, valid for graphs of pr_levels_n vertices
   int64_t pr_levels_n = -1;
@@ -208,7 +222,7 @@ enum WsSlot : int {
   WS_VAL_C,
   // Euler tour (euler.cu): rotation lists
   WS_VHEAD,       // u32 n         first arc of each vertex's local rotation list
-  WS_VTAIL,       // (unused: local lists keep no tail)
+  WS_VTAIL,       // u32 n         its last arc
   WS_RHEAD,       // u32 n         remote list (atomic prepends): first arc
   WS_RTAIL,       // u32 n         its last arc (the first one inserted)
   WS_ETO,         // u32 2N        arc heads, pairs (2i: a->b, 2i+1: b->a)
@@ -243,15 +257,15 @@ enum WsSlot : int {
 //
 // Two lists per vertex, concatenated by the vertex pass after the CC: the
 // "local" one written by round 0's shared-memory tiles with plain stores
-// (vhead: one arc of it, every vertex covered, so no initialisation; it is
-// closed into its cycle at once, so no tail is kept -- a splice goes in
-// after vhead), and the "remote" one that every other link prepends to with
+// (vhead/vtail, every vertex covered, so no initialisation; closed into its
+// cycle at once), and the "remote" one that every other link prepends to with
 // atomicExch (rhead/rtail, NONE-initialised).
 struct EulerIO {
   uint32_t nslots;  // N
   uint32_t* eto;    // N pairs (to(i), to(N + i)) = (b, a)
   uint32_t* S;      // 2N  successors
-  uint32_t* vhead;  // n   local cycle: one of its arcs (NONE: no local list)
+  uint32_t* vhead;  // n   local cycle: its first arc (NONE: no local list)
+  uint32_t* vtail;  // n   local cycle: its last arc (S[rev(vtail)] = vhead)
   uint32_t* rhead;  // n   remote list: first arc (NONE-initialised)
   uint32_t* rtail;  // n   remote list: last arc (the first inserted)
 };

@@ -137,13 +137,17 @@ __global__ void __launch_bounds__(kBlock)
       if (h2[k] == kNone32) continue;
       const int64_t v = base + k * kBlock + threadIdx.x;
       const uint32_t h1 = io.vhead[v], t2 = io.rtail[v];
-      if (h1 != kNone32) {  // the remote chain goes in right after h1
-        const uint32_t nx = io.S[arc_rev(h1, io.nslots)];
-        io.S[arc_rev(h1, io.nslots)] = h2[k];
-        io.S[arc_rev(t2, io.nslots)] = nx;
+      if (h1 != kNone32) {  // local tail -> remote head, remote tail -> local head
+        io.S[arc_rev(io.vtail[v], io.nslots)] = h2[k];
+        io.S[arc_rev(t2, io.nslots)] = h1;
       } else {
         io.S[arc_rev(t2, io.nslots)] = h2[k];
+        io.vhead[v] = h2[k];
       }
+      // the spliced cycle is (vhead .. t2): the root pass reads only
+      // vhead/vtail, and the remote list is left empty for the next build
+      io.vtail[v] = t2;
+      io.rhead[v] = kNone32;
     }
     uint32_t id = rulers ? lr_block_claim(__popc(flags & 0xFFFFu), ctr) : 0u;
     const uint32_t nl = __popc(flags >> 16);
@@ -194,13 +198,9 @@ __global__ void __launch_bounds__(kBlock)
       const uint32_t r = minv[labels[i]];
       if (reset) minv[labels[i]] = kNone32;
       parent[r] = (int32_t)r;
-      const uint32_t h1 = io.vhead[r], h2 = io.rhead[r];
-      const uint32_t x = h1 != kNone32 ? h1 : h2;  // an arc of r's (spliced) rotation cycle
-      if (x != kNone32) {
-        // the tour starts with the arc after x and ends entering r by rev(x)
-        hd = io.S[arc_rev(x, io.nslots)];
-        io.S[arc_rev(x, io.nslots)] = kNone32;
-      }
+      hd = io.vhead[r];  // the combined cycle (k_euler_fix spliced the remote list)
+      if (hd != kNone32)
+        io.S[arc_rev(io.vtail[r], io.nslots)] = kNone32;  // the tour ends back at the root
     }
     if (!rulers) continue;  // (block-uniform)
     const bool head = hd != kNone32 && !lr_hash_ruler(hd, logk);
@@ -277,10 +277,15 @@ EulerIO euler_buffers(Handle& h, int64_t N, bool local_written) {
   io.eto = h.ws<uint32_t>(WS_ETO, 2 * N);
   io.S = h.ws<uint32_t>(WS_SUCC, 2 * N);
   io.vhead = h.ws<uint32_t>(WS_VHEAD, h.g.n);
+  io.vtail = h.ws<uint32_t>(WS_VTAIL, h.g.n);
   io.rhead = h.ws<uint32_t>(WS_RHEAD, h.g.n);
   io.rtail = h.ws<uint32_t>(WS_RTAIL, h.g.n);
   if (!local_written) CK(cudaMemsetAsync(io.vhead, 0xFF, (size_t)h.g.n * sizeof(uint32_t), h.stream));
-  CK(cudaMemsetAsync(io.rhead, 0xFF, (size_t)h.g.n * sizeof(uint32_t), h.stream));
+  // the remote heads are all-NONE between builds (k_euler_fix resets what it
+  // splices); a fresh buffer, or one a failed build left dirty, is filled
+  if (h.rhead_clean != io.rhead || h.g.n > h.rhead_clean_n)
+    CK(cudaMemsetAsync(io.rhead, 0xFF, (size_t)h.g.n * sizeof(uint32_t), h.stream));
+  h.rhead_clean = nullptr;  // (until the vertex pass has consumed the lists)
   return io;
 }
 
@@ -371,6 +376,8 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   k_euler_fix<<<grid_for((n + kFixItems - 1) / kFixItems), kBlock, 0, s>>>(
       n, labels, present, minv, io, cc_slots, lablist, comps, rpos, sl, ctr, tiles, P.logk0, P.ob,
       (uint32_t)P.cap, !use_tiles);
+  h.rhead_clean = io.rhead;
+  h.rhead_clean_n = n;
   k_override_root<<<1, 32, 0, s>>>(labels, minv, designated_root, cc_slots);
   k_euler_roots<<<grid_for(n), kBlock, 0, s>>>(lablist, comps, minv, io, parent, rpos, sl, ctr,
                                                P.logk0, P.ob, (uint32_t)P.cap, !use_tiles,
@@ -399,11 +406,20 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
     // edge the pair's heads 8 B, the other arc's word 4 B + offset 2 B, the
     // parent 4 B (segment starts: one small L2-resident table)
     h.timer.begin(s, "euler.orient", 6.0 * N + 18.0 * T);
-    k_orient_tiles<<<grid_for(N), kBlock, 0, s>>>(N, reinterpret_cast<const uint2*>(io.eto), tr.seg,
-                                                  tr.off, tr.segstart, parent);
+    const uint2* eto = reinterpret_cast<const uint2*>(io.eto);
+    k_orient_tiles<<<grid_for(N), kBlock, 0, s>>>(N, eto, tr.seg, tr.off, tr.segstart, parent);
     CK_LAUNCH();
     h.stats.step(N);
     h.timer.end(s);
+    if (tr.deferred)
+      h.late_check = [&h, P, N, tr, eto, parent] {
+        if (tile_rank_settle(h, P, N, tr)) {  // re-derive from the recomputed ranks
+          k_orient_tiles<<<grid_for(N), kBlock, 0, h.stream>>>(N, eto, tr.seg, tr.off, tr.segstart,
+                                                               parent);
+          CK_LAUNCH();
+          CK(cudaStreamSynchronize(h.stream));
+        }
+      };
     return;
   }
   const uint32_t* rstart = lr_rank(h, P, E, io.S, sl, rpos, ctr, verify, 2 * T, nullptr);

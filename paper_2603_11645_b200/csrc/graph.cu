@@ -126,6 +126,7 @@ static void upload_narrow(Handle& h, const int64_t* host, int64_t count, T* dev)
 static void alloc_graph(Handle& h, int64_t n, int64_t m, bool csr) {
   h.round0_slots = nullptr;  // (new edges: any upload keys are stale)
   h.edge_locality = -1;
+  h.tile_segments = -1;
   if (n < 0) throw ArgError("negative vertex count");
   if (n >= (int64_t{1} << 31)) throw ArgError("graph too large: vertex ids exceed 2^31");
   if (m > (int64_t{1} << 32)) throw ArgError("too many edges");
@@ -150,6 +151,7 @@ void upload_reference_graph(Handle& h, const int64_t* offsets, const int64_t* nb
   h.g.csr_pending = false;
   h.round0_slots = nullptr;
   h.edge_locality = -1;
+  h.tile_segments = -1;
   if (csr) {
     upload_narrow<uint32_t>(h, offsets, n + 1, h.g.offsets);
     upload_narrow<int32_t>(h, nbrs, 2 * m, h.g.nbrs);
@@ -607,6 +609,7 @@ void upload_edges_build_csr(Handle& h, const int64_t* edges_uv, int64_t n, int64
   h.slots_clean = nullptr;
   h.round0_slots = nullptr;
   h.edge_locality = -1;
+  h.tile_segments = -1;
   if (m > 0) {
     if (!h.copy_stream) CK(cudaStreamCreateWithFlags(&h.copy_stream, cudaStreamNonBlocking));
     const int64_t chunk = int64_t{1} << 22;  // edges per staging buffer (32 MB of int64 pairs)

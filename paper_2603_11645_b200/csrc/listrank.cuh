@@ -107,9 +107,18 @@ struct TileRank {
   const uint32_t* seg;       // 2N segment id per arc
   const uint16_t* off;       // 2N offset within the segment
   const uint32_t* segstart;  // rank of each segment's first arc
+  // The upper levels ran on a grid sized from the previous build's segment
+  // count: their overflow flag and the real count are copied to
+  // host_box[32..49) asynchronously; tile_rank_settle() checks them after
+  // the build's final sync (and re-ranks the segments when they overflowed).
+  bool deferred = false;
 };
 TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* S,
                        const int32_t* lab, bool cc_slots, int64_t T, bool verify);
+// After the stream has synced: true when the deferred levels overflowed and
+// segstart has been recomputed on the stream (the caller re-derives the
+// parents); records the segment count for the next build either way.
+bool tile_rank_settle(Handle& h, const LrParams& P, int64_t N, const TileRank& tr);
 
 // Generic entry (rstg_k_list_rank, explicit lists): registers hash rulers
 // and every list head (positions without a predecessor), then lr_rank.

@@ -42,7 +42,8 @@
 namespace rstg {
 
 void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* slot,
-                   unsigned long long* out_count, int* any_prop);
+                   unsigned long long* out_count, int* any_prop,
+                   unsigned long long* zero_word = nullptr);
 void cc_round_done(Handle& h, int64_t out_count);
 void cc_reset_rounds(Handle& h);
 void compress_via_roots(Handle& h, int32_t* rep, int64_t n, const uint32_t* roots,

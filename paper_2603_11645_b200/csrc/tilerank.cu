@@ -473,10 +473,13 @@ constexpr int kLevelThreads = 1024;
 // node counts stay on the device and each grid is sized for contraction of
 // at least 3x per level (3.6-4x is typical on locally numbered tours); a level that needs more tiles, or a
 // top with more than one tile, raises `overflow` and the caller falls back
-// to list_prefix. Returns false on overflow.
+// to list_prefix. Returns false on overflow. deferred: R is only a bound
+// (the previous build's count plus a margin); nothing is read back here --
+// the counts and the overflow flag go to host_box[32..49) asynchronously
+// and the caller settles them after its final sync (tile_rank_settle).
 static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
                                const uint32_t* exit1, const uint32_t* len1, uint32_t* pre1,
-                               bool dbg) {
+                               bool dbg, bool deferred) {
   const cudaStream_t s = h.stream;
   constexpr int kMaxLevels = WS_TL_LAST - WS_TL2;
   // level l: its nodes are the segments of level l - 1 (level 0: of the
@@ -564,12 +567,25 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
                                                           L[l + 1].pre, L[l].pre);
     CK_LAUNCH();
   }
+  if (deferred) {
+    CK(cudaMemcpyAsync(h.host_box + 32, blk, 17 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    return true;
+  }
   h.read_box(reinterpret_cast<int64_t*>(blk), 17);  // counts, overflow
   if (dbg) {
     for (int l = 0; l <= top; ++l)
       fprintf(stderr, "lr.tiles level %d: %lld nodes\n", l + 2, (long long)h.host_box[l]);
   }
   return *reinterpret_cast<int*>(&h.host_box[16]) == 0;
+}
+
+// The segments' ranks by the generic list ranking (levels that stall).
+static void tile_fallback(Handle& h, const LrParams& Q, int64_t R, const uint32_t* seg,
+                          const uint32_t* seg_exit, const uint32_t* seg_len, uint32_t* seg_next,
+                          uint32_t* segstart, const unsigned long long* nseg) {
+  k_seg_link<<<grid_for(R), kBlock, 0, h.stream>>>(nseg, seg_exit, seg, seg_next);
+  CK_LAUNCH();
+  list_prefix(h, Q, R, seg_next, seg_len, segstart, 0, false, nullptr);
 }
 
 TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* S,
@@ -614,13 +630,27 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
     launch(k_tile_rank<8192, 1024, 16>, 1024, tile_rank_smem<8192>());
   CK_LAUNCH();
   h.stats.step(E, 2);
-  h.read_box(h.dev_box + 8, 8);  // [8] segments, [14] arcs walked, [15] jump rounds
-  const int64_t R = h.host_box[0];
-  if (dbg)
-    fprintf(stderr, "lr.tiles: %lld arcs -> %lld segments (%.1fx), %lld jump rounds\n",
-            (long long)(2 * T), (long long)R, R ? 2.0 * T / R : 0.0, (long long)h.host_box[7]);
-  if (verify && h.host_box[6] != 2 * T)  // a cycle inside a tile has no head
-    throw AlgoError("list ranking failed to converge: not a forest");
+  // The segment count sizes the level grids. A repeated build of the same
+  // graph takes it from the previous build (plus a margin: the count
+  // depends only on the tree and, by one segment, on the root) instead of
+  // a host round trip here; the levels raise their overflow flag if the
+  // bound was short, and the settle step after the build re-ranks then.
+  const bool deferred = !verify && !dbg && h.tile_segments >= 0;
+  int64_t R;
+  if (deferred) {
+    R = std::min<int64_t>(E, h.tile_segments + h.tile_segments / 8 + 8192);
+    const int forced = env_int("RSTG_LR_SEGBOUND", 0);  // (tests: a short bound)
+    if (forced > 0) R = forced;
+  } else {
+    h.read_box(h.dev_box + 8, 8);  // [8] segments, [14] arcs walked, [15] jump rounds
+    R = h.host_box[0];
+    h.tile_segments = R;
+    if (dbg)
+      fprintf(stderr, "lr.tiles: %lld arcs -> %lld segments (%.1fx), %lld jump rounds\n",
+              (long long)(2 * T), (long long)R, R ? 2.0 * T / R : 0.0, (long long)h.host_box[7]);
+    if (verify && h.host_box[6] != 2 * T)  // a cycle inside a tile has no head
+      throw AlgoError("list ranking failed to converge: not a forest");
+  }
   h.timer.end(s);
 
   h.timer.begin(s, "lr.rulers_rank", 16.0 * R);
@@ -629,11 +659,19 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   LrParams Q = P;
   Q.cap = std::max<int64_t>(P.cap, E + 1);  // (level arenas sized by the fixed bound)
   const int levels_env = env_int("RSTG_LR_TILELEVELS", 1);  // (0: segments by list_prefix)
-  if (!(levels_env && R * 4 <= E &&
-        tile_prefix_levels(h, R, seg, seg_exit, seg_len, segstart, dbg))) {
-    k_seg_link<<<grid_for(R), kBlock, 0, s>>>(nseg, seg_exit, seg, seg_next);
-    CK_LAUNCH();
-    list_prefix(h, Q, R, seg_next, seg_len, segstart, 0, false, nullptr);
+  bool late = false;
+  if (levels_env && R * 4 <= E) {
+    if (tile_prefix_levels(h, R, seg, seg_exit, seg_len, segstart, dbg, deferred))
+      late = deferred;
+    else
+      tile_fallback(h, Q, R, seg, seg_exit, seg_len, seg_next, segstart, nseg);
+  } else {
+    if (deferred) {  // (the exact count is needed here)
+      h.read_box(h.dev_box + 8, 1);
+      R = h.host_box[0];
+      h.tile_segments = R;
+    }
+    tile_fallback(h, Q, R, seg, seg_exit, seg_len, seg_next, segstart, nseg);
   }
   const int64_t launches = h.stats.launches;
   h.stats = before;
@@ -644,7 +682,22 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   h.stats.steps += rounds;
   h.stats.work += Rexp * rounds;
   h.timer.end(s);
-  return TileRank{seg, off, segstart};
+  return TileRank{seg, off, segstart, late};
+}
+
+bool tile_rank_settle(Handle& h, const LrParams& P, int64_t N, const TileRank& tr) {
+  if (!tr.deferred) return false;
+  const int64_t R = h.host_box[32];  // level-1 segment count (copied with the flag)
+  const bool overflow = *reinterpret_cast<const int*>(&h.host_box[32 + 16]) != 0;
+  h.tile_segments = R;
+  if (!overflow) return false;
+  const int64_t E = 2 * N;
+  LrParams Q = P;
+  Q.cap = std::max<int64_t>(P.cap, E + 1);
+  tile_fallback(h, Q, R, tr.seg, h.ws<uint32_t>(WS_RNEXT, E + 1), h.ws<uint32_t>(WS_RLEN, E + 1),
+                h.ws<uint32_t>(WS_RPOS, E + 1), const_cast<uint32_t*>(tr.segstart),
+                reinterpret_cast<unsigned long long*>(h.dev_box) + 8);
+  return true;
 }
 
 }  // namespace rstg

@@ -465,7 +465,11 @@ def test_tile_levels_overflow_fallback(rst, monkeypatch):
     out = {}
     for tag, knobs in (("walk", {"RSTG_LR_TILES": "0"}),
                        ("tiles", {"RSTG_LR_TILES": "1"}),
-                       ("overflow", {"RSTG_LR_TILES": "1", "RSTG_LR_TILECONTRACT": "1000000"})):
+                       ("overflow", {"RSTG_LR_TILES": "1", "RSTG_LR_TILECONTRACT": "1000000"}),
+                       # a repeated build sizes the levels from the previous
+                       # count; a short bound overflows and is settled after
+                       # the build (tile_rank_settle)
+                       ("shortbound", {"RSTG_LR_TILES": "1", "RSTG_LR_SEGBOUND": "20000"})):
         for k, v in knobs.items():
             monkeypatch.setenv(k, v)
         out[tag] = g.run(1, 7)[0]
@@ -473,6 +477,7 @@ def test_tile_levels_overflow_fallback(rst, monkeypatch):
             monkeypatch.delenv(k)
     assert np.array_equal(out["tiles"], out["walk"])
     assert np.array_equal(out["overflow"], out["walk"])
+    assert np.array_equal(out["shortbound"], out["walk"])
     g.close()
 
 

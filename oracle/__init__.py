@@ -352,6 +352,19 @@ def ref_run(g: Graph, algo: int, root: int = 0, workers: int = 1, jump_batch: in
     return parent, roots[: nr.value].copy(), (levels if algo == ALGO_BFS else None)
 
 
+def ref_validate(g: Graph, parent, roots, required_root=-1):
+    """The reference's validate_rooted_forest (validate.cpp:108-211):
+    (valid, first error message or "")."""
+    R = ref()
+    parent = np.ascontiguousarray(parent, dtype=I64)
+    roots = np.ascontiguousarray(roots, dtype=I64)
+    rc = R.ref_validate(ctypes.c_int64(g.n), ctypes.c_int64(g.m), _p(g.eu), _p(g.ev), _p(parent),
+                        _p(roots), ctypes.c_int64(len(roots)), ctypes.c_int64(required_root))
+    if rc < 0:
+        raise OracleError(_err(R, "ref_last_error"))
+    return rc == 1, _err(R, "ref_last_error")
+
+
 def ref_cc_spanning_forest(g: Graph, workers: int = 1):
     R = ref()
     labels = np.zeros(g.n, I64)

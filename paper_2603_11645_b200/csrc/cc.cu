@@ -419,6 +419,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
       if ((lp < 0 || lp >= cnt) && (threadIdx.x & 31) == __ffs(same) - 1) {
         // many vertices share one exit target (a big component's root):
         // a plain L2 read skips the atomic once the bit is set
+        // (batching these round trips across items measured slower: the
+        // extra registers spill at the 32-register cap of 2 x 1024 threads)
         const uint32_t bit = 1u << (p & 31);
         if (!(ld_cg(&xbits[p >> 5]) & bit) && !(atomicOr(&xbits[p >> 5], bit) & bit))
           app |= 1u << k;

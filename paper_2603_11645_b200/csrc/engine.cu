@@ -81,6 +81,10 @@ Handle::Handle(int dev) : device(dev) {
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   CK(cudaMallocHost(&host_box, 64 * sizeof(int64_t)));
   CK(cudaMalloc(&dev_box, 256 * sizeof(int64_t)));
+  // (defined contents: readbacks copy whole ranges of the box, some words of
+  // which a given path never writes)
+  memset(host_box, 0, 64 * sizeof(int64_t));
+  CK(cudaMemset(dev_box, 0, 256 * sizeof(int64_t)));
   bufs_.assign(WS_COUNT, {nullptr, 0});
 }
 

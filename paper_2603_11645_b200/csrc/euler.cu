@@ -111,19 +111,35 @@ __global__ void __launch_bounds__(kBlock)
     if (base >= n) break;
     uint32_t flags = 0;  // 2 bits per item: arc v, arc N + v; bit 16+k: label
     uint32_t h2[kFixItems];
+    // CC labels may be lazy (cc_exact with Euler): resolved here without a
+    // compression write-back (every later pass only tests lab[v] == v).
+    // The loads of all items go out together, level by level -- labels,
+    // their labels, then the rare deeper walks -- as do the remote heads:
+    // one item's chain at a time left this pass latency-bound.
+    int32_t lb[kFixItems];
 #pragma unroll
     for (int k = 0; k < kFixItems; ++k) {
       const int64_t v = base + k * kBlock + threadIdx.x;
-      // CC labels may be lazy (cc_exact with Euler): resolve
-      // (no compression write-back: every later pass only tests lab[v] == v)
-      const int32_t l = v < n ? (cc_slots ? find_root_ro(lab, (int32_t)v) : lab[v]) : -1;
+      lb[k] = v < n ? __ldcs(&lab[v]) : -1;
+      h2[k] = v < n ? __ldcs(&io.rhead[v]) : kNone32;
+    }
+    if (cc_slots) {
+      int32_t l2[kFixItems];
+#pragma unroll
+      for (int k = 0; k < kFixItems; ++k) l2[k] = lb[k] >= 0 ? lab[lb[k]] : -1;
+#pragma unroll
+      for (int k = 0; k < kFixItems; ++k)
+        if (l2[k] != lb[k]) lb[k] = find_root_ro(lab, l2[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kFixItems; ++k) {
+      const int64_t v = base + k * kBlock + threadIdx.x;
+      const int32_t l = lb[k];
       const unsigned peers = __match_any_sync(0xffffffffu, l);
-      h2[k] = kNone32;
       if (v >= n) continue;
       if ((threadIdx.x & 31) == __ffs(peers) - 1 && (uint32_t)v < minv[l])
         atomicMin(&minv[l], (uint32_t)v);  // the group's lowest lane has its smallest vertex
       if (present ? present[v] != 0 : l == (int32_t)v) flags |= 1u << (16 + k);
-      h2[k] = io.rhead[v];
       if (rulers && cc_slots && l != (int32_t)v) {
         if (lr_hash_ruler((uint32_t)v, logk)) flags |= 1u << (2 * k);
         if (lr_hash_ruler(io.nslots + (uint32_t)v, logk)) flags |= 2u << (2 * k);
@@ -132,21 +148,30 @@ __global__ void __launch_bounds__(kBlock)
     // Splices, their loads batched across the items (independent lists):
     // local tail -> remote head and remote tail -> local head, or the remote
     // list closed into a cycle of its own when there is no local list.
+    // (the splice loads of all items first: lists of distinct vertices)
+    uint32_t h1[kFixItems], t1[kFixItems], t2[kFixItems];
+#pragma unroll
+    for (int k = 0; k < kFixItems; ++k) {
+      const int64_t v = base + k * kBlock + threadIdx.x;
+      const bool sp = h2[k] != kNone32;
+      h1[k] = sp ? io.vhead[v] : kNone32;
+      t1[k] = sp ? io.vtail[v] : kNone32;
+      t2[k] = sp ? io.rtail[v] : kNone32;
+    }
 #pragma unroll
     for (int k = 0; k < kFixItems; ++k) {
       if (h2[k] == kNone32) continue;
       const int64_t v = base + k * kBlock + threadIdx.x;
-      const uint32_t h1 = io.vhead[v], t2 = io.rtail[v];
-      if (h1 != kNone32) {  // local tail -> remote head, remote tail -> local head
-        io.S[arc_rev(io.vtail[v], io.nslots)] = h2[k];
-        io.S[arc_rev(t2, io.nslots)] = h1;
+      if (h1[k] != kNone32) {  // local tail -> remote head, remote tail -> local head
+        io.S[arc_rev(t1[k], io.nslots)] = h2[k];
+        io.S[arc_rev(t2[k], io.nslots)] = h1[k];
       } else {
-        io.S[arc_rev(t2, io.nslots)] = h2[k];
+        io.S[arc_rev(t2[k], io.nslots)] = h2[k];
         io.vhead[v] = h2[k];
       }
       // the spliced cycle is (vhead .. t2): the root pass reads only
       // vhead/vtail, and the remote list is left empty for the next build
-      io.vtail[v] = t2;
+      io.vtail[v] = t2[k];
       io.rhead[v] = kNone32;
     }
     uint32_t id = rulers ? lr_block_claim(__popc(flags & 0xFFFFu), ctr) : 0u;
@@ -181,10 +206,10 @@ __global__ void k_fill_if_dirty(uint32_t* __restrict__ minv, int64_t n, const in
 // its rotation cycle opened just before its first arc (break_cycles
 // :96-101) and that first arc registered as the head ruler of its tour.
 __global__ void __launch_bounds__(kBlock)
-    k_euler_roots(const uint32_t* __restrict__ labels, const unsigned long long* nlabels,
+    k_euler_roots(uint32_t* __restrict__ labels, const unsigned long long* nlabels,
                   uint32_t* __restrict__ minv, EulerIO io, int32_t* parent, uint32_t* rpos,
                   uint32_t* sl, unsigned long long* ctr, int logk, int ob, uint32_t cap,
-                  bool rulers, int* minv_dirty) {
+                  bool rulers, int* minv_dirty, bool keep_roots) {
   const int64_t L = (int64_t)*nlabels;
   // few labels: reset their min entries here; many: leave them, flagged
   // for the fill before the next build (cheaper than a scattered reset)
@@ -198,6 +223,7 @@ __global__ void __launch_bounds__(kBlock)
       const uint32_t r = minv[labels[i]];
       if (reset) minv[labels[i]] = kNone32;
       parent[r] = (int32_t)r;
+      if (keep_roots) labels[i] = r;  // (the roots, for a deferred re-orientation)
       hd = io.vhead[r];  // the combined cycle (k_euler_fix spliced the remote list)
       if (hd != kNone32)
         io.S[arc_rev(io.vtail[r], io.nslots)] = kNone32;  // the tour ends back at the root
@@ -207,6 +233,15 @@ __global__ void __launch_bounds__(kBlock)
     const uint32_t id = lr_block_claim(head ? 1u : 0u, ctr);
     if (head) lr_put(id, hd, rpos, sl, ob, cap);
   }
+}
+
+// parent[r] = r again for the roots k_euler_roots kept in the label list.
+__global__ void k_reset_roots(const uint32_t* __restrict__ roots, const unsigned long long* count,
+                              int32_t* parent) {
+  const int64_t L = (int64_t)*count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L;
+       i += (int64_t)gridDim.x * blockDim.x)
+    parent[roots[i]] = (int32_t)roots[i];
 }
 
 // Hash-selected rulers of explicit slots [0, T) (all occupied).
@@ -381,7 +416,7 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   k_override_root<<<1, 32, 0, s>>>(labels, minv, designated_root, cc_slots);
   k_euler_roots<<<grid_for(n), kBlock, 0, s>>>(lablist, comps, minv, io, parent, rpos, sl, ctr,
                                                P.logk0, P.ob, (uint32_t)P.cap, !use_tiles,
-                                               minv_dirty);
+                                               minv_dirty, use_tiles);
   h.minv_clean = minv;
   h.minv_clean_n = n;
   if (!use_tiles && !cc_slots && T > 0)
@@ -412,8 +447,11 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
     h.stats.step(N);
     h.timer.end(s);
     if (tr.deferred)
-      h.late_check = [&h, P, N, tr, eto, parent] {
-        if (tile_rank_settle(h, P, N, tr)) {  // re-derive from the recomputed ranks
+      h.late_check = [&h, P, N, tr, eto, parent, lablist, comps] {
+        if (tile_rank_settle(h, P, N, tr)) {
+          // re-derive from the recomputed ranks: the roots first (the first
+          // orientation, on wrong ranks, may have given a root a parent)
+          k_reset_roots<<<grid_for(N), kBlock, 0, h.stream>>>(lablist, comps, parent);
           k_orient_tiles<<<grid_for(N), kBlock, 0, h.stream>>>(N, eto, tr.seg, tr.off, tr.segstart,
                                                                parent);
           CK_LAUNCH();

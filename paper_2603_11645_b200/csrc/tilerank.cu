@@ -170,7 +170,9 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
 #pragma unroll
     for (int q = 0; q < kBatch; ++q) {
       const uint32_t j = min(t0 + tid + ((q0 + q) >> 1) * kThreads, last);
-      y[q] = __ldcs(&S[((q0 + q) & 1) ? N + j : j]);
+      // (default caching, not evict-first: each segment tail re-reads its
+      // successor at the end of the tile, from L2)
+      y[q] = __ldg(&S[((q0 + q) & 1) ? N + j : j]);
     }
 #pragma unroll
     for (int q = 0; q < kBatch; ++q) word[local_of(q0 + q)] = y[q];
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
     __stcs(&off[x], (uint16_t)o);
     if (tmask >> q & 1) {
       seg_len[sid] = o + 1;
-      seg_exit[sid] = __ldg(&S[x]);  // the next segment's head (or NONE)
+      seg_exit[sid] = __ldg(&S[x]);  // the next segment's head (or NONE; L2: staged above)
     }
   }
   if (walked) {
@@ -433,7 +435,8 @@ __global__ void __launch_bounds__(kThreads, kNodes > 8192 ? 1 : 2048 / kThreads)
 
 // next segment of each segment: the one its exit arc heads
 __global__ void k_seg_link(const unsigned long long* nseg, const uint32_t* __restrict__ seg_exit,
-                           const uint32_t* __restrict__ seg, uint32_t* __restrict__ seg_next) {
+                           const uint32_t* __restrict__ S, const uint32_t* __restrict__ seg,
+                           uint32_t* __restrict__ seg_next) {
   const int64_t R = (int64_t)*nseg;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -443,9 +446,12 @@ __global__ void k_seg_link(const unsigned long long* nseg, const uint32_t* __res
 }
 
 // pre[i] = pre_up[seg[i]] + off[i] over the n_dev nodes of a level
+// (nothing when a level overflowed: counts may then exceed the arenas,
+// which are sized by the bounds; the caller falls back)
 __global__ void k_tile_expand(const unsigned long long* n_dev, const uint32_t* __restrict__ seg,
                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ pre_up,
-                              uint32_t* __restrict__ pre) {
+                              uint32_t* __restrict__ pre, const int* overflow) {
+  if (*overflow) return;
   const int64_t n = (int64_t)*n_dev;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -477,7 +483,7 @@ constexpr int kLevelThreads = 1024;
 // (the previous build's count plus a margin); nothing is read back here --
 // the counts and the overflow flag go to host_box[32..49) asynchronously
 // and the caller settles them after its final sync (tile_rank_settle).
-static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
+static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* S, const uint32_t* seg1,
                                const uint32_t* exit1, const uint32_t* len1, uint32_t* pre1,
                                bool dbg, bool deferred) {
   const cudaStream_t s = h.stream;
@@ -564,7 +570,7 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
   }
   for (int l = top - 1; l >= 0; --l) {
     k_tile_expand<<<grid_for(L[l].bound), kBlock, 0, s>>>(cnt + l, L[l].seg, L[l].off,
-                                                          L[l + 1].pre, L[l].pre);
+                                                          L[l + 1].pre, L[l].pre, overflow);
     CK_LAUNCH();
   }
   if (deferred) {
@@ -580,10 +586,11 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* seg1,
 }
 
 // The segments' ranks by the generic list ranking (levels that stall).
-static void tile_fallback(Handle& h, const LrParams& Q, int64_t R, const uint32_t* seg,
+static void tile_fallback(Handle& h, const LrParams& Q, int64_t R, const uint32_t* S,
+                          const uint32_t* seg,
                           const uint32_t* seg_exit, const uint32_t* seg_len, uint32_t* seg_next,
                           uint32_t* segstart, const unsigned long long* nseg) {
-  k_seg_link<<<grid_for(R), kBlock, 0, h.stream>>>(nseg, seg_exit, seg, seg_next);
+  k_seg_link<<<grid_for(R), kBlock, 0, h.stream>>>(nseg, seg_exit, S, seg, seg_next);
   CK_LAUNCH();
   list_prefix(h, Q, R, seg_next, seg_len, segstart, 0, false, nullptr);
 }
@@ -661,17 +668,17 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   const int levels_env = env_int("RSTG_LR_TILELEVELS", 1);  // (0: segments by list_prefix)
   bool late = false;
   if (levels_env && R * 4 <= E) {
-    if (tile_prefix_levels(h, R, seg, seg_exit, seg_len, segstart, dbg, deferred))
+    if (tile_prefix_levels(h, R, S, seg, seg_exit, seg_len, segstart, dbg, deferred))
       late = deferred;
     else
-      tile_fallback(h, Q, R, seg, seg_exit, seg_len, seg_next, segstart, nseg);
+      tile_fallback(h, Q, R, S, seg, seg_exit, seg_len, seg_next, segstart, nseg);
   } else {
     if (deferred) {  // (the exact count is needed here)
       h.read_box(h.dev_box + 8, 1);
       R = h.host_box[0];
       h.tile_segments = R;
     }
-    tile_fallback(h, Q, R, seg, seg_exit, seg_len, seg_next, segstart, nseg);
+    tile_fallback(h, Q, R, S, seg, seg_exit, seg_len, seg_next, segstart, nseg);
   }
   const int64_t launches = h.stats.launches;
   h.stats = before;
@@ -682,7 +689,7 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   h.stats.steps += rounds;
   h.stats.work += Rexp * rounds;
   h.timer.end(s);
-  return TileRank{seg, off, segstart, late};
+  return TileRank{seg, off, segstart, S, late};
 }
 
 bool tile_rank_settle(Handle& h, const LrParams& P, int64_t N, const TileRank& tr) {
@@ -694,7 +701,7 @@ bool tile_rank_settle(Handle& h, const LrParams& P, int64_t N, const TileRank& t
   const int64_t E = 2 * N;
   LrParams Q = P;
   Q.cap = std::max<int64_t>(P.cap, E + 1);
-  tile_fallback(h, Q, R, tr.seg, h.ws<uint32_t>(WS_RNEXT, E + 1), h.ws<uint32_t>(WS_RLEN, E + 1),
+  tile_fallback(h, Q, R, tr.S, tr.seg, h.ws<uint32_t>(WS_RNEXT, E + 1), h.ws<uint32_t>(WS_RLEN, E + 1),
                 h.ws<uint32_t>(WS_RPOS, E + 1), const_cast<uint32_t*>(tr.segstart),
                 reinterpret_cast<unsigned long long*>(h.dev_box) + 8);
   return true;

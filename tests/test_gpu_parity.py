@@ -218,6 +218,31 @@ def test_device_validator(rst, O):
     assert dg.validate(p, 8)[1] == 6
 
 
+@pytest.mark.parametrize("spec", [("grid", 9, 13), ("random", 300, 0.01), ("kron", 9),
+                                  ("road", 30)])
+def test_device_validator_vs_reference_corruptions(rst, O, spec):
+    # validate_rooted_forest (validate.cpp:108-211) of the reference itself
+    # on random corruptions: same verdict, same error class (first error),
+    # and for a non-edge parent the same (smallest) offending vertex
+    from test_oracle import corruptions, validation_class
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    g = O.gen(*spec) if spec[0] != "random" else O.ref_generate(f"random:{spec[1]}:{spec[2]}", 7)
+    dg = dev_graph(rst, g)
+    p = O.run(g, 1, 0)[0]
+    rs = np.random.RandomState(5)
+    for q in corruptions(g, p, rs, 80):
+        roots = np.flatnonzero(q == np.arange(g.n))
+        want_ok, want_msg = O.ref_validate(g, q, roots, 0)
+        ok, code, bad = dg.validate(q, 0)
+        assert ok == want_ok, (want_msg, code, bad)
+        if not ok:
+            assert code == validation_class(want_msg), (want_msg, code, bad)
+            if code == 2:
+                assert want_msg.startswith(f"parent edge ({bad}, "), (want_msg, bad)
+    dg.close()
+
+
 # ---- medium shapes -----------------------------------------------------------
 @pytest.mark.parametrize("spec,root", [(("grid", 1024, 1024), 0), (("road", 1000), 0),
                                         (("kron", 16), None), (("path", 1 << 18), 0)])

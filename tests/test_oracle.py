@@ -231,3 +231,60 @@ def test_same_partition_detects_differences(O):
     assert not O.same_partition(np.array([1, 1, 1, 3, 4]), root)   # merges two classes
     assert not O.same_partition(np.array([0, 1, 2, 2, 4]), root)   # splits a class
     assert not O.same_partition(np.array([0, 0, 2, 2, 9]), root)   # out of range
+
+
+def corruptions(g, parent, rs, count):
+    """Random corruptions of a valid forest: re-pointed parents (edges and
+    non-edges), 2-cycles, extra roots, roots removed."""
+    n = g.n
+    out = []
+    for _ in range(count):
+        p = parent.copy()
+        kind = rs.randint(0, 5)
+        v = int(rs.randint(0, n))
+        if kind == 0:  # any vertex
+            p[v] = int(rs.randint(0, n))
+        elif kind == 1:  # a neighbour (an edge: may close a cycle or stay valid)
+            nb = g.nbrs[g.offsets[v]:g.offsets[v + 1]]
+            if len(nb):
+                p[v] = int(nb[rs.randint(0, len(nb))])
+        elif kind == 2:  # 2-cycle on an edge
+            nb = g.nbrs[g.offsets[v]:g.offsets[v + 1]]
+            if len(nb):
+                u = int(nb[rs.randint(0, len(nb))])
+                p[v], p[u] = u, v
+        elif kind == 3:  # extra root
+            p[v] = v
+        else:  # a root removed (points at a neighbour)
+            roots = np.flatnonzero(p == np.arange(n))
+            r = int(roots[rs.randint(0, len(roots))])
+            nb = g.nbrs[g.offsets[r]:g.offsets[r + 1]]
+            if len(nb):
+                p[r] = int(nb[0])
+        out.append(p)
+    return out
+
+
+def validation_class(msg):
+    """The reference's first validation error -> the device validator's code."""
+    for key, code in (("is not a graph edge", 2), ("parent chain cycle", 3), ("has two roots", 4),
+                      ("roots but graph has", 4), ("reaches a root in a different", 5),
+                      ("was requested as root", 6)):
+        if key in msg:
+            return code
+    return -1
+
+
+@ref_needed
+@pytest.mark.parametrize("spec", [("grid", 9, 13), ("random", 300, 0.01), ("kron", 9)])
+def test_validate_restatement_vs_reference_corruptions(O, spec):
+    g = O.gen(*spec) if spec[0] != "random" else O.ref_generate(f"random:{spec[1]}:{spec[2]}", 7)
+    p, r, _ = O.run(g, 1, 0)
+    rs = np.random.RandomState(11)
+    for q in corruptions(g, p, rs, 60):
+        roots = np.flatnonzero(q == np.arange(g.n))
+        want = O.ref_validate(g, q, roots, 0)
+        got = O.validate(g, q, roots, 0)
+        assert got[0] == want[0], (want, got)
+        if not want[0]:
+            assert validation_class(got[1]) == validation_class(want[1]), (want, got)

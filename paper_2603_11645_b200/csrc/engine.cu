@@ -115,7 +115,7 @@ void* Handle::ws(int slot, size_t bytes) {
     if (slot == WS_MINV) minv_clean = nullptr;
     if (slot == WS_RHEAD) rhead_clean = nullptr;
     if (slot == WS_SLOT) slots_clean = nullptr;
-    if (slot == WS_PR_BYL || slot == WS_PR_CBASE) pr_levels_n = -1;
+    if (slot == WS_PR_BYL || slot == WS_PR_CBASE || slot == WS_PR_POS) pr_levels_n = -1;
     if (b.first) {
       CK(cudaStreamSynchronize(stream));
       CK(cudaFree(b.first));
@@ -132,7 +132,7 @@ void Handle::release(int slot) {
   if (slot == WS_MINV) minv_clean = nullptr;
   if (slot == WS_RHEAD) rhead_clean = nullptr;
   if (slot == WS_SLOT) slots_clean = nullptr;
-  if (slot == WS_PR_BYL || slot == WS_PR_CBASE) pr_levels_n = -1;
+  if (slot == WS_PR_BYL || slot == WS_PR_CBASE || slot == WS_PR_POS) pr_levels_n = -1;
   if (b.first) {
     CK(cudaStreamSynchronize(stream));
     CK(cudaFree(b.first));

@@ -202,10 +202,11 @@ enum WsSlot : int {
   // PR-RST
   WS_PR_SCRATCH,  // int32 n
   WS_PR_ONPATH,   // u8 n
-  WS_PR_FRESH,    // u8 n          skip level | root bit per vertex
+  WS_PR_FRESH,    // u8 n          skip level per vertex (built with the level order)
   WS_PR_GROOT,    // u8 n
   WS_PR_GU,       // u32 n         graft endpoints (marking seeds) of a round
-  WS_PR_ANC,      // int32 n*K     skip pointers, level-major (level k at (k-1)*n)
+  WS_PR_ANC,      // u32 ~2n       skip structure in position space (level k: C_k entries)
+  WS_PR_POS,      // u32 n         position of each vertex in the level order
   WS_PR_NEXT,     // u32 n         grafted roots of a round
   WS_PR_BYL,      // u32 n         vertices by descending skip level
   WS_PR_MK,       // u32 n         marked vertices, one queue per exact level

@@ -18,6 +18,13 @@
 //             ancestor of level >= k (or its tree root). Rebuilding level k
 //             walks ptr_{k-1} from the n/2^k vertices of level >= k,
 //             expected 2 hops each: O(n) work per round instead of O(n L).
+//             The structure lives in POSITION space: vertices sorted by
+//             descending level (ids ascending within a level), so level >= k
+//             is the prefix [0, C_k) and ptr_k is a dense array of C_k
+//             positions (level 0: the parent forest, n entries); a root
+//             points at itself. All levels take ~2n words (192 MB on road,
+//             not n x L = 2.4 GB), every level is written coalesced, and a
+//             walk at level k >= 3 stays inside an L2-resident array.
 //             Marking then touches only path vertices: an ascent from each
 //             endpoint climbs the levels (expected O(log n) hops) to the
 //             root, and a descent fills, level by level from the top, the
@@ -53,7 +60,6 @@ void launch_compress2(Handle& h, int32_t* rep, int64_t n);
 namespace {
 
 constexpr int kMaxLvl = 31;        // levels 0..K, K <= 31 (n < 2^31)
-constexpr uint8_t kRootBit = 0x80;  // lv[v]: level | root-of-its-tree bit
 
 // Device control block (u64 words in WS_BFS_CTRL).
 enum PrCtl : int {
@@ -74,16 +80,6 @@ __device__ __forceinline__ uint32_t vertex_level(uint32_t v, int K) {
   x ^= x >> 31;
   return min((uint32_t)__ffsll((long long)~x) - 1u, (uint32_t)K);  // trailing ones
 }
-__device__ __forceinline__ bool is_root(const uint8_t* lv, int32_t x) {
-  return (lv[x] & kRootBit) != 0;
-}
-__device__ __forceinline__ int lvl_of(const uint8_t* lv, int32_t x) { return lv[x] & 0x7F; }
-// ptr_k(x): k = 0 the parent, else the level-k skip pointer
-__device__ __forceinline__ int32_t up(const int32_t* parent, const int32_t* ptr, int64_t n, int k,
-                                      int32_t x) {
-  return k == 0 ? parent[x] : ptr[(int64_t)(k - 1) * n + x];
-}
-
 __global__ void k_pr_init(int64_t n, int K, int32_t* parent, int32_t* rep, int32_t* scratch,
                           uint8_t* mark, uint8_t* lv, unsigned long long* slot,
                           unsigned long long* hist) {
@@ -96,9 +92,11 @@ __global__ void k_pr_init(int64_t n, int K, int32_t* parent, int32_t* rep, int32
     scratch[v] = -1;
     mark[v] = 0;
     slot[v] = kKeyInf;
-    const uint32_t l = vertex_level((uint32_t)v, K);
-    lv[v] = (uint8_t)l | kRootBit;  // every vertex starts as its own tree
-    if (hist) atomicAdd(&s_h[l], 1u);
+    if (hist) {  // (the level order is being built: levels and their histogram)
+      const uint32_t l = vertex_level((uint32_t)v, K);
+      lv[v] = (uint8_t)l;
+      atomicAdd(&s_h[l], 1u);
+    }
   }
   __syncthreads();
   if (hist)
@@ -113,56 +111,90 @@ __global__ void k_pr_level_keys(int64_t n, int K, const uint8_t* __restrict__ lv
                                 uint32_t* ids) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    keys[v] = (uint32_t)(K - (lv[v] & 0x7F));
+    keys[v] = (uint32_t)(K - lv[v]);
     ids[v] = (uint32_t)v;
   }
 }
 
-// Level-k skip pointers (k >= 1) of the vertices of level >= k.
+// The level structure in position space (passed by value): C[k] = number
+// of positions of level >= k (C[0] = n, C[K + 1] = 0); the level-k array
+// (k = 0: parents) starts at off[k] of one buffer Q and covers [0, C[k]).
+struct PrLv {
+  uint32_t C[kMaxLvl + 2];
+  unsigned long long off[kMaxLvl + 2];
+  int K;
+};
+// level of position x (C in shared memory): levels are small (mean 1)
+__device__ __forceinline__ int level_of_pos(const uint32_t* sC, int K, uint32_t x) {
+  int l = 0;
+  while (l < K && x < sC[l + 1]) ++l;
+  return l;
+}
+
+// pos[byl[i]] = i (once per graph size, with the level order)
+__global__ void k_pr_pos(int64_t n, const uint32_t* __restrict__ byl, uint32_t* __restrict__ pos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    pos[byl[i]] = (uint32_t)i;
+}
+
+// Level 0 of the structure: the parent forest in positions (a root points
+// at itself), Q0[i] = pos[parent[byl[i]]].
+__global__ void __launch_bounds__(kBlock)
+    k_pr_q0(int64_t n, const uint32_t* __restrict__ byl, const int32_t* __restrict__ parent,
+            const uint32_t* __restrict__ pos, uint32_t* __restrict__ q0) {
+  constexpr int kB = 4;  // four gathers in flight per thread
+  const int64_t g = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += kB * g) {
+    uint32_t p[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) p[j] = i0 + j * g < n ? (uint32_t)parent[byl[i0 + j * g]] : 0u;
+#pragma unroll
+    for (int j = 0; j < kB; ++j)
+      if (i0 + j * g < n) q0[i0 + j * g] = pos[p[j]];
+  }
+}
+
+// Level k >= 1 for the positions [0, C[k]): walk the level-(k-1) pointers
+// to the first position of level >= k, or to the tree root (a position at
+// or past C[k-1] can only be a root: non-roots reached at level k-1 have
+// level >= k-1; a root of level k-1 points at itself).
 template <int kB>
 __global__ void __launch_bounds__(kBlock)
-    k_pr_rebuild(int64_t count, int k, int64_t n, const uint32_t* __restrict__ byl,
-                 const int32_t* __restrict__ parent, const uint8_t* __restrict__ lv, int32_t* ptr) {
-  const int32_t* __restrict__ below = k == 1 ? parent : ptr + (int64_t)(k - 2) * n;
-  int32_t* __restrict__ out = ptr + (int64_t)(k - 1) * n;
+    k_pr_rebuild(int k, PrLv L, uint32_t* __restrict__ Q) {
+  const uint32_t* __restrict__ in = Q + L.off[k - 1];
+  uint32_t* __restrict__ out = Q + L.off[k];
+  const uint32_t cnt = L.C[k], lo = L.C[k], hi = L.C[k - 1];
   const int64_t g = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < count; i0 += kB * g) {
-    int32_t v[kB], x[kB];
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < cnt; i0 += kB * g) {
+    uint32_t x[kB];
     bool walk[kB];
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
       const int64_t i = i0 + j * g;
-      walk[j] = i < count;
-      v[j] = walk[j] ? (int32_t)byl[i] : 0;
+      x[j] = i < cnt ? in[i] : 0u;
+      walk[j] = i < cnt;
     }
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      if (walk[j] && is_root(lv, v[j])) {
-        x[j] = v[j];
-        walk[j] = false;
-      } else {
-        x[j] = walk[j] ? below[v[j]] : 0;
-      }
-    }
-    // walks of kB vertices advance together (their loads in flight at once)
+    // the walks of kB positions advance together (their loads in flight at once)
     for (;;) {
       bool any = false;
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         if (!walk[j]) continue;
-        const uint8_t l = lv[x[j]];
-        if ((l & kRootBit) || (l & 0x7F) >= k) {
+        if (x[j] < lo || x[j] >= hi) {
           walk[j] = false;
-        } else {
-          x[j] = below[x[j]];
-          any = true;
+          continue;
         }
+        const uint32_t y = in[x[j]];
+        if (y == x[j]) walk[j] = false;
+        else x[j] = y;
+        any = true;
       }
       if (!any) break;
     }
 #pragma unroll
     for (int j = 0; j < kB; ++j)
-      if (i0 + j * g < count) out[v[j]] = x[j];
+      if (i0 + j * g < cnt) out[i0 + j * g] = x[j];
   }
 }
 
@@ -256,41 +288,49 @@ __global__ void __launch_bounds__(kBlock)
 // (starting at lvl(u)) follow ptr_k; a vertex of a higher level lifts the
 // climb to that level. Every vertex passed is on the path: marked and
 // queued by its exact level. Seeds themselves are queued first, block-
-// aggregated (round 0 has ~n/2 seeds, all singleton roots).
+// aggregated (round 0 has ~n/2 seeds, all singleton roots: `identity`,
+// the forest before any reversal, needs no climb). Positions throughout;
+// the vertex id (byl) is looked up only to mark and queue.
 __global__ void __launch_bounds__(kBlock)
-    k_pr_ascend(const uint32_t* __restrict__ seeds, const unsigned long long* nseeds, int64_t n,
-                const int32_t* __restrict__ parent, const int32_t* __restrict__ ptr,
-                const uint8_t* __restrict__ lv, uint8_t* mark, uint32_t* mk,
+    k_pr_ascend(const uint32_t* __restrict__ seeds, const unsigned long long* nseeds,
+                const uint32_t* __restrict__ Q, PrLv L, const uint32_t* __restrict__ byl,
+                const uint32_t* __restrict__ pos, bool identity, uint8_t* mark, uint32_t* mk,
                 const unsigned long long* __restrict__ bbase, unsigned long long* mcnt) {
   __shared__ unsigned int s_c[kMaxLvl + 1];
   __shared__ unsigned long long s_b[kMaxLvl + 1];
+  __shared__ uint32_t sC[kMaxLvl + 2];
+  for (int i = threadIdx.x; i < kMaxLvl + 2; i += blockDim.x) sC[i] = L.C[i];
+  const int K = L.K;
   const int64_t S = (int64_t)*nseeds;
   for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < S; b0 += (int64_t)gridDim.x * blockDim.x) {
     for (int i = threadIdx.x; i <= kMaxLvl; i += blockDim.x) s_c[i] = 0;
     __syncthreads();
     const int64_t i = b0 + threadIdx.x;
     int32_t u = -1;
+    uint32_t c = 0;
     int l = 0;
-    unsigned pos = 0;
+    unsigned slot = 0;
     if (i < S) {
       u = (int32_t)seeds[i];
-      l = lvl_of(lv, u);
-      pos = atomicAdd(&s_c[l], 1u);
+      c = pos[u];
+      l = level_of_pos(sC, K, c);
+      slot = atomicAdd(&s_c[l], 1u);
     }
     __syncthreads();
     for (int j = threadIdx.x; j <= kMaxLvl; j += blockDim.x)
       s_b[j] = s_c[j] ? atomicAdd(&mcnt[j], (unsigned long long)s_c[j]) : 0ull;
     __syncthreads();
     if (u >= 0) {
-      mk[bbase[l] + s_b[l] + pos] = (uint32_t)u;
-      int32_t c = u;
+      mk[bbase[l] + s_b[l] + slot] = (uint32_t)u;
       int k = l;
-      while (!is_root(lv, c)) {
-        const int32_t x = up(parent, ptr, n, k, c);
-        mark[x] = 1;
-        const int lx = lvl_of(lv, x);
-        enqueue(mk, bbase, mcnt, lx, x);
-        if (is_root(lv, x)) break;
+      while (!identity) {
+        const uint32_t x = Q[L.off[k] + c];  // ptr_k(c): c has level >= k
+        if (x == c) break;                    // c is its tree's root
+        const uint32_t vx = byl[x];
+        mark[vx] = 1;
+        const int lx = level_of_pos(sC, K, x);
+        enqueue(mk, bbase, mcnt, lx, (int32_t)vx);
+        if (x >= sC[k]) break;  // below level k: only the root is reached that way
         if (lx > k) k = lx;
         c = x;
       }
@@ -303,23 +343,27 @@ __global__ void __launch_bounds__(kBlock)
 // ptr_j up to the next vertex of level > j (or the root), marking the
 // level-j vertices of that gap (queued into bucket j, not read here).
 __global__ void __launch_bounds__(kBlock)
-    k_pr_descend(int j, int K, int64_t n, const int32_t* __restrict__ parent,
-                 const int32_t* __restrict__ ptr, const uint8_t* __restrict__ lv, uint8_t* mark,
-                 uint32_t* mk, const unsigned long long* __restrict__ bbase,
-                 unsigned long long* mcnt) {
+    k_pr_descend(int j, const uint32_t* __restrict__ Q, PrLv L, const uint32_t* __restrict__ byl,
+                 const uint32_t* __restrict__ pos, uint8_t* mark, uint32_t* mk,
+                 const unsigned long long* __restrict__ bbase, unsigned long long* mcnt) {
   const int b = j + 1 + (int)blockIdx.y;  // this block row's bucket (level b > j)
-  if (b > K) return;
+  if (b > L.K) return;
   const int64_t T = (int64_t)mcnt[b];
   const uint32_t* q = mk + bbase[b];
+  const uint32_t* __restrict__ in = Q + L.off[j];
+  const uint32_t lo = L.C[j + 1], hi = L.C[j];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t a = (int32_t)q[i];
-    if (is_root(lv, a)) continue;
-    int32_t x = up(parent, ptr, n, j, a);
-    while (!is_root(lv, x) && lvl_of(lv, x) == j) {
-      mark[x] = 1;
-      enqueue(mk, bbase, mcnt, j, x);
-      x = up(parent, ptr, n, j, x);
+    const uint32_t pa = pos[q[i]];
+    uint32_t x = in[pa];
+    if (x == pa) continue;  // a root
+    while (x >= lo && x < hi) {  // level exactly j (past hi: a lower root)
+      const uint32_t y = in[x];
+      if (y == x) break;  // the root (the ascent marked it)
+      const uint32_t vx = byl[x];
+      mark[vx] = 1;
+      enqueue(mk, bbase, mcnt, j, (int32_t)vx);
+      x = y;
     }
   }
 }
@@ -374,15 +418,6 @@ __global__ void k_pr_reverse_b(const uint32_t* mk, const unsigned long long* bba
   }
   block_flag(bad, bad_rev);
 }
-// Grafted roots are roots no more (their tree hangs off the winner's now).
-__global__ void k_pr_unroot(const uint32_t* __restrict__ grafted, const unsigned long long* ngraft,
-                            uint8_t* lv) {
-  const int64_t G = (int64_t)*ngraft;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < G;
-       i += (int64_t)gridDim.x * blockDim.x)
-    lv[grafted[i]] &= (uint8_t)~kRootBit;
-}
-
 __global__ void k_set_i32(int32_t* p, int32_t v) { *p = v; }
 __global__ void k_set_u8(uint8_t* p, uint8_t v) { *p = v; }
 __global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
@@ -411,7 +446,10 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   uint32_t* grafted = h.ws<uint32_t>(WS_PR_NEXT, n + 1);
   uint32_t* byl = h.ws<uint32_t>(WS_PR_BYL, n + 1);
   uint32_t* mk = h.ws<uint32_t>(WS_PR_MK, n + 1);
-  int32_t* ptr = h.ws<int32_t>(WS_PR_ANC, (size_t)n * K);
+  // the skip structure in position space: level k (k = 0: parents) at
+  // off[k], C[k] entries; sum_k C[k] < 2n + K
+  uint32_t* Q = h.ws<uint32_t>(WS_PR_ANC, 2 * (size_t)n + kMaxLvl + 2);
+  uint32_t* pos = h.ws<uint32_t>(WS_PR_POS, n + 1);
   uint32_t* rlist = h.ws<uint32_t>(WS_CCROOTS, 3 * n + 3);
   uint32_t* rl[2] = {rlist, rlist + n + 1};
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
@@ -461,26 +499,48 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
       void* tmp = h.ws(WS_SL, temp);
       CK(cub::DeviceRadixSort::SortPairs(tmp, temp, keys, keys + n, ids, byl, (int)n, 0, bits, s));
     }
+    if (n > 0) {
+      k_pr_pos<<<g, kBlock, 0, s>>>(n, byl, pos);
+      CK_LAUNCH();
+    }
     CK(cudaStreamSynchronize(s));
     h.pr_levels_C = C;
     h.pr_levels_n = n;
     h.pr_levels_byl = byl;
   }
   const std::vector<int64_t>& C = h.pr_levels_C;
+  PrLv L{};
+  L.K = K;
+  {
+    unsigned long long o = 0;
+    for (int k = 0; k <= K + 1; ++k) {
+      L.C[k] = (uint32_t)C[k];
+      L.off[k] = o;
+      o += (unsigned long long)C[k];
+    }
+  }
   CK(cudaMemcpyAsync(bbase, cbase, (kMaxLvl + 2) * sizeof(unsigned long long),
                      cudaMemcpyDeviceToDevice, s));
   h.stats.step(n, 3);
   h.timer.end(s);
 
-  bool forest_dirty = false;  // the skip pointers lag the parent forest
+  // the skip structure lags the parent forest after a reversal; before the
+  // first one the forest is the identity (every vertex its own root): the
+  // first marking needs no structure at all
+  bool forest_dirty = false, identity = true;
   auto rebuild = [&]() {
     h.timer.begin(s, "pr.rebuild", 0.0);
-    double bytes = 0;
+    // level 0: per position its id and parent (4 + 4 B), the parent's
+    // position (4 B), the entry out (4 B)
+    double bytes = 16.0 * n;
+    k_pr_q0<<<grid_for(n), kBlock, 0, s>>>(n, byl, parent, pos, Q);
+    h.stats.step(n);
     for (int k = 1; k <= K && C[k] > 0; ++k) {
-      // per vertex of level >= k: its id, ~2 hops (pointer + level byte), the pointer out
-      bytes += (double)C[k] * (4.0 + 2.0 * 5.0 + 4.0);
+      // per position of level >= k: the level-(k-1) entry in (4 B), ~1 more
+      // hop (4 B), the entry out (4 B)
+      bytes += (double)C[k] * 12.0;
       (n > (int64_t{1} << 22) ? k_pr_rebuild<4> : k_pr_rebuild<1>)
-          <<<grid_for(C[k]), kBlock, 0, s>>>(C[k], k, n, byl, parent, lv, ptr);
+          <<<grid_for(C[k]), kBlock, 0, s>>>(k, L, Q);
       h.stats.step(C[k]);
     }
     CK_LAUNCH();
@@ -493,18 +553,18 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     if (forest_dirty) rebuild();
     h.timer.begin(s, "pr.mark", 0.0);
     CK(cudaMemsetAsync(mcnt, 0, (kMaxLvl + 2) * sizeof(unsigned long long), s));
-    k_pr_ascend<<<g, kBlock, 0, s>>>(seeds, pc + P_NGRAFT, n, parent, ptr, lv, mark, mk, bbase,
-                                     mcnt);
+    k_pr_ascend<<<g, kBlock, 0, s>>>(seeds, pc + P_NGRAFT, Q, L, byl, pos, identity, mark, mk,
+                                     bbase, mcnt);
     h.stats.step(n);
     // level-j walkers are the queues of levels > j: one block row each,
     // sized by the expected queue (n / 2^(b+1) path vertices at most)
-    for (int j = K - 1; j >= 0; --j) {
-      const int64_t expect = std::max<int64_t>(C[j + 1] - C[j + 2], 1);
-      const unsigned gx = std::min<unsigned>(grid_for(expect), 2 * (unsigned)num_sms());
-      k_pr_descend<<<dim3(gx, K - j), kBlock, 0, s>>>(j, K, n, parent, ptr, lv, mark, mk, bbase,
-                                                      mcnt);
-      h.stats.step(n);
-    }
+    if (!identity)
+      for (int j = K - 1; j >= 0; --j) {
+        const int64_t expect = std::max<int64_t>(C[j + 1] - C[j + 2], 1);
+        const unsigned gx = std::min<unsigned>(grid_for(expect), 2 * (unsigned)num_sms());
+        k_pr_descend<<<dim3(gx, K - j), kBlock, 0, s>>>(j, Q, L, byl, pos, mark, mk, bbase, mcnt);
+        h.stats.step(n);
+      }
     CK_LAUNCH();
     h.timer.end(s);
   };
@@ -516,6 +576,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     h.stats.step(n);
     h.stats.step(n);
     forest_dirty = true;
+    identity = false;
   };
 
   // batched_jump's guard (pr_rst.cpp:218-219) fires only once a graft happened.
@@ -566,7 +627,6 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
                                                    bad_mark);
     h.stats.step(n);
     run_reverse();
-    k_pr_unroot<<<grid_for(nroots), kBlock, 0, s>>>(grafted, pc + P_NGRAFT, lv);
     CK_LAUNCH();
     h.timer.end(s);
 

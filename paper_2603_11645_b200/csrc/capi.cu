@@ -150,6 +150,7 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
   check_root(h, root);
   h.stats = Stats{};
   h.late_check = nullptr;
+  h.late_copy = {};
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));

@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
 // launch. flags: 3 rotating "changed" words (zeroed before the launch).
 __global__ void __launch_bounds__(kBlock)
     k_jump_x(const uint32_t* __restrict__ list, const unsigned long long* xcount, int32_t* rep,
-             int* flags, int max_rounds) {
+             int* flags, int max_rounds, uint32_t* xbits) {
   cg::grid_group grid = cg::this_grid();
   const int64_t X = (int64_t)*xcount;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -461,6 +461,9 @@ __global__ void __launch_bounds__(kBlock)
         const int64_t i = i0 + k * gsize;
         live[k] = i < X;
         v[k] = live[k] ? list[i] : 0u;
+        // the exit-set bitmap holds exactly the listed entries' bits: the
+        // first round clears them, so it is all-zero for the next pass
+        if (xbits && r == 0 && live[k]) xbits[v[k] >> 5] = 0u;
       }
 #pragma unroll
       for (int k = 0; k < kJumpBatch; ++k) p[k] = live[k] ? ld_cg(&rep[v[k]]) : 0;
@@ -543,7 +546,11 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
   {
     ZeroRanges z = extra ? *extra : ZeroRanges{};
     if (!extra) z.k = 0;
-    z.add(xbits, (size_t)words * sizeof(uint32_t));
+    // (the bitmap is all-zero after a completed pass: its exit-set jump
+    // clears the bits it set)
+    if (h.xbits_clean != xbits || words > h.xbits_clean_words)
+      z.add(xbits, (size_t)words * sizeof(uint32_t));
+    h.xbits_clean = nullptr;
     z.add(h.dev_box + 5, 3 * sizeof(int64_t));
     k_zero_ranges<<<(unsigned)std::min<int64_t>(1184, (words + 1023) / 1024 + 1), 1024, 0,
                     h.stream>>>(z);
@@ -577,9 +584,12 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
   int rounds = 2;
   while ((int64_t{1} << (rounds - 2)) < n) ++rounds;  // X-forest depth <= |X| <= n
   const unsigned long long* xc = xcount;
-  void* args[] = {(void*)&xlist, (void*)&xc, (void*)&rep, (void*)&flags, (void*)&rounds};
+  void* args[] = {(void*)&xlist, (void*)&xc, (void*)&rep, (void*)&flags, (void*)&rounds,
+                  (void*)&xbits};
   CK(cudaLaunchCooperativeKernel((void*)k_jump_x, dim3(coop_blocks), dim3(kBlock), args, 0,
                                  h.stream));
+  h.xbits_clean = xbits;
+  h.xbits_clean_words = words;
   h.stats.step(n);
   k_final_gather<<<grid_for(n), kBlock, 0, h.stream>>>(n, rep);
   CK_LAUNCH();
@@ -686,7 +696,9 @@ void jump_list(Handle& h, int32_t* rep, int64_t n, const uint32_t* list,
   }
   int rounds = 2;
   while ((int64_t{1} << (rounds - 2)) < n) ++rounds;
-  void* args[] = {(void*)&list, (void*)&count, (void*)&rep, (void*)&flags, (void*)&rounds};
+  uint32_t* no_bits = nullptr;
+  void* args[] = {(void*)&list, (void*)&count, (void*)&rep, (void*)&flags, (void*)&rounds,
+                  (void*)&no_bits};
   CK(cudaLaunchCooperativeKernel((void*)k_jump_x, dim3(coop_blocks), dim3(kBlock), args, 0,
                                  h.stream));
   h.stats.step(n);
@@ -708,7 +720,9 @@ void compress_via_roots(Handle& h, int32_t* rep, int64_t n, const uint32_t* root
   }
   int rounds = 2;
   while ((int64_t{1} << (rounds - 2)) < n) ++rounds;
-  void* args[] = {(void*)&roots, (void*)&nroots, (void*)&rep, (void*)&flags, (void*)&rounds};
+  uint32_t* no_bits = nullptr;
+  void* args[] = {(void*)&roots, (void*)&nroots, (void*)&rep, (void*)&flags, (void*)&rounds,
+                  (void*)&no_bits};
   CK(cudaLaunchCooperativeKernel((void*)k_jump_x, dim3(coop_blocks), dim3(kBlock), args, 0,
                                  h.stream));
   h.stats.step(n);

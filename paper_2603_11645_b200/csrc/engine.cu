@@ -114,6 +114,7 @@ void* Handle::ws(int slot, size_t bytes) {
     // a new buffer (possibly at the old address) holds nothing known
     if (slot == WS_MINV) minv_clean = nullptr;
     if (slot == WS_RHEAD) rhead_clean = nullptr;
+    if (slot == WS_XBITS) xbits_clean = nullptr;
     if (slot == WS_SLOT) slots_clean = nullptr;
     if (slot == WS_PR_BYL || slot == WS_PR_CBASE || slot == WS_PR_POS) pr_levels_n = -1;
     if (b.first) {
@@ -131,6 +132,7 @@ void Handle::release(int slot) {
   auto& b = bufs_[slot];
   if (slot == WS_MINV) minv_clean = nullptr;
   if (slot == WS_RHEAD) rhead_clean = nullptr;
+  if (slot == WS_XBITS) xbits_clean = nullptr;
   if (slot == WS_SLOT) slots_clean = nullptr;
   if (slot == WS_PR_BYL || slot == WS_PR_CBASE || slot == WS_PR_POS) pr_levels_n = -1;
   if (b.first) {

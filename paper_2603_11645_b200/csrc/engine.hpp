@@ -126,6 +126,13 @@ class Handle {
   // ranking's overflow flag, copied asynchronously into host_box[32..]):
   // run by run_late_checks() before anything reads the outputs.
   std::function<void()> late_check;
+  // the device words the late check reads (copied to host_box[32..]
+  // asynchronously once the last kernel that does not depend on them is
+  // enqueued, so the copy does not delay it)
+  struct {
+    const void* src = nullptr;
+    int words = 0;
+  } late_copy;
   // WS_MINV holds all-ones left by the Euler root pass (its other users --
   // BFS, validation, degree counts -- clear this when they take the buffer).
   const void* minv_clean = nullptr;
@@ -134,6 +141,10 @@ class Handle {
   // remote list it splices), so a build needs no 4n-byte fill
   const void* rhead_clean = nullptr;
   int64_t rhead_clean_n = 0;
+  // WS_XBITS (the exit-set bitmap of the two-level shortcutting) is all-zero
+  // after a completed pass: the exit-set jump clears what the tiles set
+  const void* xbits_clean = nullptr;
+  int64_t xbits_clean_words = 0;
   // PR-RST skip levels (pr.cu): vertex order by level and the counts C_k
   // of vertices of level >= k, valid for graphs of pr_levels_n vertices
   int64_t pr_levels_n = -1;

@@ -194,7 +194,10 @@ constexpr int64_t kResetMax = 1 << 16;
 
 // The min table between builds: all-ones, or flagged dirty by the root pass
 // (many components: it skipped the reset) and filled here.
-__global__ void k_fill_if_dirty(uint32_t* __restrict__ minv, int64_t n, const int* dirty) {
+__global__ void k_fill_if_dirty(uint32_t* __restrict__ minv, int64_t n, const int* dirty,
+                                unsigned long long* box) {
+  // (and the pass's counters: dev_box [4] labels, [8] ruler ids, [13] tiles)
+  if (blockIdx.x == 0 && threadIdx.x < 3) box[threadIdx.x == 0 ? 4 : threadIdx.x == 1 ? 8 : 13] = 0;
   if (!*dirty) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -389,13 +392,14 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   if (h.minv_clean != minv || n > h.minv_clean_n) {
     CK(cudaMemsetAsync(minv, 0xFF, n * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(minv_dirty, 0, sizeof(int), s));
-  } else {
-    k_fill_if_dirty<<<grid_for(n), kBlock, 0, s>>>(minv, n, minv_dirty);
+    CK(cudaMemsetAsync(h.dev_box + 4, 0, sizeof(int64_t), s));
+    CK(cudaMemsetAsync(h.dev_box + 8, 0, sizeof(int64_t), s));
+    CK(cudaMemsetAsync(h.dev_box + 13, 0, sizeof(int64_t), s));
+  } else {  // (the counters are zeroed by the same launch)
+    k_fill_if_dirty<<<grid_for(n), kBlock, 0, s>>>(minv, n, minv_dirty,
+                                                   reinterpret_cast<unsigned long long*>(h.dev_box));
   }
   h.minv_clean = nullptr;  // (until the root pass below has run)
-  CK(cudaMemsetAsync(h.dev_box + 4, 0, sizeof(int64_t), s));
-  CK(cudaMemsetAsync(h.dev_box + 8, 0, sizeof(int64_t), s));
-  CK(cudaMemsetAsync(h.dev_box + 13, 0, sizeof(int64_t), s));
   uint8_t* present = nullptr;
   if (!cc_slots) {
     present = h.ws<uint8_t>(WS_ISROOT, n);
@@ -446,6 +450,11 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
     CK_LAUNCH();
     h.stats.step(N);
     h.timer.end(s);
+    if (h.late_copy.src) {
+      CK(cudaMemcpyAsync(h.host_box + 32, h.late_copy.src, h.late_copy.words * sizeof(int64_t),
+                         cudaMemcpyDeviceToHost, s));
+      h.late_copy = {};
+    }
     if (tr.deferred)
       h.late_check = [&h, P, N, tr, eto, parent, lablist, comps] {
         if (tile_rank_settle(h, P, N, tr)) {

@@ -446,9 +446,6 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   uint32_t* grafted = h.ws<uint32_t>(WS_PR_NEXT, n + 1);
   uint32_t* byl = h.ws<uint32_t>(WS_PR_BYL, n + 1);
   uint32_t* mk = h.ws<uint32_t>(WS_PR_MK, n + 1);
-  // the skip structure in position space: level k (k = 0: parents) at
-  // off[k], C[k] entries; sum_k C[k] < 2n + K
-  uint32_t* Q = h.ws<uint32_t>(WS_PR_ANC, 2 * (size_t)n + kMaxLvl + 2);
   uint32_t* pos = h.ws<uint32_t>(WS_PR_POS, n + 1);
   uint32_t* rlist = h.ws<uint32_t>(WS_CCROOTS, 3 * n + 3);
   uint32_t* rl[2] = {rlist, rlist + n + 1};
@@ -519,6 +516,10 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
       o += (unsigned long long)C[k];
     }
   }
+  // the skip structure in position space: level k (k = 0: parents) at
+  // off[k], C[k] entries -- sum_k C[k] = n + the sum of the levels, about
+  // 2n (sized exactly: the sum is random)
+  uint32_t* Q = h.ws<uint32_t>(WS_PR_ANC, (size_t)L.off[K + 1] + 1);
   CK(cudaMemcpyAsync(bbase, cbase, (kMaxLvl + 2) * sizeof(unsigned long long),
                      cudaMemcpyDeviceToDevice, s));
   h.stats.step(n, 3);

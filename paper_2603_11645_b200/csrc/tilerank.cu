@@ -574,7 +574,7 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* S, const ui
     CK_LAUNCH();
   }
   if (deferred) {
-    CK(cudaMemcpyAsync(h.host_box + 32, blk, 17 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    h.late_copy = {blk, 17};  // (enqueued by the caller after the orientation)
     return true;
   }
   h.read_box(reinterpret_cast<int64_t*>(blk), 17);  // counts, overflow

@@ -223,6 +223,78 @@ struct RoundIO {
   bool edge_sentinel;           // round-0 slots carry kKeyEdge (empty = isolated)
 };
 
+// Run shortcut before the in-tile doubling: a vertex whose pointer is its
+// left neighbour (p = v - 1, inside the tile) continues that neighbour's
+// run. One block-wide max-scan over the tile (blocked layout: a thread owns
+// kTileV / kTileThreads consecutive vertices) gives every vertex the first
+// vertex h of its run, and s[v] = s[h] jumps the whole run at once (h keeps
+// its pointer, so no entry is read while it is written). Locally numbered
+// graphs chain along runs (a mesh row, a path): the doubling then only has
+// the runs' heads left -- two or three rounds instead of ~log2(row). A tile
+// with few such pointers (power-law graphs) skips it after one barrier.
+__device__ __forceinline__ void run_shortcut(int32_t* s, int64_t base, int cnt) {
+  constexpr int kB = kTileV / kTileThreads;
+  static_assert(kB == 8, "blocked layout: 8 vertices per thread");
+  __shared__ int s_wmax[kTileThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int i0 = t * kB;
+  int32_t pv[kB];
+  {
+    const int4 a = reinterpret_cast<const int4*>(s)[2 * t];
+    const int4 b = reinterpret_cast<const int4*>(s)[2 * t + 1];
+    pv[0] = a.x; pv[1] = a.y; pv[2] = a.z; pv[3] = a.w;
+    pv[4] = b.x; pv[5] = b.y; pv[6] = b.z; pv[7] = b.w;
+  }
+  uint32_t left = 0;
+#pragma unroll
+  for (int j = 0; j < kB; ++j) {
+    const int i = i0 + j;
+    if (i > 0 && i < cnt && (int64_t)pv[j] == base + i - 1) left |= 1u << j;
+  }
+  if (__syncthreads_count(__popc(left)) < kTileV / 8) return;  // (block-uniform)
+  // inclusive max-scan of "run start" indices: a non-left vertex starts a run
+  int key[kB];
+  int m = -1;
+#pragma unroll
+  for (int j = 0; j < kB; ++j) {
+    if (!(left >> j & 1)) m = i0 + j;
+    key[j] = m;
+  }
+  int incl = m;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = max(incl, y);
+  }
+  int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = -1;
+  if (lane == 31) s_wmax[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s_wmax[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w = max(w, y);
+    }
+    const int we = __shfl_up_sync(0xffffffffu, w, 1);
+    s_wmax[lane] = lane == 0 ? -1 : we;  // (exclusive over the warps)
+  }
+  __syncthreads();
+  const int prefix = max(excl, s_wmax[warp]);
+#pragma unroll
+  for (int j = 0; j < kB; ++j) {
+    if (!(left >> j & 1)) continue;
+    const int h = key[j] >= 0 ? key[j] : prefix;  // (a left vertex always has a start before it)
+    pv[j] = s[h];                                  // the run start's own pointer
+  }
+  __syncthreads();  // (every read of a run start done before the writes)
+#pragma unroll
+  for (int j = 0; j < kB; ++j)
+    if (left >> j & 1) s[i0 + j] = pv[j];
+  __syncthreads();
+}
+
 template <int SRC>
 __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
     k_tile_resolve(int64_t n, int32_t* rep, uint32_t* xbits, uint32_t* xlist,
@@ -383,6 +455,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
   }
   __syncthreads();
   if (SRC != kSrcRep && threadIdx.x == 0 && s_cnt) atomicAdd(io.counter, (unsigned long long)s_cnt);
+  run_shortcut(s, base, cnt);
   for (;;) {
     bool changed = false;
     for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
@@ -402,11 +475,15 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
   // then a bitmap), collected in shared memory (s[] is free once the reps
   // are out) and appended with ONE global atomic per tile -- a per-warp
   // atomic on the shared counter serialises on a single address.
+  // The bitmap round trips run after the candidates are compacted: one
+  // candidate per thread per pass, so a tile waits about one L2 latency
+  // for them, not one per item of the busiest thread (and without the
+  // registers that batching across a thread's items would need).
   constexpr int kPer = kTileV / kTileThreads;
-  __shared__ uint32_t s_xn;
+  __shared__ uint32_t s_xn, s_new, s_wr;
   __shared__ unsigned long long s_xb;
   uint32_t pk[kPer];
-  uint32_t app = 0;
+  uint32_t cand = 0;
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     const int i = threadIdx.x + k * kTileThreads;
@@ -416,26 +493,33 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
     if (i < cnt) {
       rep[base + i] = p;
       const int64_t lp = (int64_t)p - base;
-      if ((lp < 0 || lp >= cnt) && (threadIdx.x & 31) == __ffs(same) - 1) {
-        // many vertices share one exit target (a big component's root):
-        // a plain L2 read skips the atomic once the bit is set
-        // (batching these round trips across items measured slower: the
-        // extra registers spill at the 32-register cap of 2 x 1024 threads)
-        const uint32_t bit = 1u << (p & 31);
-        if (!(ld_cg(&xbits[p >> 5]) & bit) && !(atomicOr(&xbits[p >> 5], bit) & bit))
-          app |= 1u << k;
-      }
+      if ((lp < 0 || lp >= cnt) && (threadIdx.x & 31) == __ffs(same) - 1) cand |= 1u << k;
     }
   }
-  if (threadIdx.x == 0) s_xn = 0;
+  if (threadIdx.x == 0) s_xn = s_new = s_wr = 0;
   __syncthreads();  // s[] reads done
 #pragma unroll
   for (int k = 0; k < kPer; ++k)
-    if (app & (1u << k)) s[atomicAdd(&s_xn, 1u)] = (int32_t)pk[k];
+    if (cand & (1u << k)) s[atomicAdd(&s_xn, 1u)] = (int32_t)pk[k];
   __syncthreads();
-  if (threadIdx.x == 0) s_xb = s_xn ? atomicAdd(xcount, (unsigned long long)s_xn) : 0ull;
+  const uint32_t nc = s_xn;
+  for (uint32_t j = threadIdx.x; j < nc; j += kTileThreads) {
+    // many vertices share one exit target (a big component's root): a
+    // plain L2 read skips the atomic once the bit is set
+    const uint32_t p = (uint32_t)s[j];
+    const uint32_t bit = 1u << (p & 31);
+    if (!(ld_cg(&xbits[p >> 5]) & bit) && !(atomicOr(&xbits[p >> 5], bit) & bit)) {
+      s[j] = (int32_t)(p | 0x80000000u);  // (ids < 2^31: the top bit marks a new target)
+      atomicAdd(&s_new, 1u);
+    }
+  }
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < s_xn; j += kTileThreads) xlist[s_xb + j] = (uint32_t)s[j];
+  if (threadIdx.x == 0) s_xb = s_new ? atomicAdd(xcount, (unsigned long long)s_new) : 0ull;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < nc; j += kTileThreads) {
+    const uint32_t p = (uint32_t)s[j];
+    if (p & 0x80000000u) xlist[s_xb + atomicAdd(&s_wr, 1u)] = p & 0x7FFFFFFFu;
+  }
 }
 
 // In-place doubling over the exit set, all rounds in one cooperative

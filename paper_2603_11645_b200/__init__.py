@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librstg.so")
+# (RSTG_LIB_PATH: an experiment's alternative build of the same library)
+LIB_PATH = os.environ.get("RSTG_LIB_PATH") or os.path.join(HERE, "librstg.so")
 
 BFS, CC_EULER, PR_RST = 0, 1, 2  # bench.hpp:16 AlgoKind
 ALGOS = {"bfs": BFS, "cc-euler": CC_EULER, "pr-rst": PR_RST}

@@ -161,6 +161,9 @@ int64_t run_pipeline(rstg_graph* g, int algo, int64_t root, int64_t jump_batch, 
     if (!roots) roots = h.ws<int32_t>(WS_ROOTS, h.g.n + 1);
     nroots = bfs_rst(h, (int32_t)root, parent, levels, roots);
   } else if (algo == RSTG_CC_EULER) {
+    // (a tree edge's eto word holds its edge index below a flag bit)
+    if (h.g.m >= (int64_t{1} << 31))
+      throw ArgError("cc-euler needs fewer than 2^31 edges on one device");
     int32_t* labels = h.ws<int32_t>(WS_REP, h.g.n);
     // round 0 runs from the CSR (and writes every local list) when there is one
     // (round 0 runs -- from keys or the CSR -- whenever there are edges and

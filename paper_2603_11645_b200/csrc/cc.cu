@@ -234,16 +234,18 @@ struct RoundIO {
 // with few such pointers (power-law graphs) skips it after one barrier.
 __device__ __forceinline__ void run_shortcut(int32_t* s, int64_t base, int cnt) {
   constexpr int kB = kTileV / kTileThreads;
-  static_assert(kB == 8, "blocked layout: 8 vertices per thread");
+  static_assert(kB % 4 == 0 && kB <= 32, "blocked layout: a multiple of 4 vertices per thread");
   __shared__ int s_wmax[kTileThreads / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int i0 = t * kB;
   int32_t pv[kB];
-  {
-    const int4 a = reinterpret_cast<const int4*>(s)[2 * t];
-    const int4 b = reinterpret_cast<const int4*>(s)[2 * t + 1];
-    pv[0] = a.x; pv[1] = a.y; pv[2] = a.z; pv[3] = a.w;
-    pv[4] = b.x; pv[5] = b.y; pv[6] = b.z; pv[7] = b.w;
+#pragma unroll
+  for (int q = 0; q < kB / 4; ++q) {
+    const int4 a = reinterpret_cast<const int4*>(s)[kB / 4 * t + q];
+    pv[4 * q] = a.x;
+    pv[4 * q + 1] = a.y;
+    pv[4 * q + 2] = a.z;
+    pv[4 * q + 3] = a.w;
   }
   uint32_t left = 0;
 #pragma unroll
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
         if (io.tflag && e < io.m_local) io.tflag[e] = 1;
         if (io.link) {
           const int2 ab = io.edges[e];
-          link_tree_edge(io.eu, (uint32_t)v, (uint32_t)ab.x, (uint32_t)ab.y);
+          link_tree_edge(io.eu, (uint32_t)v, (uint32_t)ab.x, (uint32_t)ab.y, e);
         }
       }
     } else {
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
           }
           if (io.link) {
             const uint32_t pa = (uint32_t)v, qa = io.eu.nslots + (uint32_t)v;  // pa: u -> v, qa: v -> u
-            reinterpret_cast<uint2*>(io.eu.eto)[v] = make_uint2((uint32_t)v, (uint32_t)u);
+            io.eu.eto[v] = (uint32_t)u;  // (b = v, the slot: one word per tree edge)
             const int64_t lu = (int64_t)u - base;
             uint32_t nu;
             if (lu >= 0) {  // u < v, so lu < cnt
@@ -937,7 +939,7 @@ __global__ void __launch_bounds__(kBlock)
         if (io.tflag && e < io.m_local) io.tflag[e] = 1;
         if (io.link) {
           const int2 ab = io.edges[e];
-          link_tree_edge(io.eu, r, (uint32_t)ab.x, (uint32_t)ab.y);
+          link_tree_edge(io.eu, r, (uint32_t)ab.x, (uint32_t)ab.y, e);
         }
         atomicAdd(&s_h, 1u);
       }
@@ -1056,8 +1058,8 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
   if (round0) {
     // round 0 (min mode over singleton reps) straight from the CSR (or the
     // upload's keys), fused with its apply and shortcutting
-    // offsets, first neighbour, rep; a tree edge (arc heads + successors) per vertex
-    h.timer.begin(h.stream, "cc.round0", 4.0 * (n + 1) + 8.0 * n + (euler ? 16.0 * n : 0.0));
+    // offsets, first neighbour, rep; a tree edge (arc head 4 B + successors 8 B) per vertex
+    h.timer.begin(h.stream, "cc.round0", 4.0 * (n + 1) + 8.0 * n + (euler ? 12.0 * n : 0.0));
     resolve_round(h, rep, n, keyed ? kSrcRound0Slot : kSrcRound0, io, &zc);
     zc.k = 0;
     h.timer.end(h.stream);

@@ -274,7 +274,9 @@ enum WsSlot : int {
 // atomicExch (rhead/rtail, NONE-initialised).
 struct EulerIO {
   uint32_t nslots;  // N
-  uint32_t* eto;    // N pairs (to(i), to(N + i)) = (b, a)
+  uint32_t* eto;    // N words: the tree edge of slot i, arcs i = a -> b, N + i = b -> a:
+                    //   a, when b = i (round 0: the vertex that hooked is b), or
+                    //   kEtoEdge | e (e = the edge's index in the graph's edge list)
   uint32_t* S;      // 2N  successors
   uint32_t* vhead;  // n   local cycle: its first arc (NONE: no local list)
   uint32_t* vtail;  // n   local cycle: its last arc (S[rev(vtail)] = vhead)
@@ -311,10 +313,18 @@ __device__ __forceinline__ int32_t find_root_ro(const int32_t* rep, int32_t x) {
   }
 }
 
+constexpr uint32_t kEtoEdge = 0x80000000u;  // eto word: an edge index, not an endpoint
+// The endpoints (b, a) of slot i's tree edge (arc i = a -> b) from its eto word.
+__device__ __forceinline__ uint2 eto_ends(uint32_t w, uint32_t i, const int2* __restrict__ edges) {
+  if (!(w & kEtoEdge)) return make_uint2(i, w);
+  const int2 e = edges[w & ~kEtoEdge];
+  return make_uint2((uint32_t)e.y, (uint32_t)e.x);
+}
+// a tree edge (a, b) = edges[e] on slot `slot` (e < 2^31: checked by the callers' graphs)
 __device__ __forceinline__ void link_tree_edge(const EulerIO& io, uint32_t slot, uint32_t a,
-                                               uint32_t b) {
+                                               uint32_t b, uint32_t e) {
   const uint32_t p = slot, q = io.nslots + slot;  // p: a -> b, q: b -> a
-  reinterpret_cast<uint2*>(io.eto)[slot] = make_uint2(b, a);
+  io.eto[slot] = kEtoEdge | e;
   const uint32_t na = atomicExch(&io.rhead[a], p);  // next(p) = na
   const uint32_t nb = atomicExch(&io.rhead[b], q);  // next(q) = nb
   io.S[p] = nb;  // S[p] = next(rev p) = next(q)

@@ -265,20 +265,21 @@ __global__ void k_link_edges(int64_t T, const int2* __restrict__ edges, EulerIO 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int2 e = edges[i];
-    link_tree_edge(io, (uint32_t)i, (uint32_t)e.x, (uint32_t)e.y);
+    link_tree_edge(io, (uint32_t)i, (uint32_t)e.x, (uint32_t)e.y, (uint32_t)i);
   }
 }
 
 // derive_parents (:172-176) on (ruler, offset) ranks, one thread per slot.
 __global__ void __launch_bounds__(kBlock)
     k_orient(int64_t N, const int32_t* __restrict__ lab, bool cc_slots,
-             const uint2* __restrict__ eto, const uint32_t* __restrict__ sl,  // the rank words
+             const uint32_t* __restrict__ eto, const int2* __restrict__ edges,
+             const uint32_t* __restrict__ sl,  // the rank words
              const uint32_t* __restrict__ rstart, int ob, int32_t* __restrict__ parent) {
   const uint32_t mask = (1u << ob) - 1u;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (cc_slots && lab[i] == (int32_t)i) continue;  // no tree edge in this slot
-    const uint2 t = eto[i];  // (b, a): arc i = a -> b, arc N + i = b -> a
+    const uint2 t = eto_ends(eto[i], (uint32_t)i, edges);  // (b, a): arc i = a -> b, N + i = b -> a
     const uint32_t wp = sl[i], wq = sl[N + i];
     const uint32_t rp = rstart[wp >> ob] + (wp & mask);
     const uint32_t rq = rstart[wq >> ob] + (wq & mask);
@@ -292,14 +293,15 @@ __global__ void __launch_bounds__(kBlock)
 
 // derive_parents on tile ranks (tilerank.cu): rank = segstart[seg] + off.
 __global__ void __launch_bounds__(kBlock)
-    k_orient_tiles(int64_t N, const uint2* __restrict__ eto, const uint32_t* __restrict__ seg,
+    k_orient_tiles(int64_t N, const uint32_t* __restrict__ eto, const int2* __restrict__ edges,
+                   const uint32_t* __restrict__ seg,
                    const uint16_t* __restrict__ off, const uint32_t* __restrict__ segstart,
                    int32_t* __restrict__ parent) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t sp = seg[i];
     if (sp == kNone32) continue;  // no tree edge in this slot (the tile pass marked it)
-    const uint2 t = eto[i];  // (b, a): arc i = a -> b, arc N + i = b -> a
+    const uint2 t = eto_ends(eto[i], (uint32_t)i, edges);  // (b, a): arc i = a -> b, N + i = b -> a
     const uint32_t rp = segstart[sp] + off[i];
     const uint32_t rq = segstart[seg[N + i]] + off[N + i];
     if (rp > rq)
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kBlock)
 EulerIO euler_buffers(Handle& h, int64_t N, bool local_written) {
   EulerIO io;
   io.nslots = (uint32_t)N;
-  io.eto = h.ws<uint32_t>(WS_ETO, 2 * N);
+  io.eto = h.ws<uint32_t>(WS_ETO, N);
   io.S = h.ws<uint32_t>(WS_SUCC, 2 * N);
   io.vhead = h.ws<uint32_t>(WS_VHEAD, h.g.n);
   io.vtail = h.ws<uint32_t>(WS_VTAIL, h.g.n);
@@ -442,11 +444,13 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
     const TileRank tr = lr_rank_tiles(h, P, N, io.S, labels, cc_slots, T, verify);
     // seg of every slot; per tree edge eto, the other seg, two offsets, two starts, parent
     // compulsory: per slot its arc's segment word 4 B + offset 2 B; per tree
-    // edge the pair's heads 8 B, the other arc's word 4 B + offset 2 B, the
+    // edge its eto word 4 B, the other arc's word 4 B + offset 2 B, the
     // parent 4 B (segment starts: one small L2-resident table)
-    h.timer.begin(s, "euler.orient", 6.0 * N + 18.0 * T);
-    const uint2* eto = reinterpret_cast<const uint2*>(io.eto);
-    k_orient_tiles<<<grid_for(N), kBlock, 0, s>>>(N, eto, tr.seg, tr.off, tr.segstart, parent);
+    h.timer.begin(s, "euler.orient", 6.0 * N + 14.0 * T);
+    const uint32_t* eto = io.eto;
+    const int2* edges = h.g.edges;
+    k_orient_tiles<<<grid_for(N), kBlock, 0, s>>>(N, eto, edges, tr.seg, tr.off, tr.segstart,
+                                                  parent);
     CK_LAUNCH();
     h.stats.step(N);
     h.timer.end(s);
@@ -456,13 +460,13 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
       h.late_copy = {};
     }
     if (tr.deferred)
-      h.late_check = [&h, P, N, tr, eto, parent, lablist, comps] {
+      h.late_check = [&h, P, N, tr, eto, edges, parent, lablist, comps] {
         if (tile_rank_settle(h, P, N, tr)) {
           // re-derive from the recomputed ranks: the roots first (the first
           // orientation, on wrong ranks, may have given a root a parent)
           k_reset_roots<<<grid_for(N), kBlock, 0, h.stream>>>(lablist, comps, parent);
-          k_orient_tiles<<<grid_for(N), kBlock, 0, h.stream>>>(N, eto, tr.seg, tr.off, tr.segstart,
-                                                               parent);
+          k_orient_tiles<<<grid_for(N), kBlock, 0, h.stream>>>(N, eto, edges, tr.seg, tr.off,
+                                                               tr.segstart, parent);
           CK_LAUNCH();
           CK(cudaStreamSynchronize(h.stream));
         }
@@ -471,8 +475,8 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   }
   const uint32_t* rstart = lr_rank(h, P, E, io.S, sl, rpos, ctr, verify, 2 * T, nullptr);
 
-  h.timer.begin(s, "euler.orient", 8.0 * N + 16.0 * T + 4.0 * T);
-  k_orient<<<grid_for(N), kBlock, 0, s>>>(N, labels, cc_slots, reinterpret_cast<const uint2*>(io.eto),
+  h.timer.begin(s, "euler.orient", 8.0 * N + 12.0 * T + 4.0 * T);
+  k_orient<<<grid_for(N), kBlock, 0, s>>>(N, labels, cc_slots, io.eto, h.g.edges,
                                           sl, rstart, P.ob, parent);
   CK_LAUNCH();
   h.stats.step(N);

@@ -22,9 +22,12 @@ def main(src, dst, tag):
             out = json.load(f)
     for f in sorted(glob.glob(os.path.join(src, "phases_*.json"))):
         wl = os.path.basename(f)[len("phases_"):-len(".json")]
+        algo = "cc-euler"
+        if "__" in wl:  # phases_<workload>__<algo>.json
+            wl, algo = wl.split("__", 1)
         with open(f) as fh:
             ph = json.load(fh)
-        out.setdefault(wl, {})["cc-euler"] = {
+        out.setdefault(wl, {})[algo] = {
             "source": f"ncu --nvtx --print-nvtx-rename kernel, dram__bytes_read.sum + dram__bytes_write.sum, "
                       f"per build, capture {tag} (profiles/{tag}/)",
             "phases": ph,

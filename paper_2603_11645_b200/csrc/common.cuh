@@ -16,6 +16,9 @@
 namespace rstg {
 
 constexpr uint32_t kNone32 = 0xFFFFFFFFu;
+// successor word of an arc whose slot holds no tree edge (never an arc id:
+// 2N < 2^32 - 2; NONE is a tour's end)
+constexpr uint32_t kEmptySlot = 0xFFFFFFFEu;
 // kKeyInf = INT64_MAX exactly as the reference: every real key is below it
 // (vertex ids < 2^31 - 1), so unsigned and signed order agree and an NCCL
 // int64 MIN all-reduce combines slots like combine_min (multi-GPU CC).

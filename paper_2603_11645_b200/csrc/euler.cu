@@ -95,7 +95,8 @@ __global__ void __launch_bounds__(kBlock)
     k_euler_fix(int64_t n, const int32_t* lab, const uint8_t* __restrict__ present,
                 uint32_t* minv, EulerIO io, bool cc_slots, uint32_t* labels_out,
                 unsigned long long* nlabels, uint32_t* rpos, uint32_t* sl, unsigned long long* ctr,
-                unsigned long long* tiles, int logk, int ob, uint32_t cap, bool rulers) {
+                unsigned long long* tiles, int logk, int ob, uint32_t cap, bool rulers,
+                bool mark_empty) {
   constexpr int64_t kTile = (int64_t)kFixItems * kBlock;
   __shared__ unsigned long long s_tile;
   __shared__ uint32_t s_nl;
@@ -140,6 +141,10 @@ __global__ void __launch_bounds__(kBlock)
       if ((threadIdx.x & 31) == __ffs(peers) - 1 && (uint32_t)v < minv[l])
         atomicMin(&minv[l], (uint32_t)v);  // the group's lowest lane has its smallest vertex
       if (present ? present[v] != 0 : l == (int32_t)v) flags |= 1u << (16 + k);
+      if (mark_empty && l == (int32_t)v) {  // (cc slots: a root's slot holds no tree edge)
+        io.S[v] = kEmptySlot;
+        io.S[io.nslots + v] = kEmptySlot;
+      }
       if (rulers && cc_slots && l != (int32_t)v) {
         if (lr_hash_ruler((uint32_t)v, logk)) flags |= 1u << (2 * k);
         if (lr_hash_ruler(io.nslots + (uint32_t)v, logk)) flags |= 2u << (2 * k);
@@ -416,7 +421,7 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
       !verify && (tiles_env ? atoi(tiles_env) != 0 : cc_slots && edge_locality(h) >= 50);
   k_euler_fix<<<grid_for((n + kFixItems - 1) / kFixItems), kBlock, 0, s>>>(
       n, labels, present, minv, io, cc_slots, lablist, comps, rpos, sl, ctr, tiles, P.logk0, P.ob,
-      (uint32_t)P.cap, !use_tiles);
+      (uint32_t)P.cap, !use_tiles, use_tiles && cc_slots);
   h.rhead_clean = io.rhead;
   h.rhead_clean_n = n;
   k_override_root<<<1, 32, 0, s>>>(labels, minv, designated_root, cc_slots);
@@ -441,7 +446,9 @@ void euler_root(Handle& h, const int32_t* labels, const EulerIO& io, int64_t N, 
   if (T == 0) return;
 
   if (use_tiles) {
-    const TileRank tr = lr_rank_tiles(h, P, N, io.S, labels, cc_slots, T, verify);
+    // (cc slots: the vertex pass marked the empty slots in S, no labels needed)
+    const TileRank tr = lr_rank_tiles(h, P, N, io.S, cc_slots ? nullptr : labels, cc_slots, T,
+                                      verify);
     // seg of every slot; per tree edge eto, the other seg, two offsets, two starts, parent
     // compulsory: per slot its arc's segment word 4 B + offset 2 B; per tree
     // edge its eto word 4 B, the other arc's word 4 B + offset 2 B, the

@@ -147,7 +147,10 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
   //    (staged in word[], free until the walks)
   uint32_t vmask = 0;  // own arcs that exist
   const uint32_t last = N - 1;  // loads are unconditional (clamped): all in flight at once
-  if (cc_slots) {
+  // (cc_slots with lab == nullptr: the Euler vertex pass marked every empty
+  // slot's successor words kEmptySlot, so validity comes with the S loads
+  // below and the labels are not read at all)
+  if (cc_slots && lab) {
     int32_t lv[kPer];
 #pragma unroll
     for (int k = 0; k < kPer; ++k) lv[k] = __ldcs(&lab[min(t0 + tid + k * kThreads, last)]);
@@ -156,13 +159,14 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
       const uint32_t j = tid + k * kThreads;
       vmask |= (j < cnt && lv[k] != (int32_t)(t0 + j)) ? 3u << (2 * k) : 0u;
     }
-  } else {
+  } else if (!cc_slots) {
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const uint32_t j = tid + k * kThreads;
       vmask |= (j < cnt && t0 + j < T) ? 3u << (2 * k) : 0u;
     }
   }
+  const bool marked = cc_slots && !lab;
   constexpr int kBatch = kOwn < 16 ? kOwn : 16;
 #pragma unroll
   for (int q0 = 0; q0 < kOwn; q0 += kBatch) {
@@ -175,7 +179,12 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
       y[q] = __ldg(&S[((q0 + q) & 1) ? N + j : j]);
     }
 #pragma unroll
-    for (int q = 0; q < kBatch; ++q) word[local_of(q0 + q)] = y[q];
+    for (int q = 0; q < kBatch; ++q) {
+      word[local_of(q0 + q)] = y[q];
+      if (marked && !((q0 + q) & 1) && tid + ((q0 + q) >> 1) * kThreads < cnt &&
+          y[q] != kEmptySlot)
+        vmask |= 3u << (q0 + q);  // (both arcs of the slot)
+    }
   }
   __syncthreads();  // haspred zeroed
   uint32_t tmask = 0;  // own arcs whose successor leaves the tile (segment tails)

@@ -77,19 +77,33 @@ __device__ __forceinline__ void tile_publish(unsigned long long* state, uint32_t
   // waits on a returned value)
   st_relaxed_gpu(&state[1 + tile], (tile == 0 ? kLbInc : kLbAgg) | count);
 }
-__device__ __forceinline__ uint32_t tile_prefix(unsigned long long* state, uint32_t tile,
-                                                uint32_t count) {
-  if (tile == 0) return 0;
+// The look-back by one whole warp (all 32 lanes call it): each step reads
+// 32 predecessors' words at once and stops at the nearest inclusive prefix
+// -- one L2 round trip per 32 tiles instead of one per tile (a thread
+// walking back alone left the rest of its CTA waiting at the barrier).
+__device__ __forceinline__ uint32_t tile_prefix_warp(unsigned long long* state, uint32_t tile,
+                                                     uint32_t count) {
+  const unsigned lane = threadIdx.x & 31u;
   unsigned long long* st = state + 1;
   unsigned long long excl = 0;
-  for (int64_t p = (int64_t)tile - 1;;) {
-    const unsigned long long v = ld_relaxed_gpu(&st[p]);
-    if (!(v >> 62)) continue;  // not published yet
-    excl += v & kLbVal;
-    if ((v >> 62) == 2) break;
-    --p;
+  for (int64_t base = (int64_t)tile - 1; base >= 0; base -= 32) {
+    const int64_t p = base - (int64_t)lane;
+    unsigned long long v;
+    unsigned inc;
+    for (;;) {
+      v = p >= 0 ? ld_relaxed_gpu(&st[p]) : kLbInc;  // (before tile 0: an inclusive 0)
+      inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+      const unsigned lim = inc ? (2u << (__ffs(inc) - 1)) - 1u : 0xffffffffu;  // lanes that count
+      if (!(__ballot_sync(0xffffffffu, (v >> 62) == 0) & lim)) break;  // all of them published
+    }
+    const unsigned first = inc ? (unsigned)__ffs(inc) - 1u : 31u;
+    unsigned long long add = lane <= first ? (v & kLbVal) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+    excl += add;
+    if (inc) break;
   }
-  st_relaxed_gpu(&st[tile], kLbInc | (excl + count));
+  if (lane == 0) st_relaxed_gpu(&st[tile], kLbInc | (excl + count));
   return (uint32_t)excl;
 }
 
@@ -252,9 +266,12 @@ __global__ void __launch_bounds__(kThreads, tile_rank_blocks<kSlots, kThreads>()
     for (uint32_t m = hmask; m; m &= m - 1) hid[local_of(__ffs(m) - 1)] = (uint16_t)k++;
   }
   __syncthreads();
-  if (tid == 0) {
-    s_base = tile_prefix(state, tile, s_nh);
-    if (tile == gridDim.x - 1) *nseg = s_base + s_nh;
+  if (tid < 32) {
+    const uint32_t b = tile_prefix_warp(state, tile, s_nh);
+    if (tid == 0) {
+      s_base = b;
+      if (tile == gridDim.x - 1) *nseg = b + s_nh;
+    }
   }
   __syncthreads();
   const uint32_t sbase = s_base;
@@ -416,9 +433,12 @@ __global__ void __launch_bounds__(kThreads, kNodes > 8192 ? 1 : 2048 / kThreads)
     for (uint32_t m = hmask; m; m &= m - 1) hid[tid + (__ffs(m) - 1) * kThreads] = (uint16_t)c++;
   }
   __syncthreads();
-  if (tid == 0) {
-    s_base = tile_prefix(state, tile, s_nh);
-    if (tile == ntiles - 1) *nseg = s_base + s_nh;
+  if (tid < 32) {
+    const uint32_t b = tile_prefix_warp(state, tile, s_nh);
+    if (tid == 0) {
+      s_base = b;
+      if (tile == ntiles - 1) *nseg = b + s_nh;
+    }
   }
   __syncthreads();
 #pragma unroll

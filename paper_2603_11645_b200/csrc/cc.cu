@@ -858,7 +858,7 @@ void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* 
   const int64_t m = h.g.m;
   const uint32_t eb = (uint32_t)h.g.e_base;
   bool launched = false;
-  if (h.cc_round == 0 || m == 0) {
+  if (h.cc_round == 0 || m == 0 || h.cc_round < h.cc_filter_from) {
     if (m > 0) {
       launch_hook_k(h, mode, h.g.edges, m, eb, nullptr, rep, slot, any_prop, nullptr, nullptr,
                     zero_word);
@@ -881,7 +881,7 @@ void cc_hook_round(Handle& h, int mode, const int32_t* rep, unsigned long long* 
   if (zero_word && !launched) CK(cudaMemsetAsync(zero_word, 0, sizeof(*zero_word), h.stream));
 }
 void cc_round_done(Handle& h, int64_t out_count) {
-  if (h.cc_round >= 1 && h.g.m > 0) {
+  if (h.cc_round >= 1 && h.cc_round >= h.cc_filter_from && h.g.m > 0) {
     if (h.cc_active >= 0) h.cc_list ^= 1;
     h.cc_active = out_count;
   }
@@ -895,6 +895,13 @@ void cc_reset_rounds(Handle& h) {
   h.cc_round = 0;
   h.cc_active = -1;
   h.cc_list = 0;
+  // Active-edge filtering records the edges a round still saw crossing; on
+  // a dense graph the first hook round sees most edges cross the round-0
+  // trees (RMAT-24: 219M of 260M), so its list costs more to write and to
+  // gather from than a second full pass over the edge stream: start the
+  // lists one round later there (RSTG_CC_FILTER_FROM overrides: 1 or 2).
+  const char* e = getenv("RSTG_CC_FILTER_FROM");
+  h.cc_filter_from = e ? std::max(1, atoi(e)) : (h.g.m > 4 * h.g.n ? 2 : 1);
 }
 
 void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tflag,
@@ -1173,7 +1180,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     // Lazy finds cost extra gathers per active edge endpoint; while many
     // edges are still active one compression pass over n is cheaper (the
     // two-level resolve: hook chains of one round may be long).
-    if (h.cc_active > n / 4) {
+    if (h.cc_active < 0 || h.cc_active > n / 4) {  // (-1: no list yet, every edge active)
       h.timer.begin(h.stream, "cc.compress", 8.0 * n);
       compress();
       h.timer.end(h.stream);

@@ -104,6 +104,7 @@ class Handle {
   int cc_round = 0;
   int64_t cc_active = -1;  // edges in the current active list, -1 = all
   int cc_list = 0;
+  int cc_filter_from = 1;  // first hook round that records its crossing edges
   bool cc_lazy = false;    // hook rounds find roots (no per-round compression)
   // WS_SLOT holds all-empty keys from a completed cc_exact (apply resets
   // every slot it consumes), so the next build skips re-initialising it;

@@ -214,7 +214,7 @@ __global__ void k_pr_resolve(const uint32_t* __restrict__ list, const unsigned l
                              int64_t n, const int2* __restrict__ edges, uint32_t e_base,
                              const int32_t* __restrict__ rep, const unsigned long long* __restrict__ slot,
                              uint8_t* mark, int32_t* scratch, uint32_t* seeds, uint32_t* grafted,
-                             unsigned long long* ngraft) {
+                             unsigned long long* ngraft, int32_t* direct_parent) {
   const int64_t R = list ? (int64_t)*cnt : n;
   __shared__ uint32_t s_n;
   __shared__ unsigned long long s_b;
@@ -232,8 +232,15 @@ __global__ void k_pr_resolve(const uint32_t* __restrict__ list, const unsigned l
         const int2 uv = edges[(uint32_t)key - e_base];
         u = (rep[uv.x] == (int32_t)v) ? uv.x : uv.y;
         const int32_t w = (u == uv.x) ? uv.y : uv.x;
-        mark[u] = 1;
-        scratch[u] = w;
+        if (direct_parent) {
+          // the identity forest (no reversal yet): u = v is a singleton
+          // tree, its path to reverse is u alone -- reverse_paths reduces
+          // to parent[u] = w (no marking, no queues, no check needed)
+          direct_parent[u] = w;
+        } else {
+          mark[u] = 1;
+          scratch[u] = w;
+        }
         g = true;
       }
     }
@@ -242,7 +249,7 @@ __global__ void k_pr_resolve(const uint32_t* __restrict__ list, const unsigned l
     __syncthreads();
     if (threadIdx.x == 0) s_b = s_n ? atomicAdd(ngraft, (unsigned long long)s_n) : 0ull;
     __syncthreads();
-    if (g) {
+    if (g && !direct_parent) {
       seeds[s_b + pos] = (uint32_t)u;
       grafted[s_b + pos] = v;
     }
@@ -608,9 +615,13 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
 
     h.timer.begin(s, "pr.resolve", 24.0 * nroots);
     CK(cudaMemsetAsync(pc + P_NROOTS_OUT, 0, 2 * sizeof(unsigned long long), s));  // out, ngraft
+    // (the first graft round on the identity forest reverses singleton
+    // paths: the resolve sets the parents itself)
+    const bool direct = identity;
     k_pr_resolve<<<grid_for(nroots), kBlock, 0, s>>>(in_list, pc + P_NROOTS_IN, n, h.g.edges,
                                                      (uint32_t)h.g.e_base, rep, slot, mark,
-                                                     scratch, seeds, grafted, pc + P_NGRAFT);
+                                                     scratch, seeds, grafted, pc + P_NGRAFT,
+                                                     direct ? parent : nullptr);
     k_pr_update<<<grid_for(nroots), kBlock, 0, s>>>(in_list, pc + P_NROOTS_IN, n, rep, slot,
                                                     rl[out], pc + P_NROOTS_OUT);
     CK(cudaMemcpyAsync(pc + P_NROOTS_IN, pc + P_NROOTS_OUT, sizeof(unsigned long long),
@@ -622,14 +633,19 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     h.stats.step(n);
     h.timer.end(s);
 
-    run_marking();
-    h.timer.begin(s, "pr.reverse", 0.0);
-    k_pr_check<<<grid_for(nroots), kBlock, 0, s>>>(grafted, seeds, pc + P_NGRAFT, mark, parent,
-                                                   bad_mark);
-    h.stats.step(n);
-    run_reverse();
-    CK_LAUNCH();
-    h.timer.end(s);
+    if (direct) {
+      identity = false;
+      forest_dirty = true;
+    } else {
+      run_marking();
+      h.timer.begin(s, "pr.reverse", 0.0);
+      k_pr_check<<<grid_for(nroots), kBlock, 0, s>>>(grafted, seeds, pc + P_NGRAFT, mark, parent,
+                                                     bad_mark);
+      h.stats.step(n);
+      run_reverse();
+      CK_LAUNCH();
+      h.timer.end(s);
+    }
 
     // converged reps again (batched_jump's result, :216-252): the grafted
     // roots' chains are jumped as a list, then one gather over n

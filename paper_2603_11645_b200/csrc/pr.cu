@@ -139,20 +139,13 @@ __global__ void k_pr_pos(int64_t n, const uint32_t* __restrict__ byl, uint32_t* 
 }
 
 // Level 0 of the structure: the parent forest in positions (a root points
-// at itself), Q0[i] = pos[parent[byl[i]]].
-__global__ void __launch_bounds__(kBlock)
-    k_pr_q0(int64_t n, const uint32_t* __restrict__ byl, const int32_t* __restrict__ parent,
-            const uint32_t* __restrict__ pos, uint32_t* __restrict__ q0) {
-  constexpr int kB = 4;  // four gathers in flight per thread
-  const int64_t g = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += kB * g) {
-    uint32_t p[kB];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) p[j] = i0 + j * g < n ? (uint32_t)parent[byl[i0 + j * g]] : 0u;
-#pragma unroll
-    for (int j = 0; j < kB; ++j)
-      if (i0 + j * g < n) q0[i0 + j * g] = pos[p[j]];
-  }
+// at itself), Q0[i] = pos[parent[byl[i]]]. The identity at the start; every
+// parent write after that (the first round's direct grafts, each reversal)
+// updates its entry, so no rebuild pass over n is needed for it.
+__global__ void k_pr_q0_identity(int64_t n, uint32_t* __restrict__ q0) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    q0[i] = (uint32_t)i;
 }
 
 // Level k >= 1 for the positions [0, C[k]): walk the level-(k-1) pointers
@@ -214,7 +207,8 @@ __global__ void k_pr_resolve(const uint32_t* __restrict__ list, const unsigned l
                              int64_t n, const int2* __restrict__ edges, uint32_t e_base,
                              const int32_t* __restrict__ rep, const unsigned long long* __restrict__ slot,
                              uint8_t* mark, int32_t* scratch, uint32_t* seeds, uint32_t* grafted,
-                             unsigned long long* ngraft, int32_t* direct_parent) {
+                             unsigned long long* ngraft, int32_t* direct_parent,
+                             const uint32_t* __restrict__ pos, uint32_t* __restrict__ q0) {
   const int64_t R = list ? (int64_t)*cnt : n;
   __shared__ uint32_t s_n;
   __shared__ unsigned long long s_b;
@@ -237,6 +231,7 @@ __global__ void k_pr_resolve(const uint32_t* __restrict__ list, const unsigned l
           // tree, its path to reverse is u alone -- reverse_paths reduces
           // to parent[u] = w (no marking, no queues, no check needed)
           direct_parent[u] = w;
+          q0[pos[u]] = pos[w];
         } else {
           mark[u] = 1;
           scratch[u] = w;
@@ -406,7 +401,8 @@ __global__ void k_pr_reverse_a(const uint32_t* mk, const unsigned long long* bba
 }
 __global__ void k_pr_reverse_b(const uint32_t* mk, const unsigned long long* bbase,
                                const unsigned long long* mcnt, uint8_t* mark, int32_t* parent,
-                               int32_t* scratch, int* bad_rev) {
+                               int32_t* scratch, int* bad_rev, const uint32_t* __restrict__ pos,
+                               uint32_t* __restrict__ q0) {
   const int b = (int)blockIdx.y;
   const int64_t T = (int64_t)mcnt[b];
   const uint32_t* q = mk + bbase[b];
@@ -420,6 +416,7 @@ __global__ void k_pr_reverse_b(const uint32_t* mk, const unsigned long long* bba
       continue;
     }
     parent[v] = s;
+    q0[pos[v]] = pos[s];  // (level 0 of the skip structure follows the parents)
     scratch[v] = -1;
     mark[v] = 0;
   }
@@ -527,6 +524,10 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   // off[k], C[k] entries -- sum_k C[k] = n + the sum of the levels, about
   // 2n (sized exactly: the sum is random)
   uint32_t* Q = h.ws<uint32_t>(WS_PR_ANC, (size_t)L.off[K + 1] + 1);
+  if (n > 0) {
+    k_pr_q0_identity<<<g, kBlock, 0, s>>>(n, Q);
+    CK_LAUNCH();
+  }
   CK(cudaMemcpyAsync(bbase, cbase, (kMaxLvl + 2) * sizeof(unsigned long long),
                      cudaMemcpyDeviceToDevice, s));
   h.stats.step(n, 3);
@@ -538,11 +539,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   bool forest_dirty = false, identity = true;
   auto rebuild = [&]() {
     h.timer.begin(s, "pr.rebuild", 0.0);
-    // level 0: per position its id and parent (4 + 4 B), the parent's
-    // position (4 B), the entry out (4 B)
-    double bytes = 16.0 * n;
-    k_pr_q0<<<grid_for(n), kBlock, 0, s>>>(n, byl, parent, pos, Q);
-    h.stats.step(n);
+    double bytes = 0;  // (level 0 is kept current by the parent writes)
     for (int k = 1; k <= K && C[k] > 0; ++k) {
       // per position of level >= k: the level-(k-1) entry in (4 B), ~1 more
       // hop (4 B), the entry out (4 B)
@@ -579,7 +576,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   auto run_reverse = [&]() {
     const dim3 dg(2 * num_sms(), K + 1);
     k_pr_reverse_a<<<dg, kBlock, 0, s>>>(mk, bbase, mcnt, parent, scratch);
-    k_pr_reverse_b<<<dg, kBlock, 0, s>>>(mk, bbase, mcnt, mark, parent, scratch, bad_rev);
+    k_pr_reverse_b<<<dg, kBlock, 0, s>>>(mk, bbase, mcnt, mark, parent, scratch, bad_rev, pos, Q);
     CK_LAUNCH();
     h.stats.step(n);
     h.stats.step(n);
@@ -621,7 +618,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     k_pr_resolve<<<grid_for(nroots), kBlock, 0, s>>>(in_list, pc + P_NROOTS_IN, n, h.g.edges,
                                                      (uint32_t)h.g.e_base, rep, slot, mark,
                                                      scratch, seeds, grafted, pc + P_NGRAFT,
-                                                     direct ? parent : nullptr);
+                                                     direct ? parent : nullptr, pos, Q);
     k_pr_update<<<grid_for(nroots), kBlock, 0, s>>>(in_list, pc + P_NROOTS_IN, n, rep, slot,
                                                     rl[out], pc + P_NROOTS_OUT);
     CK(cudaMemcpyAsync(pc + P_NROOTS_IN, pc + P_NROOTS_OUT, sizeof(unsigned long long),

@@ -708,9 +708,10 @@ constexpr int kJumpHash = 2 * kJumpSmallMax;
 constexpr size_t kJumpSmallSmem = kJumpHash * (sizeof(uint32_t) + sizeof(uint16_t)) +
                                   kJumpSmallMax * (sizeof(uint16_t) + sizeof(uint32_t));
 constexpr int kJumpPer = kJumpSmallMax / 1024;
-__global__ void __launch_bounds__(1024)
-    k_jump_small(const uint32_t* __restrict__ list, const unsigned long long* count, int32_t* rep) {
-  extern __shared__ uint32_t hkey[];  // vertex + 1, 0 = empty
+// (one block of 1024 threads; smem: kJumpSmallSmem bytes)
+__device__ __forceinline__ void jump_small_block(const uint32_t* __restrict__ list,
+                                                 const unsigned long long* count, int32_t* rep,
+                                                 uint32_t* hkey) {
   uint32_t* lst = hkey + kJumpHash;   // the list
   uint16_t* hval = reinterpret_cast<uint16_t*>(lst + kJumpSmallMax);  // list index
   uint16_t* par = hval + kJumpHash;  // index of the entry's pointer target
@@ -775,6 +776,11 @@ __global__ void __launch_bounds__(1024)
     const uint32_t t = lst[par[i]];
     if (t != v[k] && t != p[k]) rep[v[k]] = (int32_t)t;
   }
+}
+__global__ void __launch_bounds__(1024)
+    k_jump_small(const uint32_t* __restrict__ list, const unsigned long long* count, int32_t* rep) {
+  extern __shared__ uint32_t hkey[];  // vertex + 1, 0 = empty
+  jump_small_block(list, count, rep, hkey);
 }
 
 // Pointer-jumps the entries of a vertex list in place (one cooperative
@@ -978,6 +984,152 @@ void launch_cc_init(Handle& h, int32_t* rep, unsigned long long* slot) {
   h.stats.step(h.g.n);
 }
 
+// ---- the tail rounds, on the device ---------------------------------------
+// Once few edges still cross (meshes: a few thousand after the first hook
+// round) and the round-0 roots list is short, a round's kernels take a few
+// microseconds and its host round trip (the counter read, then the next
+// launches) takes longer than they do. The tail runs all remaining rounds
+// in ONE cooperative launch with the same steps as the host loop -- apply
+// over the current roots, the round-0 roots jump (block 0, in shared
+// memory), the next filtered lazy hook -- a grid barrier between steps and
+// the stop decision (no proposal) on the device. Proposals, hooks and
+// labels are those of the host loop: only the order of list entries
+// differs, which no result depends on.
+constexpr int kTailThreads = 1024;
+constexpr int64_t kTailMaxEdges = int64_t{1} << 20;
+struct TailArgs {
+  RoundIO io;                   // apply: slot, tflag, edges, link, eu; io.counter = hooks total
+  int32_t* rep;
+  uint32_t* elist[2];           // crossing-edge lists (ping-pong); round r's in elist[cur]
+  unsigned long long* lcount;   // their lengths (2 words): lcount[cur] = first_count
+  int64_t first_count;
+  int cur;
+  uint32_t* rl[3];              // roots lists: [0] the round-0 roots, [1], [2] current
+  unsigned long long* rcount;   // their lengths (dev_box[20..22])
+  int in;                       // the list round r's apply reads (0, 1 or 2)
+  int mode;                     // round r + 1's hook mode
+  int* any;                     // proposal flag (dev_box[2])
+  unsigned long long* out;      // [0] hook rounds run, [1] hooks of the last productive
+                                // round, [2] rounds exhausted flag
+  int64_t rounds_left;          // (cc_forest.cpp:88: the round cap)
+  unsigned long long hooks_before;  // hooks applied before round r's apply
+};
+
+// appends v to list/count with one atomic per warp
+__device__ __forceinline__ void warp_append(bool keep, uint32_t v, uint32_t* list,
+                                            unsigned long long* count) {
+  const unsigned ball = __ballot_sync(0xffffffffu, keep);
+  if (!ball) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(ball) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(ball));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (keep) list[base + __popc(ball & ((1u << lane) - 1u))] = v;
+}
+
+__global__ void __launch_bounds__(kTailThreads, 1) k_cc_tail(TailArgs a) {
+  extern __shared__ uint32_t jump_smem[];  // block 0's roots jump
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+  int in = a.in, cur = a.cur, mode = a.mode;
+  unsigned long long rounds = 0, last_hooks = 0, hooks_before = a.hooks_before;
+  if (gtid == 0) {
+    a.lcount[cur] = (unsigned long long)a.first_count;  // (read two barriers later)
+    a.out[2] = 0;
+  }
+  for (;;) {
+    // ---- apply (cc_forest.cpp:39-46) over the current roots
+    const int out = in == 1 ? 2 : 1;
+    {
+      const int64_t R = (int64_t)*(volatile unsigned long long*)&a.rcount[in];
+      const uint32_t* list = a.rl[in];
+      uint32_t hooked = 0;
+      for (int64_t b = gtid - (threadIdx.x & 31); b < R; b += gsize) {  // (warp-uniform trips)
+        const int64_t i = b + (threadIdx.x & 31);
+        bool keep = false;
+        uint32_t r = 0;
+        if (i < R) {
+          r = list[i];
+          const unsigned long long key = a.io.slot[r];
+          if (key == kKeyInf) {
+            keep = true;
+          } else {
+            a.rep[r] = (int32_t)(key >> 32);
+            a.io.slot[r] = kKeyInf;
+            const uint32_t e = (uint32_t)key - a.io.e_base;
+            if (a.io.tflag && e < a.io.m_local) a.io.tflag[e] = 1;
+            if (a.io.link) {
+              const int2 ab = a.io.edges[e];
+              link_tree_edge(a.io.eu, r, (uint32_t)ab.x, (uint32_t)ab.y, e);
+            }
+            ++hooked;
+          }
+        }
+        warp_append(keep, r, a.rl[out], &a.rcount[out]);
+      }
+      for (int o = 16; o > 0; o >>= 1) hooked += __shfl_xor_sync(0xffffffffu, hooked, o);
+      if ((threadIdx.x & 31) == 0 && hooked) atomicAdd(a.io.counter, (unsigned long long)hooked);
+    }
+    grid.sync();
+    // ---- the round-0 roots jump (block 0); the next round's counters zeroed
+    if (blockIdx.x == 0) {
+      jump_small_block(a.rl[0], &a.rcount[0], a.rep, jump_smem);
+    } else if (blockIdx.x == 1 && threadIdx.x == 0) {
+      a.lcount[cur ^ 1] = 0;
+      *a.any = 0;
+      if (in != 0) a.rcount[in] = 0;  // (the list just consumed is the next output)
+    }
+    {
+      const unsigned long long t = *(volatile unsigned long long*)a.io.counter;  // (after the barrier)
+      last_hooks = t - hooks_before;
+      hooks_before = t;
+    }
+    grid.sync();
+    // ---- the next hook round (lazy: roots found by walking up), over the
+    // edges the previous round saw crossing
+    {
+      const int64_t M = (int64_t)*(volatile unsigned long long*)&a.lcount[cur];
+      const uint32_t* el = a.elist[cur];
+      bool proposed = false;
+      for (int64_t b = gtid - (threadIdx.x & 31); b < M; b += gsize) {
+        const int64_t i = b + (threadIdx.x & 31);
+        bool cross = false;
+        uint32_t idx = 0;
+        if (i < M) {
+          idx = el[i];
+          const int2 e = a.io.edges[idx];
+          const int32_t ru = find_root(a.rep, e.x), rv = find_root(a.rep, e.y);
+          if (ru != rv) {
+            cross = true;
+            const int32_t lo = min(ru, rv), hi = max(ru, rv);
+            const int32_t winner = mode == 0 ? lo : hi, loser = mode == 0 ? hi : lo;
+            const unsigned long long key = pack_key((uint32_t)winner, a.io.e_base + idx);
+            if (key < a.io.slot[loser]) atomicMin(&a.io.slot[loser], key);
+          }
+        }
+        proposed |= cross;
+        warp_append(cross, idx, a.elist[cur ^ 1], &a.lcount[cur ^ 1]);
+      }
+      if (__any_sync(0xffffffffu, proposed) && (threadIdx.x & 31) == 0) *a.any = 1;
+    }
+    grid.sync();
+    ++rounds;
+    if (*(volatile int*)a.any == 0) break;  // a round without proposals (cc_forest.cpp:91)
+    if ((int64_t)rounds >= a.rounds_left) {
+      if (gtid == 0) a.out[2] = 1;
+      break;
+    }
+    cur ^= 1;
+    in = out;
+    mode ^= 1;
+  }
+  if (gtid == 0) {
+    a.out[0] = rounds;
+    a.out[1] = last_hooks;
+  }
+}
+
 // Edge-partitioned rounds (multi-GPU): the proposals of
 // every rank's local edges are MIN-combined before each apply --
 // combine_min (cc_forest.cpp:34) across ranks. Round 0 exchanges the dense
@@ -1105,7 +1257,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     const char* e = getenv("RSTG_CC_JUMP_ROOTS");
     return e ? atoi(e) != 0 : true;
   }();
-  int64_t total = 0, last_hooks = 0, prev_total = 0;
+  int64_t total = 0, last_hooks = 0, prev_total = 0, tail_last_hooks = -1;
   for (;; ++round) {
     if (round > n + 1) {
       h.cc_lazy = false;
@@ -1175,6 +1327,54 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     h.stats.rounds = round + 1;
     // a round without proposals applies nothing (cc_forest.cpp:91)
     if (!proposed) break;
+    // the remaining rounds on the device (see k_cc_tail) once they are small
+    static const bool tail_on = [] {
+      const char* e = getenv("RSTG_CC_TAIL");
+      return e ? atoi(e) != 0 : true;
+    }();
+    if (tail_on && !ex && have_r0 && jump_roots && r0_count <= kJumpSmallMax && h.cc_active >= 0 &&
+        h.cc_active <= kTailMaxEdges && h.cc_active <= n / 4) {
+      // per round: the crossing list read and rewritten (4 + 4 B), each edge
+      // 8 B and its two roots (~4 B each), the current roots' slots (16 B)
+      h.timer.begin(h.stream, "cc.tail", 24.0 * (double)h.cc_active + 16.0 * (double)cur_roots);
+      unsigned long long* box = reinterpret_cast<unsigned long long*>(h.dev_box);
+      TailArgs ta;
+      ta.io = io;
+      ta.rep = rep;
+      ta.elist[0] = h.ws<uint32_t>(WS_ELIST0, m);
+      ta.elist[1] = h.ws<uint32_t>(WS_ELIST1, m);
+      ta.lcount = box + 24;
+      ta.first_count = h.cc_active;
+      ta.cur = h.cc_list;
+      ta.rl[0] = rl[0];
+      ta.rl[1] = rl[1];
+      ta.rl[2] = rl[2];
+      ta.rcount = rcount;
+      ta.in = in;
+      ta.mode = mode ^ 1;
+      ta.any = any;
+      ta.out = box + 26;
+      ta.rounds_left = std::max<int64_t>(n + 1 - round, 1);
+      ta.hooks_before = (unsigned long long)total;
+      ensure_dyn_smem((const void*)k_cc_tail, kJumpSmallSmem);
+      void* args[] = {(void*)&ta};
+      CK(cudaLaunchCooperativeKernel((void*)k_cc_tail, dim3(num_sms()), dim3(kTailThreads), args,
+                                     kJumpSmallSmem, h.stream));
+      h.timer.end(h.stream);
+      h.read_box(h.dev_box, 29);
+      const int64_t tail_rounds = h.host_box[26];
+      if (h.host_box[28]) {
+        h.cc_lazy = false;
+        throw AlgoError("hooking failed to converge");
+      }
+      total = h.host_box[0];
+      tail_last_hooks = h.host_box[27];
+      h.stats.rounds = round + 1 + tail_rounds;
+      h.stats.step(n, 1);
+      for (int64_t t = 0; t < tail_rounds; ++t) h.stats.step(n, 0);
+      h.cc_lazy = true;
+      break;
+    }
     // per current root: list entry 4 B, slot 8 B, rep or next-list entry 4 B
     h.timer.begin(h.stream, "cc.apply", 16.0 * cur_roots);
     k_apply_roots<<<grid_for(n), kBlock, 0, h.stream>>>(in_list, rcount + in, n, rep, io, rl[out],
@@ -1218,7 +1418,7 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     }
     last_hooks = -total;  // completed when the next round reads the hook total
   }
-  last_hooks += total;
+  last_hooks = tail_last_hooks >= 0 ? tail_last_hooks : last_hooks + total;
   // Labels left lazy by the last productive round: the Euler vertex pass
   // resolves them itself with find_root when that round hooked few roots
   // (short chains); otherwise, and for every other caller, compress here.

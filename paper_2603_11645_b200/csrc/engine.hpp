@@ -169,7 +169,7 @@ class Handle {
   // Device counters block (256 x int64) zeroed per use by the caller; fixed
   // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,15] lr / tile ranking,
   // [16] pr bad mark, [17] edge-locality count, [18] pr crossing, [19] euler min-table
-  // dirty flag (persists across builds), [20,22] cc roots, [30] bfs, [40] validate,
+  // dirty flag (persists across builds), [20,22] cc roots, [24,29) cc tail rounds, [30] bfs, [40] validate,
   // [48] normalize, [50,53) capi/lr verify, [54,57) edge-upload input checks, [57] upload_ids, [128,160) jump-round flags.
   int64_t* dev_box = nullptr;
 

@@ -1358,7 +1358,14 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
       ta.hooks_before = (unsigned long long)total;
       ensure_dyn_smem((const void*)k_cc_tail, kJumpSmallSmem);
       void* args[] = {(void*)&ta};
-      CK(cudaLaunchCooperativeKernel((void*)k_cc_tail, dim3(num_sms()), dim3(kTailThreads), args,
+      // (one block per SM: measured on road, 8 or 32 blocks cost more than
+      // the cheaper barriers save -- the lazy finds need the parallelism)
+      static const int tail_blocks_env = [] {
+        const char* e = getenv("RSTG_CC_TAIL_BLOCKS");
+        return e ? atoi(e) : 0;
+      }();
+      const int tail_blocks = tail_blocks_env > 0 ? std::min(tail_blocks_env, num_sms()) : num_sms();
+      CK(cudaLaunchCooperativeKernel((void*)k_cc_tail, dim3(tail_blocks), dim3(kTailThreads), args,
                                      kJumpSmallSmem, h.stream));
       h.timer.end(h.stream);
       h.read_box(h.dev_box, 29);

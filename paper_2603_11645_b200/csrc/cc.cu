@@ -1013,6 +1013,13 @@ struct TailArgs {
                                 // round, [2] rounds exhausted flag
   int64_t rounds_left;          // (cc_forest.cpp:88: the round cap)
   unsigned long long hooks_before;  // hooks applied before round r's apply
+  // speculative launch (right after round r's hook, before the host reads
+  // its counters): the counts come from the device and the tail runs only
+  // if round r proposed, the round-0 roots list is short and few edges
+  // cross (out[3] = 1 when it ran)
+  bool speculative;
+  const unsigned long long* cross_dev;  // round r's crossing count (dev_box[1])
+  int64_t max_cross;
 };
 
 // appends v to list/count with one atomic per warp
@@ -1034,8 +1041,19 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_cc_tail(TailArgs a) {
   const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
   int in = a.in, cur = a.cur, mode = a.mode;
   unsigned long long rounds = 0, last_hooks = 0, hooks_before = a.hooks_before;
+  unsigned long long first = (unsigned long long)a.first_count;
+  if (a.speculative) {
+    const bool go = *(volatile int*)a.any != 0 &&
+                    *(volatile unsigned long long*)&a.rcount[0] <= (unsigned long long)kJumpSmallMax &&
+                    *(volatile const unsigned long long*)a.cross_dev <= (unsigned long long)a.max_cross;
+    if (gtid == 0) a.out[3] = go ? 1 : 0;
+    if (!go) return;  // (uniform: every thread read the same words)
+    first = *(volatile const unsigned long long*)a.cross_dev;
+    hooks_before = *(volatile unsigned long long*)a.io.counter;
+    grid.sync();  // (every thread has read the counters before any apply adds)
+  }
   if (gtid == 0) {
-    a.lcount[cur] = (unsigned long long)a.first_count;  // (read two barriers later)
+    a.lcount[cur] = first;  // (read two barriers later)
     a.out[2] = 0;
   }
   for (;;) {
@@ -1258,6 +1276,50 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     return e ? atoi(e) != 0 : true;
   }();
   int64_t total = 0, last_hooks = 0, prev_total = 0, tail_last_hooks = -1;
+  // the device-side tail rounds (k_cc_tail)
+  static const bool tail_on = [] {
+    const char* e = getenv("RSTG_CC_TAIL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  auto tail_args = [&](int64_t first_count, int cur, int in_idx, int next_mode,
+                       int64_t hooks_before, int64_t at_round, bool speculative) {
+    unsigned long long* box = reinterpret_cast<unsigned long long*>(h.dev_box);
+    TailArgs ta{};
+    ta.io = io;
+    ta.rep = rep;
+    ta.elist[0] = h.ws<uint32_t>(WS_ELIST0, m);
+    ta.elist[1] = h.ws<uint32_t>(WS_ELIST1, m);
+    ta.lcount = box + 24;
+    ta.first_count = first_count;
+    ta.cur = cur;
+    ta.rl[0] = rl[0];
+    ta.rl[1] = rl[1];
+    ta.rl[2] = rl[2];
+    ta.rcount = rcount;
+    ta.in = in_idx;
+    ta.mode = next_mode;
+    ta.any = any;
+    ta.out = box + 26;
+    ta.rounds_left = std::max<int64_t>(n + 1 - at_round, 1);
+    ta.hooks_before = (unsigned long long)hooks_before;
+    ta.speculative = speculative;
+    ta.cross_dev = box + 1;
+    ta.max_cross = std::min<int64_t>(kTailMaxEdges, n / 4);
+    return ta;
+  };
+  auto launch_tail = [&](TailArgs& ta) {
+    ensure_dyn_smem((const void*)k_cc_tail, kJumpSmallSmem);
+    void* args[] = {(void*)&ta};
+    // (one block per SM: measured on road, 8 or 32 blocks cost more than
+    // the cheaper barriers save -- the lazy finds need the parallelism)
+    static const int tail_blocks_env = [] {
+      const char* e = getenv("RSTG_CC_TAIL_BLOCKS");
+      return e ? atoi(e) : 0;
+    }();
+    const int blocks = tail_blocks_env > 0 ? std::min(tail_blocks_env, num_sms()) : num_sms();
+    CK(cudaLaunchCooperativeKernel((void*)k_cc_tail, dim3(blocks), dim3(kTailThreads), args,
+                                   kJumpSmallSmem, h.stream));
+  };
   for (;; ++round) {
     if (round > n + 1) {
       h.cc_lazy = false;
@@ -1275,9 +1337,34 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     // (the hook clears the count this round's apply appends to)
     cc_hook_round(h, mode, rep, slot, counter + 1, any, rcount + out);
     h.timer.end(h.stream);
+    // The first listed round on a sparse graph: launch the device-side tail
+    // right away; it checks its own conditions on the device and returns at
+    // once when they fail, so the host reads this round's counters once.
+    const bool spec_tail = tail_on && !ex && have_r0 && jump_roots && h.cc_round == 1 &&
+                           h.cc_filter_from == 1 && m > 0;
+    TailArgs ta{};
+    if (spec_tail) {
+      h.timer.begin(h.stream, "cc.tail", 0.0);
+      ta = tail_args(-1, /*cur=*/0, in, mode ^ 1, total, round, true);
+      launch_tail(ta);
+      h.timer.end(h.stream);
+    }
     // hooks so far, crossing, any; [20] the round-0 roots count, [20 + in]
     // the current roots count (same read)
-    h.read_box(reinterpret_cast<int64_t*>(counter), 23);
+    h.read_box(reinterpret_cast<int64_t*>(counter), spec_tail ? 30 : 23);
+    if (spec_tail && h.host_box[29]) {  // the tail ran every remaining round
+      if (h.host_box[28]) {
+        h.cc_lazy = false;
+        throw AlgoError("hooking failed to converge");
+      }
+      total = h.host_box[0];
+      tail_last_hooks = h.host_box[27];
+      h.stats.rounds = round + 1 + h.host_box[26];
+      h.stats.step(n, 1);
+      for (int64_t t = 0; t < h.host_box[26]; ++t) h.stats.step(n, 0);
+      h.cc_lazy = true;
+      break;
+    }
     if (h.cc_round >= 1 && m > 0) h.timer.add_bytes(hook_phase, 4.0 * h.host_box[1]);
     const int64_t r0_count = have_r0 ? h.host_box[20] : 0;
     const int64_t cur_roots = have_r0 ? h.host_box[20 + in] : n;
@@ -1328,45 +1415,13 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
     // a round without proposals applies nothing (cc_forest.cpp:91)
     if (!proposed) break;
     // the remaining rounds on the device (see k_cc_tail) once they are small
-    static const bool tail_on = [] {
-      const char* e = getenv("RSTG_CC_TAIL");
-      return e ? atoi(e) != 0 : true;
-    }();
     if (tail_on && !ex && have_r0 && jump_roots && r0_count <= kJumpSmallMax && h.cc_active >= 0 &&
         h.cc_active <= kTailMaxEdges && h.cc_active <= n / 4) {
       // per round: the crossing list read and rewritten (4 + 4 B), each edge
       // 8 B and its two roots (~4 B each), the current roots' slots (16 B)
       h.timer.begin(h.stream, "cc.tail", 24.0 * (double)h.cc_active + 16.0 * (double)cur_roots);
-      unsigned long long* box = reinterpret_cast<unsigned long long*>(h.dev_box);
-      TailArgs ta;
-      ta.io = io;
-      ta.rep = rep;
-      ta.elist[0] = h.ws<uint32_t>(WS_ELIST0, m);
-      ta.elist[1] = h.ws<uint32_t>(WS_ELIST1, m);
-      ta.lcount = box + 24;
-      ta.first_count = h.cc_active;
-      ta.cur = h.cc_list;
-      ta.rl[0] = rl[0];
-      ta.rl[1] = rl[1];
-      ta.rl[2] = rl[2];
-      ta.rcount = rcount;
-      ta.in = in;
-      ta.mode = mode ^ 1;
-      ta.any = any;
-      ta.out = box + 26;
-      ta.rounds_left = std::max<int64_t>(n + 1 - round, 1);
-      ta.hooks_before = (unsigned long long)total;
-      ensure_dyn_smem((const void*)k_cc_tail, kJumpSmallSmem);
-      void* args[] = {(void*)&ta};
-      // (one block per SM: measured on road, 8 or 32 blocks cost more than
-      // the cheaper barriers save -- the lazy finds need the parallelism)
-      static const int tail_blocks_env = [] {
-        const char* e = getenv("RSTG_CC_TAIL_BLOCKS");
-        return e ? atoi(e) : 0;
-      }();
-      const int tail_blocks = tail_blocks_env > 0 ? std::min(tail_blocks_env, num_sms()) : num_sms();
-      CK(cudaLaunchCooperativeKernel((void*)k_cc_tail, dim3(tail_blocks), dim3(kTailThreads), args,
-                                     kJumpSmallSmem, h.stream));
+      TailArgs tb = tail_args(h.cc_active, h.cc_list, in, mode ^ 1, total, round, false);
+      launch_tail(tb);
       h.timer.end(h.stream);
       h.read_box(h.dev_box, 29);
       const int64_t tail_rounds = h.host_box[26];

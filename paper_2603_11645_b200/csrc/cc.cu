@@ -181,6 +181,9 @@ __global__ void __launch_bounds__(kBlock)
 #define RSTG_JUMP_BATCH 4
 #endif
 constexpr int kJumpBatch = RSTG_JUMP_BATCH;  // entries in flight per thread in k_jump_x
+#ifndef RSTG_JUMP_HOPS
+#define RSTG_JUMP_HOPS 4  // pointer hops per entry per round of k_jump_x
+#endif
 
 // Level 1 (k_tile_resolve): each CTA owns a tile of kTileV consecutive
 // vertices held in shared memory and follows every pointer while it stays
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
       for (int k = 0; k < kJumpBatch; ++k) walk[k] = live[k];
 #pragma unroll
-      for (int hop = 1; hop < 4; ++hop) {
+      for (int hop = 1; hop < RSTG_JUMP_HOPS; ++hop) {
 #pragma unroll
         for (int k = 0; k < kJumpBatch; ++k) {
           if (!walk[k]) continue;
@@ -1407,8 +1410,8 @@ int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,
       proposed = *reinterpret_cast<int*>(h.host_box) != 0;
     }
     if (getenv("RSTG_CC_DEBUG"))
-      fprintf(stderr, "cc round %d mode %d: visited %.0f, hooks so far %lld, crossing %lld, lazy %d, r0 %lld\n",
-              round, mode, visited, (long long)total, (long long)h.host_box[1], (int)h.cc_lazy,
+      fprintf(stderr, "cc round %lld mode %d: visited %.0f, hooks so far %lld, crossing %lld, lazy %d, r0 %lld\n",
+              (long long)round, mode, visited, (long long)total, (long long)h.host_box[1], (int)h.cc_lazy,
               (long long)r0_count);
     cc_round_done(h, h.host_box[1]);
     h.stats.rounds = round + 1;

@@ -233,6 +233,11 @@ struct RoundIO {
   uint32_t* roots;              // round 0: vertices left as roots (nullable)
   unsigned long long* nroots;
   bool edge_sentinel;           // round-0 slots carry kKeyEdge (empty = isolated)
+  // PR-RST's first graft round (identity forest): a hooked v gets parent u
+  // and the skip structure's level 0 its entry (pr.cu)
+  int32_t* pr_parent;
+  const uint32_t* pr_pos;
+  uint32_t* pr_q0;
 };
 
 // Run shortcut before the in-tile doubling: a vertex whose pointer is its
@@ -407,6 +412,10 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
           if (io.tflag) {
             const uint32_t e = SRC == kSrcRound0 ? io.arc_edge[io.offsets[v]] : ekey - io.e_base;
             if (e < io.m_local) io.tflag[e] = 1;
+          }
+          if (SRC == kSrcRound0 && io.pr_parent) {
+            io.pr_parent[v] = u;
+            io.pr_q0[io.pr_pos[v]] = io.pr_pos[u];
           }
           if (io.link) {
             const uint32_t pa = (uint32_t)v, qa = io.eu.nslots + (uint32_t)v;  // pa: u -> v, qa: v -> u
@@ -1188,6 +1197,36 @@ static void exchange(Handle& h, const CcExchange& ex, int which, int64_t count) 
   // the caller's collective is enqueued on the handle's stream (the
   // caller sets it: rstg_set_stream) after the proposals
   if (ex.reduce_min(ex.ctx, which, count) != 0) throw AlgoError("slot exchange failed");
+}
+
+// PR-RST's first graft round from the CSR (pr.cu): the same round 0 as the
+// CC's (min-mode proposals over singleton reps = each vertex's first
+// neighbour), fused with its apply and shortcutting, with the graft's
+// reversal (singleton paths: parent[v] = u) done on the way. Returns the
+// grafts; the vertices left as roots go to `roots` (count in *nroots).
+int64_t pr_round0(Handle& h, int32_t* rep, int32_t* parent, const uint32_t* pos, uint32_t* q0,
+                  uint32_t* roots, unsigned long long* nroots) {
+  const int64_t n = h.g.n;
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(h.dev_box);
+  RoundIO io{};
+  io.e_base = (uint32_t)h.g.e_base;
+  io.m_local = (uint32_t)h.g.m;
+  io.counter = counter;
+  io.offsets = h.g.offsets;
+  io.nbrs = h.g.nbrs;
+  io.arc_edge = h.g.arc_edge;
+  io.edges = h.g.edges;
+  io.roots = roots;
+  io.nroots = nroots;
+  io.pr_parent = parent;
+  io.pr_pos = pos;
+  io.pr_q0 = q0;
+  ZeroRanges z{};
+  z.add(counter, sizeof(unsigned long long));
+  z.add(nroots, sizeof(unsigned long long));
+  resolve_round(h, rep, n, kSrcRound0, io, &z);
+  h.read_box(h.dev_box, 1);
+  return h.host_box[0];
 }
 
 int64_t cc_exact(Handle& h, int32_t* rep, uint8_t* tflag, const EulerIO* euler,

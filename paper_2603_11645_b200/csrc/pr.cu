@@ -56,6 +56,8 @@ void cc_reset_rounds(Handle& h);
 void compress_via_roots(Handle& h, int32_t* rep, int64_t n, const uint32_t* roots,
                         const unsigned long long* nroots);
 void launch_compress2(Handle& h, int32_t* rep, int64_t n);
+int64_t pr_round0(Handle& h, int32_t* rep, int32_t* parent, const uint32_t* pos, uint32_t* q0,
+                  uint32_t* roots, unsigned long long* nroots);
 
 namespace {
 
@@ -591,7 +593,27 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   const uint32_t* in_list = nullptr;  // nullptr: every vertex is a root
   int out = 0;
   int mode = 0;
-  for (int64_t round = 0;; ++round) {
+  int64_t first_round = 0;
+  if (h.g.has_csr() && h.g.m > 0 && n > 0) {
+    // The first graft round from the CSR, fused with its resolve, update,
+    // reversal (singleton paths) and jump: the CC's round-0 tile pass
+    // (cc.cu pr_round0). Grafts, parents and converged reps are those of the
+    // round-0 loop below; the roots left go to rl[0].
+    h.timer.begin(s, "pr.round0", 4.0 * (n + 1) + 8.0 * n + 12.0 * n);
+    const int64_t grafts0 = pr_round0(h, rep, parent, pos, Q, rl[0], pc + P_NROOTS_IN);
+    h.timer.end(s);
+    // batched_jump's guard (pr_rst.cpp:218-219) fires once a graft happened
+    if (grafts0 > 0 && !batch_ok) throw AlgoError("jump batch out of range [1, 20]");
+    h.stats.step(n, 4);
+    cc_round_done(h, 0);  // (the next graft round starts the active-edge lists)
+    in_list = rl[0];
+    out = 1;
+    mode = 1;
+    identity = false;
+    forest_dirty = true;
+    first_round = 1;
+  }
+  for (int64_t round = first_round;; ++round) {
     if (round > n + 1) throw AlgoError("grafting failed to converge");
     h.timer.begin(s, "pr.graft", 0.0);
     // graft proposals with active-edge filtering (as in the CC: an edge

@@ -528,13 +528,15 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* S, const ui
     uint32_t* seg;  // up-mapping of this level's nodes
     uint32_t* off;
     int64_t bound;  // node-count bound (grid sizing)
-    int tile;       // nodes per tile: 8K (two CTAs per SM) while a level
-                    // fills the GPU, 16K (one CTA per SM, twice the
-                    // contraction) once one wave of 16K tiles covers it
+    int tile;       // nodes per tile: 16K (one CTA per SM, twice the
+                    // contraction of 8K at two CTAs per SM; see big_tiles)
   } L[kMaxLevels + 2];
   L[0] = Level{exit1, seg1, len1, pre1, nullptr, nullptr, R, 0};
   const int contract = std::max(2, env_int("RSTG_LR_TILECONTRACT", 3));
-  static const int big_tiles = env_int("RSTG_LR_BIGTILES", 1);
+  // 16K-node tiles at every level (2; 1: only once one wave of them covers
+  // a level, 0: never): they contract 7-12x where 8K tiles contract ~4x, so
+  // one level fewer; measured on road, rulers_rank 0.293 -> 0.283 ms
+  static const int big_tiles = env_int("RSTG_LR_BIGTILES", 2);
   const int64_t big_max = big_tiles == 2 ? INT64_MAX
                           : big_tiles ? (int64_t)num_sms() * kBigLevelNodes : 0;
   int top = 0;

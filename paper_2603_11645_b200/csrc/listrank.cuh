@@ -107,7 +107,6 @@ struct TileRank {
   const uint32_t* seg;       // 2N segment id per arc
   const uint16_t* off;       // 2N offset within the segment
   const uint32_t* segstart;  // rank of each segment's first arc
-  const uint32_t* S;         // the tour's successors (segment exits are last arcs)
   // The upper levels ran on a grid sized from the previous build's segment
   // count: their overflow flag and the real count are copied to
   // host_box[32..49) asynchronously; tile_rank_settle() checks them after

@@ -464,8 +464,7 @@ __global__ void __launch_bounds__(kThreads, kNodes > 8192 ? 1 : 2048 / kThreads)
 
 // next segment of each segment: the one its exit arc heads
 __global__ void k_seg_link(const unsigned long long* nseg, const uint32_t* __restrict__ seg_exit,
-                           const uint32_t* __restrict__ S, const uint32_t* __restrict__ seg,
-                           uint32_t* __restrict__ seg_next) {
+                           const uint32_t* __restrict__ seg, uint32_t* __restrict__ seg_next) {
   const int64_t R = (int64_t)*nseg;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -617,11 +616,10 @@ static bool tile_prefix_levels(Handle& h, int64_t R, const uint32_t* S, const ui
 }
 
 // The segments' ranks by the generic list ranking (levels that stall).
-static void tile_fallback(Handle& h, const LrParams& Q, int64_t R, const uint32_t* S,
-                          const uint32_t* seg,
+static void tile_fallback(Handle& h, const LrParams& Q, int64_t R, const uint32_t* seg,
                           const uint32_t* seg_exit, const uint32_t* seg_len, uint32_t* seg_next,
                           uint32_t* segstart, const unsigned long long* nseg) {
-  k_seg_link<<<grid_for(R), kBlock, 0, h.stream>>>(nseg, seg_exit, S, seg, seg_next);
+  k_seg_link<<<grid_for(R), kBlock, 0, h.stream>>>(nseg, seg_exit, seg, seg_next);
   CK_LAUNCH();
   list_prefix(h, Q, R, seg_next, seg_len, segstart, 0, false, nullptr);
 }
@@ -702,14 +700,14 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
     if (tile_prefix_levels(h, R, S, seg, seg_exit, seg_len, segstart, dbg, deferred))
       late = deferred;
     else
-      tile_fallback(h, Q, R, S, seg, seg_exit, seg_len, seg_next, segstart, nseg);
+      tile_fallback(h, Q, R, seg, seg_exit, seg_len, seg_next, segstart, nseg);
   } else {
     if (deferred) {  // (the exact count is needed here)
       h.read_box(h.dev_box + 8, 1);
       R = h.host_box[0];
       h.tile_segments = R;
     }
-    tile_fallback(h, Q, R, S, seg, seg_exit, seg_len, seg_next, segstart, nseg);
+    tile_fallback(h, Q, R, seg, seg_exit, seg_len, seg_next, segstart, nseg);
   }
   const int64_t launches = h.stats.launches;
   h.stats = before;
@@ -720,7 +718,7 @@ TileRank lr_rank_tiles(Handle& h, const LrParams& P, int64_t N, const uint32_t* 
   h.stats.steps += rounds;
   h.stats.work += Rexp * rounds;
   h.timer.end(s);
-  return TileRank{seg, off, segstart, S, late};
+  return TileRank{seg, off, segstart, late};
 }
 
 bool tile_rank_settle(Handle& h, const LrParams& P, int64_t N, const TileRank& tr) {
@@ -732,7 +730,7 @@ bool tile_rank_settle(Handle& h, const LrParams& P, int64_t N, const TileRank& t
   const int64_t E = 2 * N;
   LrParams Q = P;
   Q.cap = std::max<int64_t>(P.cap, E + 1);
-  tile_fallback(h, Q, R, tr.S, tr.seg, h.ws<uint32_t>(WS_RNEXT, E + 1), h.ws<uint32_t>(WS_RLEN, E + 1),
+  tile_fallback(h, Q, R, tr.seg, h.ws<uint32_t>(WS_RNEXT, E + 1), h.ws<uint32_t>(WS_RLEN, E + 1),
                 h.ws<uint32_t>(WS_RPOS, E + 1), const_cast<uint32_t*>(tr.segstart),
                 reinterpret_cast<unsigned long long*>(h.dev_box) + 8);
   return true;

@@ -594,7 +594,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   int out = 0;
   int mode = 0;
   int64_t first_round = 0;
-  if (h.g.has_csr() && h.g.m > 0 && n > 0) {
+  if (h.g.has_csr() && !h.g.csr_pending && h.g.m > 0 && n > 0) {  // (a built CSR)
     // The first graft round from the CSR, fused with its resolve, update,
     // reversal (singleton paths) and jump: the CC's round-0 tile pass
     // (cc.cu pr_round0). Grafts, parents and converged reps are those of the

@@ -596,6 +596,23 @@ def test_handle_reuse_unconsumed_upload(rst, O):
     h.close()
 
 
+@pytest.mark.parametrize("algo", [2, 1, 0])
+@pytest.mark.parametrize("spec,root", [(("road", 60), 0), (("kron", 11), 5), (("grid", 30, 40), 77)])
+def test_edge_list_upload_each_strategy_first(rst, O, spec, root, algo):
+    # an edge-list upload leaves the CSR pending (built on first use): each
+    # strategy run FIRST on such a handle takes its no-CSR path (PR-RST: the
+    # graft loop instead of the fused round-0 pass; cc-euler: keyed round 0)
+    g = O.gen(*spec)
+    h = rst.DeviceGraph.from_host(g.n, np.stack([g.eu, g.ev], 1))
+    p, r, _, _ = h.run(algo, root)
+    ep, er, _ = O.run(g, algo, root)
+    assert np.array_equal(p, ep) and np.array_equal(r, er)
+    # and then the others on the same handle
+    for a2 in (0, 1, 2):
+        assert np.array_equal(h.run(a2, root)[0], O.run(g, a2, root)[0])
+    h.close()
+
+
 def test_edge_upload_rejects_bad_edge_lists(rst, O):
     # build_csr's argument checks (graph.cpp:145-156),
     # on the device, in the reference's order, for the edge-list upload

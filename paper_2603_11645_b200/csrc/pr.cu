@@ -42,9 +42,13 @@
 // Tree edges and converged reps equal the CC's (same proposals, same
 // rounds); the parents are those of the reference's path reversals.
 // The designated root's tree is re-rooted at the end (:298-303).
+#include <cooperative_groups.h>
+
 #include <cub/cub.cuh>
 
 #include "engine.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace rstg {
 
@@ -131,6 +135,29 @@ __device__ __forceinline__ int level_of_pos(const uint32_t* sC, int K, uint32_t 
   int l = 0;
   while (l < K && x < sC[l + 1]) ++l;
   return l;
+}
+
+// Levels k0 .. K of the rebuild in ONE cooperative launch (small levels:
+// C_k below ~2^18 positions, L2-resident; a grid barrier between levels).
+__global__ void __launch_bounds__(kBlock) k_pr_rebuild_tail(int k0, PrLv L, uint32_t* Q) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+  for (int k = k0; k <= L.K && L.C[k] > 0; ++k) {
+    const uint32_t* __restrict__ in = Q + L.off[k - 1];
+    uint32_t* __restrict__ out = Q + L.off[k];
+    const uint32_t lo = L.C[k], hi = L.C[k - 1];
+    for (int64_t i = gtid; i < (int64_t)lo; i += gsize) {
+      uint32_t x = ld_cg(&in[i]);  // (written by the previous level, this launch)
+      while (x >= lo && x < hi) {
+        const uint32_t y = ld_cg(&in[x]);
+        if (y == x) break;
+        x = y;
+      }
+      out[i] = x;
+    }
+    grid.sync();
+  }
 }
 
 // pos[byl[i]] = i (once per graph size, with the level order)
@@ -542,9 +569,30 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   auto rebuild = [&]() {
     h.timer.begin(s, "pr.rebuild", 0.0);
     double bytes = 0;  // (level 0 is kept current by the parent writes)
+    // big levels one launch each; the small ones (C_k < 2^18) in one
+    // cooperative launch (they were bound by launch latency)
+    static const int64_t small_level = [] {
+      const char* e = getenv("RSTG_PR_SMALL_LEVEL");
+      return e ? atoll(e) : (int64_t{1} << 18);
+    }();
+    static int tail_blocks = 0;
+    if (!tail_blocks) {
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_rebuild_tail, kBlock, 0));
+      tail_blocks = std::max(1, std::min(per_sm, 4)) * num_sms();
+    }
     for (int k = 1; k <= K && C[k] > 0; ++k) {
       // per position of level >= k: the level-(k-1) entry in (4 B), ~1 more
       // hop (4 B), the entry out (4 B)
+      if (C[k] < small_level) {
+        for (int kk = k; kk <= K && C[kk] > 0; ++kk) bytes += (double)C[kk] * 12.0;
+        int k0 = k;
+        void* args[] = {(void*)&k0, (void*)&L, (void*)&Q};
+        CK(cudaLaunchCooperativeKernel((void*)k_pr_rebuild_tail, dim3(tail_blocks), dim3(kBlock),
+                                       args, 0, s));
+        h.stats.step(C[k]);
+        break;
+      }
       bytes += (double)C[k] * 12.0;
       (n > (int64_t{1} << 22) ? k_pr_rebuild<4> : k_pr_rebuild<1>)
           <<<grid_for(C[k]), kBlock, 0, s>>>(k, L, Q);
@@ -565,6 +613,9 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     h.stats.step(n);
     // level-j walkers are the queues of levels > j: one block row each,
     // sized by the expected queue (n / 2^(b+1) path vertices at most)
+    // (one launch per level: a single cooperative launch with a grid
+    // barrier per level measured slower -- the gap walks dominate, not the
+    // launches)
     if (!identity)
       for (int j = K - 1; j >= 0; --j) {
         const int64_t expect = std::max<int64_t>(C[j + 1] - C[j + 2], 1);

@@ -399,6 +399,50 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// The top descent levels (K-1 .. jmin) in ONE block, a block barrier
+// between levels: their walkers are few (a path holds ~2^-j of its
+// vertices at level >= j), so one launch per level was launch latency.
+__global__ void __launch_bounds__(1024)
+    k_pr_descend_top(int jmin, const uint32_t* __restrict__ Q, PrLv L,
+                     const uint32_t* __restrict__ byl, const uint32_t* __restrict__ pos,
+                     uint8_t* mark, uint32_t* mk, const unsigned long long* __restrict__ bbase,
+                     unsigned long long* mcnt) {
+  __shared__ unsigned long long s_pre[kMaxLvl + 3];
+  const int K = L.K;
+  for (int j = K - 1; j >= jmin; --j) {
+    if (threadIdx.x == 0) {  // walkers: buckets j+1 .. K
+      unsigned long long acc = 0;
+      for (int b = j + 1; b <= K; ++b) {
+        s_pre[b] = acc;
+        acc += *(volatile unsigned long long*)&mcnt[b];
+      }
+      s_pre[K + 1] = acc;
+    }
+    __syncthreads();
+    const unsigned long long total = s_pre[K + 1];
+    const uint32_t* __restrict__ in = Q + L.off[j];
+    const uint32_t lo = L.C[j + 1], hi = L.C[j];
+    for (unsigned long long t = threadIdx.x; t < total; t += blockDim.x) {
+      int b = j + 1;
+      while (b < K && t >= s_pre[b + 1]) ++b;
+      const uint32_t a = mk[bbase[b] + (t - s_pre[b])];
+      const uint32_t pa = pos[a];
+      uint32_t x = in[pa];
+      if (x == pa) continue;  // a root
+      while (x >= lo && x < hi) {  // level exactly j
+        const uint32_t y = in[x];
+        if (y == x) break;
+        const uint32_t vx = byl[x];
+        mark[vx] = 1;
+        enqueue(mk, bbase, mcnt, j, (int32_t)vx);
+        x = y;
+      }
+    }
+    __syncthreads();  // (level j's queue complete before level j - 1 reads it)
+    __threadfence_block();
+  }
+}
+
 // The check (pr_rst.cpp:281-288): each grafted root is marked and still a
 // root; records the smallest offending (r, u).
 __global__ void k_pr_check(const uint32_t* __restrict__ grafted, const uint32_t* __restrict__ seeds,
@@ -616,13 +660,24 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     // (one launch per level: a single cooperative launch with a grid
     // barrier per level measured slower -- the gap walks dominate, not the
     // launches)
-    if (!identity)
-      for (int j = K - 1; j >= 0; --j) {
+    if (!identity) {
+      static const int top_from = [] {
+        const char* e = getenv("RSTG_PR_TOP_LEVEL");
+        return e ? atoi(e) : 6;  // (road pr.mark 0.52 -> 0.43 ms at 6, 0.44 at 10)
+      }();
+      int j = K - 1;
+      if (top_from > 0 && K - 1 >= top_from) {
+        k_pr_descend_top<<<1, 1024, 0, s>>>(top_from, Q, L, byl, pos, mark, mk, bbase, mcnt);
+        h.stats.step(n);
+        j = top_from - 1;
+      }
+      for (; j >= 0; --j) {
         const int64_t expect = std::max<int64_t>(C[j + 1] - C[j + 2], 1);
         const unsigned gx = std::min<unsigned>(grid_for(expect), 2 * (unsigned)num_sms());
         k_pr_descend<<<dim3(gx, K - j), kBlock, 0, s>>>(j, Q, L, byl, pos, mark, mk, bbase, mcnt);
         h.stats.step(n);
       }
+    }
     CK_LAUNCH();
     h.timer.end(s);
   };

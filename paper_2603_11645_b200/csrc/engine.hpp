@@ -170,7 +170,7 @@ class Handle {
   // regions: [0,3] cc, [4] euler roots, [5,7] cc exit set, [8,15] lr / tile ranking,
   // [16] pr bad mark, [17] edge-locality count, [18] pr crossing, [19] euler min-table
   // dirty flag (persists across builds), [20,22] cc roots, [24,29) cc tail rounds, [30] bfs, [40] validate,
-  // [48] normalize, [50,53) capi/lr verify, [54,57) edge-upload input checks, [57] upload_ids, [128,160) jump-round flags.
+  // [48] normalize, [50,53) capi/lr verify, [54,57) edge-upload input checks, [57] upload_ids, [60] pr short path, [128,160) jump-round flags.
   int64_t* dev_box = nullptr;
 
   // Copies `count` int64 device values into host_box and syncs the stream.

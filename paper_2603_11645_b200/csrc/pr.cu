@@ -443,6 +443,36 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// mark_path for ONE seed by walking the parents (level 0 of the skip
+// structure, kept current by every parent write) -- the re-rooting's path
+// when it is short: no rebuild of the stale upper levels for one path.
+// Marks and queues exactly what the ascent + descent would (every ancestor
+// of u, by exact level); *ok = 0 when the path is longer than `cap`.
+__global__ void k_pr_short_path(int32_t u, const uint32_t* __restrict__ q0, PrLv L,
+                                const uint32_t* __restrict__ byl, const uint32_t* __restrict__ pos,
+                                uint8_t* mark, uint32_t* mk, const unsigned long long* __restrict__ bbase,
+                                unsigned long long* mcnt, int cap, int* ok) {
+  auto level_of = [&](uint32_t x) {
+    int l = 0;
+    while (l < L.K && x < L.C[l + 1]) ++l;
+    return l;
+  };
+  uint32_t c = pos[u];
+  enqueue(mk, bbase, mcnt, level_of(c), u);  // (the seed, as the ascent queues it)
+  for (int hop = 0; hop < cap; ++hop) {
+    const uint32_t x = q0[c];
+    if (x == c) {  // c is the tree root
+      *ok = 1;
+      return;
+    }
+    const uint32_t vx = byl[x];
+    mark[vx] = 1;
+    enqueue(mk, bbase, mcnt, level_of(x), (int32_t)vx);
+    c = x;
+  }
+  *ok = 0;
+}
+
 // The check (pr_rst.cpp:281-288): each grafted root is marked and still a
 // root; records the smallest offending (r, u).
 __global__ void k_pr_check(const uint32_t* __restrict__ grafted, const uint32_t* __restrict__ seeds,
@@ -815,8 +845,23 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
     k_set_u64<<<1, 1, 0, s>>>(pc + P_NGRAFT, 1ull);
     k_set_u8<<<1, 1, 0, s>>>(mark + root, 1);
     CK_LAUNCH();
+    bool marked = false;
+    if (forest_dirty) {
+      // one path: walk it on the (current) parents while it is short,
+      // instead of rebuilding the whole skip structure for it
+      const char* cap_env = getenv("RSTG_PR_SHORT_PATH");  // (per call: the tests force the fallback)
+      const int cap = cap_env ? atoi(cap_env) : 512;
+      if (cap > 0) {
+        int* ok = reinterpret_cast<int*>(h.dev_box + 60);  // (dev_box [60]: the short-path flag)
+        CK(cudaMemsetAsync(mcnt, 0, (kMaxLvl + 2) * sizeof(unsigned long long), s));
+        k_pr_short_path<<<1, 1, 0, s>>>(root, Q, L, byl, pos, mark, mk, bbase, mcnt, cap, ok);
+        CK_LAUNCH();
+        h.read_box(h.dev_box + 60, 1);
+        marked = *reinterpret_cast<const int*>(h.host_box) != 0;
+      }
+    }
     h.timer.end(s);
-    run_marking();
+    if (!marked) run_marking();
     h.timer.begin(s, "pr.reroot", 0.0);
     k_pr_check<<<1, 32, 0, s>>>(grafted, seeds, pc + P_NGRAFT, mark, parent, bad_mark);
     k_set_i32<<<1, 1, 0, s>>>(scratch + root, root);  // reverse_path :212

@@ -86,6 +86,22 @@ def test_pr_golden(rst, O):
     assert list(dev_graph(rst, g).run(2, 0)[0]) == [0, 0, 1]
 
 
+@pytest.mark.parametrize("cap", ["1", "3", "0"])
+def test_pr_reroot_short_path_and_fallback(rst, O, monkeypatch, cap):
+    # the re-rooting's path walked on the parents when short (cap hops), else
+    # the skip structure rebuilt and the path marked by ascent + descent:
+    # both give the reference's parents
+    monkeypatch.setenv("RSTG_PR_SHORT_PATH", cap)
+    for spec, root in ((("grid", 20, 30), 377), (("road", 40), 999), (("kron", 10), 3),
+                       (("path", 3000), 1500)):
+        g = O.gen(*spec)
+        dg = dev_graph(rst, g)
+        p, r, _, _ = dg.run(2, root)
+        ep, er, _ = O.run(g, 2, root)
+        assert np.array_equal(p, ep) and np.array_equal(r, er), (spec, cap)
+        dg.close()
+
+
 def test_jump_batch_invariance(rst, O):
     # acceptance.cpp:386-401, test_pr.cpp:300-311
     g = O.gen("path", 4096)

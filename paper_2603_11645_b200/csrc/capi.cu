@@ -687,6 +687,7 @@ int rstg_k_hook_step(int64_t n, int64_t m, const int64_t* edges_uv, int mode, in
     h.read_box(reinterpret_cast<int64_t*>(bad), 1);
     if (*reinterpret_cast<int*>(h.host_box)) throw AlgoError("hooking ran on uncompressed labels");
     unsigned long long* sl = h.ws<unsigned long long>(WS_SLOT, n);
+    h.slots_clean = nullptr;  // (the caller's slot values go here)
     std::vector<unsigned long long> hs((size_t)n);
     for (int64_t v = 0; v < n; ++v)
       hs[(size_t)v] = (unsigned long long)slot[v];

@@ -434,6 +434,10 @@ __global__ void __launch_bounds__(kTileThreads, kTileV > 8192 ? 1 : 2)
             io.eu.S[pa] = nv;  // S[pa] = next(qa), S[qa] = next(pa)
             io.eu.S[qa] = nu;
           }
+        } else if (SRC == kSrcRound0 && io.pr_parent) {  // (a root: PR-RST's identity entries)
+          io.pr_parent[v] = (int32_t)v;
+          const uint32_t pv = io.pr_pos[v];
+          io.pr_q0[pv] = pv;
         }
       }
     }

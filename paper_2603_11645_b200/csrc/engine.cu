@@ -115,6 +115,7 @@ void* Handle::ws(int slot, size_t bytes) {
     if (slot == WS_MINV) minv_clean = nullptr;
     if (slot == WS_RHEAD) rhead_clean = nullptr;
     if (slot == WS_XBITS) xbits_clean = nullptr;
+    if (slot == WS_PR_SCRATCH || slot == WS_PR_ONPATH) pr_clean = nullptr;
     if (slot == WS_SLOT) slots_clean = nullptr;
     if (slot == WS_PR_BYL || slot == WS_PR_CBASE || slot == WS_PR_POS) pr_levels_n = -1;
     if (b.first) {
@@ -133,6 +134,7 @@ void Handle::release(int slot) {
   if (slot == WS_MINV) minv_clean = nullptr;
   if (slot == WS_RHEAD) rhead_clean = nullptr;
   if (slot == WS_XBITS) xbits_clean = nullptr;
+  if (slot == WS_PR_SCRATCH || slot == WS_PR_ONPATH) pr_clean = nullptr;
   if (slot == WS_SLOT) slots_clean = nullptr;
   if (slot == WS_PR_BYL || slot == WS_PR_CBASE || slot == WS_PR_POS) pr_levels_n = -1;
   if (b.first) {

@@ -146,6 +146,11 @@ class Handle {
   // after a completed pass: the exit-set jump clears what the tiles set
   const void* xbits_clean = nullptr;
   int64_t xbits_clean_words = 0;
+  // PR-RST's scratch (-1) and mark (0) arrays as a completed build leaves
+  // them, for their first pr_clean_n entries
+  const void* pr_clean = nullptr;
+  const void* pr_clean_mark = nullptr;
+  int64_t pr_clean_n = 0;
   // PR-RST skip levels (pr.cu): vertex order by level and the counts C_k
   // of vertices of level >= k, valid for graphs of pr_levels_n vertices
   int64_t pr_levels_n = -1;

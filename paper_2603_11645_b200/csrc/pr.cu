@@ -86,6 +86,8 @@ __device__ __forceinline__ uint32_t vertex_level(uint32_t v, int K) {
   x ^= x >> 31;
   return min((uint32_t)__ffsll((long long)~x) - 1u, (uint32_t)K);  // trailing ones
 }
+// (the identity forest: parent/rep unless the fused round 0 writes them;
+// scratch/mark/slot unless the last build left them clean)
 __global__ void k_pr_init(int64_t n, int K, int32_t* parent, int32_t* rep, int32_t* scratch,
                           uint8_t* mark, uint8_t* lv, unsigned long long* slot,
                           unsigned long long* hist) {
@@ -94,10 +96,12 @@ __global__ void k_pr_init(int64_t n, int K, int32_t* parent, int32_t* rep, int32
   __syncthreads();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    parent[v] = rep[v] = (int32_t)v;
-    scratch[v] = -1;
-    mark[v] = 0;
-    slot[v] = kKeyInf;
+    if (parent) parent[v] = rep[v] = (int32_t)v;
+    if (scratch) {
+      scratch[v] = -1;
+      mark[v] = 0;
+    }
+    if (slot) slot[v] = kKeyInf;
     if (hist) {  // (the level order is being built: levels and their histogram)
       const uint32_t l = vertex_level((uint32_t)v, K);
       lv[v] = (uint8_t)l;
@@ -557,7 +561,6 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   uint32_t* rlist = h.ws<uint32_t>(WS_CCROOTS, 3 * n + 3);
   uint32_t* rl[2] = {rlist, rlist + n + 1};
   unsigned long long* slot = h.ws<unsigned long long>(WS_SLOT, n);
-  h.slots_clean = nullptr;  // graft rounds leave slots of their own
   cc_reset_rounds(h);       // (graft rounds use the CC's active-edge lists)
   h.round0_slots = nullptr;  // (and overwrite an upload's round-0 keys)
   unsigned long long* pc =
@@ -575,11 +578,25 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   // The level order (vertices sorted by descending level, ids ascending
   // within a level, so level-k walks sweep ids in order) and the counts C_k
   // depend on n only: built once per graph size, kept with the handle.
-  h.timer.begin(s, "pr.init", (4.0 + 4.0 + 4.0 + 1.0 + 8.0 + 1.0) * n);
+  // What a build leaves behind is the identity's state again for scratch
+  // (-1), mark (0) and the slots (INF) -- every entry it sets is reset by the
+  // reversal or the update that consumes it -- and the fused round 0 (a
+  // built CSR) writes every parent and rep itself: the init writes only what
+  // is not known to hold (nothing, on a repeated build of a CSR graph).
+  const bool fused0 = h.g.has_csr() && !h.g.csr_pending && h.g.m > 0 && n > 0;
+  const bool slots_ok = h.slots_clean == slot && n <= h.slots_clean_n;
+  const bool marks_ok = h.pr_clean == scratch && h.pr_clean_mark == mark && n <= h.pr_clean_n;
+  h.slots_clean = nullptr;  // graft rounds use the slots (clean again at the end)
+  h.pr_clean = nullptr;
+  h.timer.begin(s, "pr.init", (fused0 ? 0.0 : 8.0 * n) + (marks_ok ? 0.0 : 5.0 * n) +
+                                  (slots_ok ? 0.0 : 8.0 * n));
   CK(cudaMemsetAsync(pc, 0, (P_NWORDS + 2 * (kMaxLvl + 2)) * sizeof(unsigned long long), s));
   const bool cached = h.pr_levels_n == n && h.pr_levels_byl == byl && (int)h.pr_levels_C.size() == K + 2;
-  k_pr_init<<<g, kBlock, 0, s>>>(n, K, parent, rep, scratch, mark, lv, slot, cached ? nullptr : cursor);
-  CK_LAUNCH();
+  if (!cached || !fused0 || !marks_ok || !slots_ok) {
+    k_pr_init<<<g, kBlock, 0, s>>>(n, K, fused0 ? nullptr : parent, rep, marks_ok ? nullptr : scratch,
+                                   mark, lv, slots_ok ? nullptr : slot, cached ? nullptr : cursor);
+    CK_LAUNCH();
+  }
   CK(cudaMemsetAsync(bad_mark, 0xFF, sizeof(unsigned long long), s));
   unsigned long long* cbase = h.ws<unsigned long long>(WS_PR_CBASE, kMaxLvl + 2);
   if (!cached) {
@@ -627,7 +644,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   // off[k], C[k] entries -- sum_k C[k] = n + the sum of the levels, about
   // 2n (sized exactly: the sum is random)
   uint32_t* Q = h.ws<uint32_t>(WS_PR_ANC, (size_t)L.off[K + 1] + 1);
-  if (n > 0) {
+  if (n > 0 && !fused0) {  // (the fused round 0 writes every level-0 entry)
     k_pr_q0_identity<<<g, kBlock, 0, s>>>(n, Q);
     CK_LAUNCH();
   }
@@ -730,7 +747,7 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
   int out = 0;
   int mode = 0;
   int64_t first_round = 0;
-  if (h.g.has_csr() && !h.g.csr_pending && h.g.m > 0 && n > 0) {  // (a built CSR)
+  if (fused0) {  // (a built CSR)
     // The first graft round from the CSR, fused with its resolve, update,
     // reversal (singleton paths) and jump: the CC's round-0 tile pass
     // (cc.cu pr_round0). Grafts, parents and converged reps are those of the
@@ -877,6 +894,13 @@ void pr_rst(Handle& h, int32_t root, int64_t jump_batch, int32_t* parent) {
                       " is not the root above " + std::to_string((uint32_t)bm));
     if (badrev) throw AlgoError("reversal found a marked vertex with no source");
   }
+  // every slot, scratch entry and mark this build set was reset by the step
+  // that consumed it: the next build may skip their fills
+  h.slots_clean = slot;
+  h.slots_clean_n = n;
+  h.pr_clean = scratch;
+  h.pr_clean_mark = mark;
+  h.pr_clean_n = n;
 }
 
 }  // namespace rstg

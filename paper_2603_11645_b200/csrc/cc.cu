@@ -663,7 +663,9 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
       z.add(xbits, (size_t)words * sizeof(uint32_t));
     h.xbits_clean = nullptr;
     z.add(h.dev_box + 5, 3 * sizeof(int64_t));
-    k_zero_ranges<<<(unsigned)std::min<int64_t>(1184, (words + 1023) / 1024 + 1), 1024, 0,
+    uint32_t most = 0;  // (the grid covers the largest range actually zeroed)
+    for (int r = 0; r < z.k; ++r) most = std::max(most, z.words[r]);
+    k_zero_ranges<<<(unsigned)std::min<int64_t>(1184, ((int64_t)most + 1023) / 1024), 1024, 0,
                     h.stream>>>(z);
     CK_LAUNCH();
   }

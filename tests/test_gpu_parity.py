@@ -86,12 +86,14 @@ def test_pr_golden(rst, O):
     assert list(dev_graph(rst, g).run(2, 0)[0]) == [0, 0, 1]
 
 
-@pytest.mark.parametrize("cap", ["1", "3", "0"])
+@pytest.mark.parametrize("cap", ["1", "3", "0", "100000"])
 def test_pr_reroot_short_path_and_fallback(rst, O, monkeypatch, cap):
-    # the re-rooting's path walked on the parents when short (cap hops), else
-    # the skip structure rebuilt and the path marked by ascent + descent:
-    # both give the reference's parents
+    # the re-rooting's path, and every round's paths, walked on the parents
+    # when short (cap hops), else the skip structure rebuilt and the paths
+    # marked by ascent + descent: both give the reference's parents
     monkeypatch.setenv("RSTG_PR_SHORT_PATH", cap)
+    monkeypatch.setenv("RSTG_PR_SHORT_PATHS", cap)
+    monkeypatch.setenv("RSTG_PR_SHORT_PATHS_ROOTS", "1000000000")
     for spec, root in ((("grid", 20, 30), 377), (("road", 40), 999), (("kron", 10), 3),
                        (("path", 3000), 1500)):
         g = O.gen(*spec)

@@ -129,6 +129,22 @@ def test_jump_batch_out_of_range(rst, O):
         dev_graph(rst, g).run(2, 0, 0)
 
 
+def test_handle_after_failed_builds(rst, O):
+    # a build that throws midway (after its first grafts) leaves the state
+    # a repeated build skips re-initialising (slots, scratch, marks) unknown:
+    # the next builds on the same handle must re-initialise and stay exact
+    g = O.gen("road", 60)
+    dg = dev_graph(rst, g)
+    ep = {a: O.run(g, a, 7)[0] for a in (0, 1, 2)}
+    for _ in range(2):
+        assert np.array_equal(dg.run(2, 7)[0], ep[2])
+        with pytest.raises(rst.RSTError, match=r"jump batch out of range"):
+            dg.run(2, 7, 0)
+        for a in (2, 1, 2, 0):
+            assert np.array_equal(dg.run(a, 7)[0], ep[a]), a
+    dg.close()
+
+
 def test_determinism_repeats(rst, O):
     g = O.gen("random", 1500, 0.002, seed=31)
     dg = dev_graph(rst, g)

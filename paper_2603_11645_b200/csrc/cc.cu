@@ -654,6 +654,19 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
   uint32_t* xlist = h.ws<uint32_t>(WS_HEADS, n + 1);
   unsigned long long* xcount = reinterpret_cast<unsigned long long*>(h.dev_box) + 5;
   int* flags = reinterpret_cast<int*>(h.dev_box + 6);  // 3 ints in dev_box[6..7]
+  // (host-side setup first, so that the zeroing and the tile pass launch
+  // back to back: the GPU otherwise idles between them)
+  const unsigned tiles = (unsigned)((n + kTileV - 1) / kTileV);
+  static int coop_blocks = 0;
+  ensure_dyn_smem((const void*)k_tile_resolve<kSrcApply>, kTileSmem);
+  ensure_dyn_smem((const void*)k_tile_resolve<kSrcRound0>, 3 * kTileSmem);
+  ensure_dyn_smem((const void*)k_tile_resolve<kSrcRound0Slot>, 3 * kTileSmem);
+  ensure_dyn_smem((const void*)k_tile_resolve<kSrcRep>, kTileSmem);
+  if (!coop_blocks) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jump_x, kBlock, 0));
+    coop_blocks = std::max(1, per_sm) * num_sms();
+  }
   {
     ZeroRanges z = extra ? *extra : ZeroRanges{};
     if (!extra) z.k = 0;
@@ -668,17 +681,6 @@ void resolve_round(Handle& h, int32_t* rep, int64_t n, int src, const RoundIO& i
     k_zero_ranges<<<(unsigned)std::min<int64_t>(1184, ((int64_t)most + 1023) / 1024), 1024, 0,
                     h.stream>>>(z);
     CK_LAUNCH();
-  }
-  const unsigned tiles = (unsigned)((n + kTileV - 1) / kTileV);
-  static int coop_blocks = 0;
-  ensure_dyn_smem((const void*)k_tile_resolve<kSrcApply>, kTileSmem);
-  ensure_dyn_smem((const void*)k_tile_resolve<kSrcRound0>, 3 * kTileSmem);
-  ensure_dyn_smem((const void*)k_tile_resolve<kSrcRound0Slot>, 3 * kTileSmem);
-  ensure_dyn_smem((const void*)k_tile_resolve<kSrcRep>, kTileSmem);
-  if (!coop_blocks) {
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jump_x, kBlock, 0));
-    coop_blocks = std::max(1, per_sm) * num_sms();
   }
   if (src == kSrcApply)
     k_tile_resolve<kSrcApply><<<tiles, kTileThreads, kTileSmem, h.stream>>>(n, rep, xbits, xlist,
@@ -933,8 +935,11 @@ void cc_reset_rounds(Handle& h) {
   // trees (RMAT-24: 219M of 260M), so its list costs more to write and to
   // gather from than a second full pass over the edge stream: start the
   // lists one round later there (RSTG_CC_FILTER_FROM overrides: 1 or 2).
-  const char* e = getenv("RSTG_CC_FILTER_FROM");
-  h.cc_filter_from = e ? std::max(1, atoi(e)) : (h.g.m > 4 * h.g.n ? 2 : 1);
+  static const int forced = [] {
+    const char* e = getenv("RSTG_CC_FILTER_FROM");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  h.cc_filter_from = forced ? forced : (h.g.m > 4 * h.g.n ? 2 : 1);
 }
 
 void launch_apply(Handle& h, int32_t* rep, unsigned long long* slot, uint8_t* tflag,
